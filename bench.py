@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""CountGauss T.X = G.(S.X) throughput on B200 (BASELINE.json metric), one JSON line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Workload (N=1 default): BASELINE config 2 -- dense X, n = 2^24 rows x d = 32 fp32,
+B = 65536 buckets, m = 64 -- the configuration the metric is quoted on (configs[1]).  A
+step is one countgauss_apply over the whole X; X (2.15 GB) is generated in HBM before the
+timed region and is larger than L2 (126 MB), so no L2 flush is needed.  For N > 1
+(torchrun, one process per GPU over NCCL) the rows are sharded contiguously ("strong"):
+each rank sketches its shard with the shared seed and the m x d partial Z's are summed
+with an NCCL all-reduce; time is the max over ranks.
+
+Reported beside `value` (device-resident X):
+  roofline      -- the sketch kernel (stage 1), CUDA events on its launch stream,
+                   algorithmic bytes n*d*4 + B*d*8 per launch vs MEASURED_PEAKS hbm_gbs;
+  e2e           -- the same metric through the C-ABI with X in pinned HOST memory
+                   (H2D of X and D2H of Z inside the timed region);
+  cpu_baseline  -- the reference's own countgauss_apply (oracle/_ref, compiled from the
+                   reference sources) on the box's host cores, full c2 in fp64.
+--impl reference times that CPU implementation alone (rank 0), as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CountGauss T·X throughput: nnz(X)/s and HBM GB/s at 1/2/4/8 B200 vs CPU ref"
+SEED = 12345  # CLI default seed (countgauss_main.cpp:46)
+
+CONFIGS = {
+    "c1": dict(kind="dense", n=65536, d=8, B=2048, m=16, dtype="f64"),
+    "c2": dict(kind="dense", n=1 << 24, d=32, B=65536, m=64, dtype="f32"),
+    "c3": dict(kind="csr", n=1 << 26, d=256, B=262144, m=128, density=0.01),
+    "c4": dict(kind="dense", n=1 << 25, d=128, B=131072, m=32, dtype="f32"),
+}
+
+
+def mix64(a, b):
+    M = (1 << 64) - 1
+    z = (a + 0x9E3779B97F4A7C15 + b * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def workload_name(cfg_name, c):
+    if c["kind"] == "dense":
+        return (f"{cfg_name}: dense X {c['n']}x{c['d']} {c['dtype']} row-major, CountGauss B={c['B']}, "
+                f"m={c['m']}")
+    return f"{cfg_name}: CSR X {c['n']}x{c['d']} Bernoulli({c['density']}) fp32/int32, B={c['B']}, m={c['m']}"
+
+
+def units_of(c, nnz=None):
+    return c["n"] * c["d"] if c["kind"] == "dense" else nnz
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU baseline (reference)
+def cpu_reference_run(cfg_name, c, steps, warmup):
+    """The reference's production countgauss_apply (OpenMP) on the host cores."""
+    import oracle
+
+    R = oracle.Reference()
+    O = oracle.Restatement()
+    threads = os.cpu_count() or 1
+    R.set_threads(threads)
+    cores = R.max_threads()
+    t_seed_rng = SEED
+    t0 = time.time()
+    xf = R.countgauss_new(c["m"], c["B"], c["n"], t_seed_rng)
+    construct_s = time.time() - t0
+    if c["kind"] != "dense":
+        raise SystemExit("cpu reference arm implemented for dense configs")
+    xm = R.dense_generated(c["n"], c["d"], mix64(SEED, 2), O)
+    ms, _ = xf.time_apply(xm, 1, max(1, steps + warmup - 1))
+    ms = list(ms)[warmup - 1:] if warmup > 1 else list(ms)
+    med = statistics.median(ms)
+    units = c["n"] * c["d"]
+    return dict(value=units / (med / 1e3), ms=ms, median_ms=med, cores=cores, construct_s=construct_s,
+                sample=(f"full {cfg_name}: countgauss_apply on fp64 column-major X (the reference layout), "
+                        f"{len(ms)} timed calls after warm-up, median; reference CSR/dense code as-is"))
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    c = CONFIGS[args.config]
+    r = cpu_reference_run(args.config, c, args.steps, args.warmup)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": r["value"], "unit": "nnz/s", "n_gpus": args.gpus,
+        "steps": len(r["ms"]), "warmup": args.warmup, "ms_per_step": r["median_ms"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config, c), "layout": "fp64 column-major (reference DenseMatrix)"},
+        "cpu_baseline": {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "reference",
+                         "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "construct_s": r["construct_s"],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_1606_05732_b200 as cg
+    from paper_1606_05732_b200 import bench_data
+    from paper_1606_05732_b200.distributed import shard_range
+
+    c = CONFIGS[args.config]
+    ctx = cg.context(local)
+    n, d, B, m = c["n"], c["d"], c["B"], c["m"]
+    r0, r1 = shard_range(n, world, rank)
+    rows = r1 - r0
+    t_seed = cg.SeededRng(SEED).next_u64()
+
+    # inputs in HBM
+    if c["kind"] == "dense":
+        dt = torch.float32 if c["dtype"] == "f32" else torch.float64
+        x = bench_data.dense_normal(rows, d, seed=mix64(SEED, 2), dtype=dt, row0=r0, device=local)
+        nnz_local = rows * d
+        x_bytes = rows * d * x.element_size()
+    else:
+        x = bench_data.csr_bernoulli(rows, d, c["density"], seed=mix64(SEED, 3) + r0, device=local)
+        nnz_local = x.nnz()
+        x_bytes = nnz_local * 8 + (rows + 1) * 8
+    torch.cuda.synchronize()
+
+    # transform construction (per-transform work, timed separately: the reference's
+    # countgauss_new is likewise outside countgauss_apply)
+    t0 = time.perf_counter()
+    t = cg.api.countgauss_new_shard(m, B, n, r0, rows, t_seed, ctx=ctx)
+    torch.cuda.synchronize()
+    construct_ms = (time.perf_counter() - t0) * 1e3
+
+    stream = torch.cuda.current_stream(dev)
+    z = torch.empty((d, m), dtype=torch.float64, device=dev).t()
+
+    def step():
+        zz = cg.api.countgauss_apply_into(t, x, z)
+        if world > 1:
+            dist.all_reduce(zz)
+        return zz
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.profile(True)
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = ctx.launches - launches0
+    elapsed_ms = ev0.elapsed_time(ev1)
+    sk_ms, sk_n = ctx.profile_read(0)
+    gm_ms, gm_n = ctx.profile_read(1)
+    ctx.profile(False)
+
+    tot_units = nnz_local
+    if world > 1:
+        tt = torch.tensor([elapsed_ms, float(nnz_local)], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        elapsed_ms = float(mx[0])
+        tot_units = float(sm[1])
+    ms_per_step = elapsed_ms / args.steps
+    value = tot_units / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (stage-1 sketch), per launch
+    peak, peak_kind = peaks()
+    bytes_alg = x_bytes + B * d * 8
+    sk_avg_ms = sk_ms / max(sk_n, 1)
+    achieved = bytes_alg / (sk_avg_ms / 1e3) / 1e9
+
+    # e2e: same call with X in pinned host memory (H2D + D2H inside the timed region)
+    e2e = None
+    if c["kind"] == "dense" and not args.no_e2e:
+        xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        xh.copy_(x)
+        zh = None
+        for _ in range(1):
+            zh = cg.countgauss_apply(t, xh.numpy())
+        if world > 1:
+            dist.barrier()
+        ts = []
+        k_e2e = max(1, min(args.steps, 5))
+        for _ in range(k_e2e):
+            a = time.perf_counter()
+            zh = cg.countgauss_apply(t, xh.numpy())  # synchronous: returns with Z on the host
+            if world > 1:
+                zt = torch.from_numpy(zh.copy()).to(dev)
+                dist.all_reduce(zt)
+                zh = zt.cpu().numpy()
+            ts.append(time.perf_counter() - a)
+        e_s = statistics.median(ts)
+        if world > 1:
+            tt = torch.tensor([e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_s = float(tt[0])
+        e2e = {"value": tot_units / e_s, "unit": "nnz/s", "h2d_bytes_per_step": int(x_bytes),
+               "d2h_bytes_per_step": int(m * d * 8), "ms_per_step": e_s * 1e3, "steps": k_e2e,
+               "how": "cgx_countgauss_apply_dense with x_mem=HOST (pinned), wall clock, median"}
+        del xh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and c["kind"] == "dense":
+        try:
+            r = cpu_reference_run(args.config, c, 1, 1)
+            cpu = {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "reference",
+                   "sample": r["sample"]}
+        except Exception as exc:  # reported, not fatal
+            cpu = {"value": None, "unit": "nnz/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": workload_name(args.config, c), "n": n, "d": d, "B": B, "m": m,
+                "rows_per_rank": rows, "parallelism": f"rows sharded x{world}" + (", NCCL all-reduce of Z" if world > 1 else ""),
+                "input_dtype": c.get("dtype", "f32"), "accumulate": "f64 (S.X and G.(S.X))",
+                "l2": f"inputs larger than L2 ({x_bytes / 1e9:.2f} GB X per rank), no flush",
+                "construct_ms": construct_ms,
+                "stage_ms": {"sketch": sk_avg_ms, "gemm_fused_G": gm_ms / max(gm_n, 1)},
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "sketch_dense_kernel (stage 1)",
+                         "bytes_per_launch": bytes_alg, "peak_source": peak_kind},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,173 @@
+/* cgx.h -- C-ABI of the B200-native CountGauss path (T.X = G.(S.X), arXiv 1606.05732).
+ *
+ * Drop-in boundary for the reference library's hot path
+ * (/root/reference/proj/include/countgauss/sketch.hpp:25-54, nmf.hpp:51-52).  The
+ * reference has no C ABI; each entry point below names the C++ symbol it replaces.
+ * Plain pointers and sizes only -- no C++ or torch types cross this boundary, and no
+ * exception escapes it: every function returns a CGX_* status and sets a thread-local
+ * message readable with cgx_last_error().  The C++ shim maps
+ * CGX_EINVAL to std::invalid_argument with the reference's own messages.
+ *
+ * Memory: every array argument carries a `mem` flag.  CGX_MEM_HOST arrays are ordinary
+ * (pageable or pinned) host memory and the call is synchronous, exactly like the
+ * reference.  CGX_MEM_DEVICE arrays are device pointers on the context's GPU; such a
+ * call is stream-ordered on `stream` (NULL = the context's own stream) and returns
+ * without waiting for the GPU when every array is device-resident.  Inputs are
+ * borrowed for the duration of the call; outputs are caller-owned.
+ *
+ * Threading: a context may be shared by threads (the reference's functions are called
+ * from inside OpenMP regions, distcheck.cpp:107-111); calls on one context serialize.
+ *
+ * Results: hashes, signs, per-row extremes and S.X are bit-identical to the reference
+ * (S.X accumulates every (bucket, column) in ascending row order, as sketch.cpp:52-113
+ * does, including the 8192-row chunked CSR branch).  G is the reference's
+ * SplitMix64 + Acklam/Halley quantile evaluated with CUDA's libm (tolerance parity),
+ * and Z = G.(S.X) is within a relative Frobenius tolerance of the reference.
+ */
+#ifndef CGX_H
+#define CGX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    CGX_OK = 0,
+    CGX_EINVAL = 1,  /* std::invalid_argument in the reference */
+    CGX_ENOMEM = 2,  /* device or pinned-host allocation failed */
+    CGX_ECUDA = 3,   /* CUDA runtime / launch error */
+    CGX_ENCCL = 4,   /* reserved: collective failure */
+    CGX_ERANGE = 5   /* std::length_error in the reference (size overflow) */
+};
+enum { CGX_F64 = 0, CGX_F32 = 1 };            /* value dtype */
+enum { CGX_I64 = 0, CGX_I32 = 1 };            /* CSR column-index dtype */
+enum { CGX_COL_MAJOR = 0, CGX_ROW_MAJOR = 1 }; /* dense layout */
+enum { CGX_MEM_HOST = 0, CGX_MEM_DEVICE = 1 };
+
+typedef struct cgx_ctx cgx_ctx;     /* one GPU: stream, scratch, counters */
+typedef struct cgx_xform cgx_xform; /* a CountSketch map, optionally with its Gaussian G */
+
+/* ---- library / context ------------------------------------------------------------- */
+const char* cgx_last_error(void);
+const char* cgx_version(void);
+int cgx_init(int device, cgx_ctx** out);
+int cgx_free(cgx_ctx* ctx);
+int cgx_synchronize(cgx_ctx* ctx, void* stream);
+/* Device allocations owned by the context's GPU (for callers without an allocator). */
+int cgx_device_alloc(cgx_ctx* ctx, size_t bytes, void** out);
+int cgx_device_free(cgx_ctx* ctx, void* p);
+int cgx_host_alloc(cgx_ctx* ctx, size_t bytes, void** out); /* pinned */
+int cgx_host_free(cgx_ctx* ctx, void* p);
+int cgx_memcpy(cgx_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream);
+
+/* ---- seed plumbing (pure host functions; rng.hpp:12-37) ---------------------------- */
+/* mix64(a, b)  -- include/countgauss/rng.hpp:12-17 */
+uint64_t cgx_mix64(uint64_t a, uint64_t b);
+/* draw k (0-based) of SeededRng(seed)  -- rng.hpp:31-37 */
+uint64_t cgx_rng_draw(uint64_t seed, uint64_t k);
+
+/* ---- construction ------------------------------------------------------------------- */
+/* countsketch_new(buckets, input_dim, rng)  -- sketch.cpp:12-28.  `map_seed` is the
+ * value the reference stores in map.seed, i.e. the caller's rng.next_u64(). */
+int cgx_countsketch_new(cgx_ctx* ctx, uint64_t map_seed, int64_t buckets, int64_t input_dim,
+                        cgx_xform** out);
+/* countsketch_injective(buckets, input_dim, rng)  -- sketch.cpp:30-50 (Fisher-Yates on
+ * the host: its hashes are not an index function of the seed). */
+int cgx_countsketch_injective(cgx_ctx* ctx, uint64_t map_seed, int64_t buckets, int64_t input_dim,
+                              cgx_xform** out);
+/* A hand-built CountSketchMap (CountSketchMap fields, sketch.hpp:15-21): hash[i] in
+ * [0, buckets), sign[i] in {-1, +1}. */
+int cgx_countsketch_explicit(cgx_ctx* ctx, int64_t buckets, int64_t input_dim, const int64_t* hash,
+                             const double* sign, int mem, cgx_xform** out);
+/* countgauss_new(m, buckets, input_dim, rng)  -- sketch.cpp:115-126.  `t_seed` is the
+ * caller's rng.next_u64() (the reference's t.seed); S and G derive from it.  The
+ * two-argument overload (sketch.cpp:128-130) is buckets = 5*m. */
+int cgx_countgauss_new(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
+                       cgx_xform** out);
+/* Row shard [row0, row0+rows) of the same transform (multi-GPU row sharding; no
+ * reference counterpart -- the paper's seed-sharing): hashes and signs
+ * are those of the shard's *global* rows, applied to an X holding only the shard's rows.
+ * Sum over shards of countsketch_apply == the full S.X up to fp reassociation. */
+int cgx_countgauss_new_shard(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
+                             int64_t row0, int64_t rows, cgx_xform** out);
+/* Attach G to a map: seeded (G column-major draw order of SeededRng(g_seed),
+ * matrix.cpp:199-207) or explicit (m x buckets, column-major). */
+int cgx_xform_set_gaussian_seeded(cgx_ctx* ctx, cgx_xform* xf, int64_t m, uint64_t g_seed);
+int cgx_xform_set_gaussian_explicit(cgx_ctx* ctx, cgx_xform* xf, int64_t m, const double* g, int mem);
+int cgx_xform_info(const cgx_xform* xf, uint64_t* t_seed, uint64_t* map_seed, uint64_t* g_seed,
+                   int64_t* m, int64_t* buckets, int64_t* input_dim);
+int cgx_xform_free(cgx_xform* xf);
+
+/* ---- materializers (the transform structs' public fields) -------------------------- */
+/* cs.hash / cs.sign  (sketch.hpp:18-19) */
+int cgx_fill_hash_sign(cgx_ctx* ctx, const cgx_xform* xf, int64_t* hash, double* sign, int mem,
+                       void* stream);
+/* g, m x buckets column-major  (sketch.hpp:45) */
+int cgx_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, int mem, void* stream);
+/* inverse_normal_cdf elementwise  (rng.hpp:62, rng.cpp:45-55); p outside (0,1) -> CGX_EINVAL */
+int cgx_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int mem,
+                           void* stream);
+
+/* ---- apply -------------------------------------------------------------------------- */
+/* countsketch_apply(map, DenseMatrix)  -- sketch.cpp:52-66.  X is n x d with leading
+ * dimension ld (elements) in `layout`; sx receives S.X, buckets x d, in `sx_layout`
+ * (CGX_COL_MAJOR = the reference DenseMatrix). */
+int cgx_countsketch_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype,
+                                int layout, int64_t ld, int64_t n, int64_t d, int x_mem, double* sx,
+                                int sx_layout, int sx_mem, void* stream);
+/* countsketch_apply(map, SparseMatrix)  -- sketch.cpp:68-113.  CSR with int64 row offsets
+ * (n+1), column indices (int32/int64, strictly increasing per row), values (f32/f64). */
+int cgx_countsketch_apply_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr,
+                              const void* cols, int idx_type, const void* vals, int dtype, int64_t n,
+                              int64_t d, int64_t nnz, int x_mem, double* sx, int sx_layout, int sx_mem,
+                              void* stream);
+/* countgauss_apply(t, DenseMatrix)  -- sketch.cpp:132-134.  z: m x d, column-major. */
+int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout,
+                               int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem,
+                               void* stream);
+/* countgauss_apply(t, SparseMatrix)  -- sketch.cpp:136-138. */
+int cgx_countgauss_apply_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols,
+                             int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
+                             int x_mem, double* z, int z_mem, void* stream);
+/* Stage 2 alone: z = G . sx  (gemm(t.g, SX), matrix.cpp:111-129) with G regenerated
+ * inside the kernel from the transform's seed (never materialized). */
+int cgx_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int sx_layout, int64_t d,
+                   int sx_mem, double* z, int z_mem, void* stream);
+/* Split-K piece of stage 2: z = G[:, b0:b1) . sx_rows, where sx_rows is the row-major
+ * (b1-b0) x d slice of S.X for buckets [b0, b1) (a reduce-scatter's output). */
+int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_rows, int64_t b0, int64_t b1,
+                         int64_t d, int sx_mem, double* z, int z_mem, void* stream);
+
+/* select_extremes(Z)  -- nmf.cpp:99-118: per row argmax/argmin of an m x d column-major
+ * Z, strict compares (ties to the lowest column), tie_rows = rows whose max or min is
+ * attained more than once.  amax/amin: m entries each (unsorted, per row). */
+int cgx_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d, int mem, int64_t* amax,
+                        int64_t* amin, int64_t* tie_rows, void* stream);
+
+/* ---- synthetic inputs (device generators; the oracle shares their definition) ------ */
+/* Dense n x d, entry (i,j) = fp32 N(0,1) quantile of draw i*d+j of SeededRng(seed)
+ * (oracle/cgoracle.c cgo_normal_f32); dtype F64 stores the exact widening. */
+int cgx_gen_dense_normal(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype,
+                         int layout, void* x_dev, void* stream); /* rows [row0, row0+n) */
+/* CSR n x d with Bernoulli(density) entries (int32 cols, fp32 N(0,1) values).  Call once
+ * with cols/vals NULL to get row offsets and *nnz_out, then again with buffers. */
+int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double density,
+                          int64_t* rowptr_dev, int32_t* cols_dev, float* vals_dev, int64_t* nnz_out,
+                          void* stream);
+
+/* ---- instrumentation ---------------------------------------------------------------- */
+/* Number of kernels this context has launched so far. */
+uint64_t cgx_launch_count(const cgx_ctx* ctx);
+/* When enabled, the sketch (stage 1) and gemm (stage 2) kernels of every apply are
+ * bracketed with CUDA events on their launch stream; cgx_profile_read synchronizes and
+ * returns total milliseconds and launches per stage (0 = sketch, 1 = gemm), then resets. */
+int cgx_profile_enable(cgx_ctx* ctx, int on);
+int cgx_profile_read(cgx_ctx* ctx, int stage, double* total_ms, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGX_H */

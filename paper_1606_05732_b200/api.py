@@ -1,0 +1,539 @@
+"""Python mirror of the reference's CountGauss API, running on the B200 through libcgx.
+
+Same names, argument meaning and error behaviour as the reference C++ library
+(``/root/reference/proj/include/countgauss/{rng,sketch,nmf}.hpp``):
+
+=====================================  ==============================================
+reference (C++)                        here
+=====================================  ==============================================
+``SeededRng`` (rng.hpp:23-59)          :class:`SeededRng` (host-side seed plumbing)
+``mix64`` (rng.hpp:12-17)              :func:`mix64`
+``inverse_normal_cdf`` (rng.hpp:62)    :func:`inverse_normal_cdf` (GPU kernel)
+``CountSketchMap`` (sketch.hpp:15-21)  :class:`CountSketchMap`
+``countsketch_new`` (sketch.cpp:12)    :func:`countsketch_new`
+``countsketch_injective`` (:30)        :func:`countsketch_injective`
+``countsketch_apply`` x2 (:52, :68)    :func:`countsketch_apply`
+``CountGaussTransform`` (:42-47)       :class:`CountGaussTransform`
+``countgauss_new`` x2 (:115, :128)     :func:`countgauss_new`
+``countgauss_apply`` x2 (:132, :136)   :func:`countgauss_apply`
+``cg_nmf`` x2 (nmf.cpp:141-153)        :func:`cg_nmf` -> :class:`AnchorSet`
+``SparseMatrix`` (matrix.hpp:45-61)    :class:`SparseMatrix`
+=====================================  ==============================================
+
+``std::invalid_argument`` surfaces as :class:`ValueError` with the reference's message.
+Dense matrices are numpy arrays (host; results come back as numpy, column-major like the
+reference's ``DenseMatrix``) or CUDA torch tensors (device-resident; results stay on the
+device, stream-ordered on torch's current stream).  Every computation runs in libcgx's
+sm_100a kernels; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from typing import Any, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import (CGX_COL_MAJOR, CGX_F32, CGX_F64, CGX_I32, CGX_I64, CGX_MEM_DEVICE, CGX_MEM_HOST,
+                   CGX_ROW_MAJOR, check, lib)
+
+GAMMA = 0x9E3779B97F4A7C15
+_MASK = (1 << 64) - 1
+
+
+# ----------------------------------------------------------------------------- RNG
+def mix64(a: int, b: int) -> int:
+    """Child-seed mixer (rng.hpp:12-17)."""
+    return int(lib.cgx_mix64(a & _MASK, b & _MASK))
+
+
+class SeededRng:
+    """SplitMix64 stream (rng.hpp:23-59).  Host-side: it only carries seeds into the GPU."""
+
+    kAlgorithm = "splitmix64/inverse-cdf-normal"
+
+    def __init__(self, seed: int):
+        self._seed = seed & _MASK
+        self._state = seed & _MASK
+
+    def seed(self) -> int:
+        return self._seed
+
+    def next_u64(self) -> int:
+        self._state = (self._state + GAMMA) & _MASK
+        z = self._state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK
+        return z ^ (z >> 31)
+
+    def next_uniform(self) -> float:
+        return ((self.next_u64() >> 11) + 0.5) * 2.0 ** -53
+
+    def next_below(self, bound: int) -> int:
+        return self.next_u64() % bound
+
+    def next_normal(self) -> float:
+        return inverse_normal_cdf(self.next_uniform())
+
+    def split(self) -> "SeededRng":
+        return SeededRng(self.next_u64())
+
+
+# ------------------------------------------------------------------------- context
+class Context:
+    """One GPU: a libcgx context (stream, scratch, launch counter)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.cgx_init(int(device), C.byref(h)))
+        self.h = h
+        self.device = int(device)
+
+    def close(self):
+        if self.h:
+            lib.cgx_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(lib.cgx_launch_count(self.h))
+
+    def synchronize(self, stream=None):
+        check(lib.cgx_synchronize(self.h, stream))
+
+    # profiling of stage 1 (sketch) / stage 2 (gemm) with CUDA events on the launch stream
+    def profile(self, on: bool = True):
+        check(lib.cgx_profile_enable(self.h, int(on)))
+
+    def profile_read(self, stage: int):
+        ms, n = C.c_double(), C.c_int64()
+        check(lib.cgx_profile_read(self.h, stage, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+
+_ctx_lock = threading.Lock()
+_contexts: dict[int, Context] = {}
+
+
+def context(device: Optional[int] = None) -> Context:
+    """The process-wide context of `device` (default: torch's current device, else 0)."""
+    if device is None:
+        device = 0
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                device = torch.cuda.current_device()
+        except ImportError:
+            pass
+    with _ctx_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = _contexts[device] = Context(device)
+        return ctx
+
+
+def inverse_normal_cdf(p: float) -> float:
+    """Standard normal quantile (rng.cpp:45-55), evaluated by the GPU kernel."""
+    a = np.array([p], np.float64)
+    out = np.empty(1, np.float64)
+    check(lib.cgx_inverse_normal_cdf(context().h, a.ctypes.data, out.ctypes.data, 1, CGX_MEM_HOST, None))
+    return float(out[0])
+
+
+def inverse_normal_cdf_array(p: np.ndarray) -> np.ndarray:
+    p = np.ascontiguousarray(p, np.float64)
+    out = np.empty_like(p)
+    check(lib.cgx_inverse_normal_cdf(context().h, p.ctypes.data, out.ctypes.data, p.size, CGX_MEM_HOST, None))
+    return out
+
+
+# ---------------------------------------------------------------------- transforms
+class _Xform:
+    """Owns one cgx_xform (freed when the last Python view goes away)."""
+
+    def __init__(self, ctx: Context, h: C.c_void_p):
+        self.ctx, self.h = ctx, h
+
+    def __del__(self):
+        try:
+            lib.cgx_xform_free(self.h)
+        except Exception:
+            pass
+
+    def info(self):
+        t, ms, gs = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        m, B, n = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.cgx_xform_info(self.h, C.byref(t), C.byref(ms), C.byref(gs), C.byref(m), C.byref(B),
+                                 C.byref(n)))
+        return dict(t_seed=t.value, map_seed=ms.value, g_seed=gs.value, m=m.value, B=B.value, n=n.value)
+
+
+class CountSketchMap:
+    """buckets x input_dim CountSketch (sketch.hpp:15-21).  ``hash``/``sign`` are
+    materialized from the GPU on first access; the apply kernels never need them."""
+
+    def __init__(self, xf: _Xform):
+        self._xf = xf
+        inf = xf.info()
+        self.buckets = inf["B"]
+        self.input_dim = inf["n"]
+        self.seed = inf["map_seed"]
+        self._hash = self._sign = None
+
+    @classmethod
+    def from_arrays(cls, buckets: int, hash_, sign, ctx: Optional[Context] = None) -> "CountSketchMap":
+        """A hand-built map (the reference fills the struct fields directly,
+        test_sketch.cpp:72-78)."""
+        ctx = ctx or context()
+        hash_ = np.ascontiguousarray(hash_, np.int64)
+        sign = np.ascontiguousarray(sign, np.float64)
+        if hash_.shape != sign.shape:
+            raise ValueError("countsketch map: hash and sign lengths differ")
+        h = C.c_void_p()
+        check(lib.cgx_countsketch_explicit(ctx.h, int(buckets), int(hash_.size), hash_.ctypes.data,
+                                           sign.ctypes.data, CGX_MEM_HOST, C.byref(h)))
+        return cls(_Xform(ctx, h))
+
+    def _materialize(self):
+        if self._hash is None:
+            h = np.empty(self.input_dim, np.int64)
+            s = np.empty(self.input_dim, np.float64)
+            check(lib.cgx_fill_hash_sign(self._xf.ctx.h, self._xf.h, h.ctypes.data, s.ctypes.data,
+                                         CGX_MEM_HOST, None))
+            self._hash, self._sign = h, s
+
+    @property
+    def hash(self) -> np.ndarray:
+        self._materialize()
+        return self._hash
+
+    @property
+    def sign(self) -> np.ndarray:
+        self._materialize()
+        return self._sign
+
+
+class CountGaussTransform:
+    """T = G.S with G m x buckets (sketch.hpp:42-47).  ``g`` is materialized on demand;
+    countgauss_apply regenerates G inside its GEMM instead."""
+
+    def __init__(self, xf: _Xform):
+        self._xf = xf
+        inf = xf.info()
+        self.cs = CountSketchMap(xf)
+        self.m = inf["m"]
+        self.seed = inf["t_seed"]
+        self._g = None
+
+    @property
+    def g(self) -> np.ndarray:
+        if self._g is None:
+            g = np.empty((self.cs.buckets, self.m), np.float64)  # col-major m x B
+            check(lib.cgx_fill_gaussian(self._xf.ctx.h, self._xf.h, g.ctypes.data, CGX_MEM_HOST, None))
+            self._g = g.T
+        return self._g
+
+
+def countsketch_new(buckets: int, input_dim: int, rng: SeededRng, ctx: Optional[Context] = None) -> CountSketchMap:
+    """sketch.cpp:12-28: map.seed = rng.next_u64(); hash/sign are index functions of it."""
+    if buckets < 1 or input_dim < 1:
+        raise ValueError("countsketch_new: buckets and input_dim must be >= 1")
+    ctx = ctx or context()
+    h = C.c_void_p()
+    check(lib.cgx_countsketch_new(ctx.h, rng.next_u64(), int(buckets), int(input_dim), C.byref(h)))
+    return CountSketchMap(_Xform(ctx, h))
+
+
+def countsketch_injective(buckets: int, input_dim: int, rng: SeededRng,
+                          ctx: Optional[Context] = None) -> CountSketchMap:
+    """sketch.cpp:30-50 (distinct buckets; requires buckets >= input_dim)."""
+    if buckets < input_dim:
+        raise ValueError("countsketch_injective: needs buckets >= input_dim")
+    ctx = ctx or context()
+    h = C.c_void_p()
+    check(lib.cgx_countsketch_injective(ctx.h, rng.next_u64(), int(buckets), int(input_dim), C.byref(h)))
+    return CountSketchMap(_Xform(ctx, h))
+
+
+def countgauss_new(m: int, *args, ctx: Optional[Context] = None) -> CountGaussTransform:
+    """``countgauss_new(m, buckets, input_dim, rng)`` (sketch.cpp:115-126) or
+    ``countgauss_new(m, input_dim, rng)`` with buckets = 5m (sketch.cpp:128-130)."""
+    if len(args) == 3:
+        buckets, input_dim, rng = args
+    elif len(args) == 2:
+        input_dim, rng = args
+        buckets = 5 * m
+    else:
+        raise TypeError("countgauss_new(m, buckets, input_dim, rng) or countgauss_new(m, input_dim, rng)")
+    if m < 1 or buckets < 1 or input_dim < 1:
+        raise ValueError("countgauss_new: m, buckets and input_dim must be >= 1")
+    ctx = ctx or context()
+    h = C.c_void_p()
+    check(lib.cgx_countgauss_new(ctx.h, rng.next_u64(), int(m), int(buckets), int(input_dim), C.byref(h)))
+    return CountGaussTransform(_Xform(ctx, h))
+
+
+def countgauss_new_shard(m: int, buckets: int, input_dim: int, row0: int, rows: int, t_seed: int,
+                         ctx: Optional[Context] = None) -> CountGaussTransform:
+    """Rows [row0, row0+rows) of the transform countgauss_new(m, buckets, input_dim, .)
+    whose t.seed is `t_seed` (multi-GPU row sharding: every rank derives S and G from the
+    shared seed -- the paper's seed sharing)."""
+    if m < 1 or buckets < 1 or input_dim < 1:
+        raise ValueError("countgauss_new: m, buckets and input_dim must be >= 1")
+    ctx = ctx or context()
+    h = C.c_void_p()
+    check(lib.cgx_countgauss_new_shard(ctx.h, t_seed & _MASK, int(m), int(buckets), int(input_dim), int(row0),
+                                       int(rows), C.byref(h)))
+    return CountGaussTransform(_Xform(ctx, h))
+
+
+# ------------------------------------------------------------------------ matrices
+@dataclass
+class SparseMatrix:
+    """CSR matrix (matrix.hpp:45-61): int64 row offsets, column indices strictly
+    increasing per row (int64 or int32), values (float64 or float32).  Arrays may be
+    numpy (host) or CUDA torch tensors (device)."""
+
+    rows: int
+    cols: int
+    row_offsets: Any
+    col_indices: Any
+    values: Any
+
+    def nnz(self) -> int:
+        return int(self.values.shape[0])
+
+    @staticmethod
+    def from_dense(x: np.ndarray, drop_tol: float = 0.0) -> "SparseMatrix":
+        """SparseMatrix::from_dense (matrix.cpp:69-84)."""
+        x = np.asarray(x, np.float64)
+        mask = np.abs(x) > drop_tol
+        rows, cols = np.nonzero(mask)
+        counts = np.bincount(rows, minlength=x.shape[0])
+        rp = np.zeros(x.shape[0] + 1, np.int64)
+        np.cumsum(counts, out=rp[1:])
+        return SparseMatrix(x.shape[0], x.shape[1], rp, cols.astype(np.int64), x[rows, cols])
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.rows, self.cols), np.float64, order="F")
+        rp = np.asarray(self.row_offsets)
+        r = np.repeat(np.arange(self.rows), np.diff(rp))
+        out[r, np.asarray(self.col_indices)] = np.asarray(self.values)
+        return out
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _stream_of(x):
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+
+
+def _dense_args(x):
+    """(ptr, dtype, layout, ld, n, d, mem, keepalive, is_torch)."""
+    if _is_torch(x):
+        import torch
+
+        if x.dim() != 2:
+            raise ValueError("countsketch_apply: X must be a matrix")
+        if x.dtype not in (torch.float32, torch.float64):
+            x = x.to(torch.float64)
+        if not x.is_cuda:
+            x = x.numpy()
+            return _dense_args(x)
+        n, d = x.shape
+        es = x.element_size()
+        if x.stride(1) == 1 and (x.stride(0) >= max(d, 1) or n <= 1):
+            layout, ld = CGX_ROW_MAJOR, max(x.stride(0), d, 1)
+        elif x.stride(0) == 1 and (x.stride(1) >= max(n, 1) or d <= 1):
+            layout, ld = CGX_COL_MAJOR, max(x.stride(1), n, 1)
+        else:
+            x = x.contiguous()
+            layout, ld = CGX_ROW_MAJOR, max(d, 1)
+        dt = CGX_F32 if x.dtype == torch.float32 else CGX_F64
+        del es
+        return x.data_ptr(), dt, layout, ld, n, d, CGX_MEM_DEVICE, x, True
+    x = np.asarray(x)
+    if x.ndim != 2:
+        raise ValueError("countsketch_apply: X must be a matrix")
+    if x.dtype not in (np.float32, np.float64):
+        x = x.astype(np.float64)
+    n, d = x.shape
+    if x.flags.c_contiguous:
+        layout, ld = CGX_ROW_MAJOR, max(d, 1)
+    elif x.flags.f_contiguous:
+        layout, ld = CGX_COL_MAJOR, max(n, 1)
+    else:
+        x = np.ascontiguousarray(x)
+        layout, ld = CGX_ROW_MAJOR, max(d, 1)
+    dt = CGX_F32 if x.dtype == np.float32 else CGX_F64
+    return x.ctypes.data, dt, layout, ld, n, d, CGX_MEM_HOST, x, False
+
+
+def _csr_args(x: SparseMatrix):
+    if _is_torch(x.values) and x.values.is_cuda:
+        import torch
+
+        rp = x.row_offsets.to(torch.int64).contiguous()
+        ci = x.col_indices
+        if ci.dtype not in (torch.int32, torch.int64):
+            ci = ci.to(torch.int64)
+        ci = ci.contiguous()
+        v = x.values
+        if v.dtype not in (torch.float32, torch.float64):
+            v = v.to(torch.float64)
+        v = v.contiguous()
+        return (rp.data_ptr(), ci.data_ptr(), CGX_I32 if ci.dtype == torch.int32 else CGX_I64, v.data_ptr(),
+                CGX_F32 if v.dtype == torch.float32 else CGX_F64, CGX_MEM_DEVICE, (rp, ci, v), True)
+    rp = np.ascontiguousarray(np.asarray(x.row_offsets), np.int64)
+    ci = np.asarray(x.col_indices)
+    if ci.dtype not in (np.int32, np.int64):
+        ci = ci.astype(np.int64)
+    ci = np.ascontiguousarray(ci)
+    v = np.asarray(x.values)
+    if v.dtype not in (np.float32, np.float64):
+        v = v.astype(np.float64)
+    v = np.ascontiguousarray(v)
+    if rp.shape[0] != x.rows + 1:
+        raise ValueError("SparseMatrix: row_offsets length must be rows+1")
+    return (rp.ctypes.data, ci.ctypes.data, CGX_I32 if ci.dtype == np.int32 else CGX_I64, v.ctypes.data,
+            CGX_F32 if v.dtype == np.float32 else CGX_F64, CGX_MEM_HOST, (rp, ci, v), False)
+
+
+def _out(rows: int, cols: int, on_device: bool, like=None):
+    """Column-major rows x cols float64 result (numpy F-order or a transposed torch view)."""
+    if on_device:
+        import torch
+
+        buf = torch.empty((cols, rows), dtype=torch.float64, device=like.device)
+        return buf.t(), buf.data_ptr()
+    arr = np.empty((rows, cols), np.float64, order="F")
+    return arr, arr.ctypes.data
+
+
+def countsketch_apply(cs: CountSketchMap, x):
+    """S.X (sketch.cpp:52-113): buckets x d, bit-identical to the reference."""
+    if isinstance(cs, CountGaussTransform):
+        cs = cs.cs
+    xf = cs._xf
+    if isinstance(x, SparseMatrix):
+        rp, ci, it, v, dt, mem, keep, dev = _csr_args(x)
+        out, optr = _out(cs.buckets, x.cols, dev, x.values)
+        check(lib.cgx_countsketch_apply_csr(xf.ctx.h, xf.h, rp, ci, it, v, dt, x.rows, x.cols, x.nnz(), mem,
+                                            optr, CGX_COL_MAJOR, mem, _stream_of(x.values) if dev else None))
+        return out
+    ptr, dt, layout, ld, n, d, mem, keep, dev = _dense_args(x)
+    out, optr = _out(cs.buckets, d, dev, keep)
+    check(lib.cgx_countsketch_apply_dense(xf.ctx.h, xf.h, ptr, dt, layout, ld, n, d, mem, optr, CGX_COL_MAJOR, mem,
+                                          _stream_of(keep) if dev else None))
+    return out
+
+
+def countgauss_apply(t: CountGaussTransform, x):
+    """Z = G.(S.X) (sketch.cpp:132-138): m x d."""
+    xf = t._xf
+    if isinstance(x, SparseMatrix):
+        rp, ci, it, v, dt, mem, keep, dev = _csr_args(x)
+        out, optr = _out(t.m, x.cols, dev, x.values)
+        check(lib.cgx_countgauss_apply_csr(xf.ctx.h, xf.h, rp, ci, it, v, dt, x.rows, x.cols, x.nnz(), mem, optr,
+                                           mem, _stream_of(x.values) if dev else None))
+        return out
+    ptr, dt, layout, ld, n, d, mem, keep, dev = _dense_args(x)
+    out, optr = _out(t.m, d, dev, keep)
+    check(lib.cgx_countgauss_apply_dense(xf.ctx.h, xf.h, ptr, dt, layout, ld, n, d, mem, optr, mem,
+                                         _stream_of(keep) if dev else None))
+    return out
+
+
+def countgauss_apply_into(t: CountGaussTransform, x, z):
+    """Device-resident countgauss_apply writing into a preallocated column-major m x d
+    CUDA tensor `z` (e.g. ``torch.empty((d, m)).t()``) -- no allocation per call."""
+    xf = t._xf
+    assert z.stride(0) == 1 and z.shape[0] == t.m, "z must be column-major m x d"
+    if isinstance(x, SparseMatrix):
+        rp, ci, it, v, dt, mem, keep, dev = _csr_args(x)
+        if not dev:
+            raise ValueError("countgauss_apply_into: device inputs only")
+        check(lib.cgx_countgauss_apply_csr(xf.ctx.h, xf.h, rp, ci, it, v, dt, x.rows, x.cols, x.nnz(), mem,
+                                           z.data_ptr(), CGX_MEM_DEVICE, _stream_of(x.values)))
+        return z
+    ptr, dt, layout, ld, n, d, mem, keep, dev = _dense_args(x)
+    if not dev:
+        raise ValueError("countgauss_apply_into: device inputs only")
+    check(lib.cgx_countgauss_apply_dense(xf.ctx.h, xf.h, ptr, dt, layout, ld, n, d, mem, z.data_ptr(),
+                                         CGX_MEM_DEVICE, _stream_of(keep)))
+    return z
+
+
+# --------------------------------------------------------------------------- NMF
+@dataclass
+class AnchorSet:
+    """nmf.hpp:38-46."""
+
+    i_max: list = field(default_factory=list)
+    i_min: list = field(default_factory=list)
+    unioned: list = field(default_factory=list)
+    tie_rows: int = 0
+
+    def contains_all(self, wanted) -> bool:
+        return all(w in self.unioned for w in wanted)
+
+    def subset_of(self, allowed) -> bool:
+        allowed = set(allowed)
+        return all(u in allowed for u in self.unioned)
+
+
+def select_extremes(z, ctx: Optional[Context] = None) -> AnchorSet:
+    """Per-row argmax/argmin of Z (nmf.cpp:99-132) on the GPU; sorted-unique sets."""
+    ctx = ctx or context()
+    if _is_torch(z) and z.is_cuda:
+        zz = z.t().contiguous().t() if not (z.stride(0) == 1) else z  # column-major
+        m, d = zz.shape
+        import torch
+
+        amax = torch.empty(m, dtype=torch.int64, device=z.device)
+        amin = torch.empty(m, dtype=torch.int64, device=z.device)
+        ties = C.c_int64()
+        check(lib.cgx_select_extremes(ctx.h, zz.data_ptr(), m, d, CGX_MEM_DEVICE, amax.data_ptr(), amin.data_ptr(),
+                                      C.byref(ties), _stream_of(z)))
+        amax, amin = amax.cpu().numpy(), amin.cpu().numpy()
+    else:
+        zz = np.asfortranarray(z, np.float64)
+        m, d = zz.shape
+        amax = np.empty(m, np.int64)
+        amin = np.empty(m, np.int64)
+        ties = C.c_int64()
+        check(lib.cgx_select_extremes(ctx.h, zz.ctypes.data, m, d, CGX_MEM_HOST, amax.ctypes.data, amin.ctypes.data,
+                                      C.byref(ties), None))
+    i_max = sorted(set(int(a) for a in amax))
+    i_min = sorted(set(int(a) for a in amin))
+    return AnchorSet(i_max, i_min, sorted(set(i_max) | set(i_min)), int(ties.value))
+
+
+def cg_nmf(x, m: int, buckets: int, rng: SeededRng, ctx: Optional[Context] = None) -> AnchorSet:
+    """CountGauss anchor extraction (nmf.cpp:141-153): Z = G.(S.X) with a fresh transform
+    from rng, then per-row extremes.  buckets < 1 selects 5m."""
+    if isinstance(x, SparseMatrix):
+        n, d = x.rows, x.cols
+    else:
+        n, d = x.shape
+    if m < 1:
+        raise ValueError("anchor extraction: m must be >= 1")
+    if d < 1:
+        raise ValueError("anchor extraction: X must have at least one column")
+    if buckets < 1:
+        buckets = 5 * m
+    t = countgauss_new(m, buckets, n, rng, ctx=ctx)
+    return select_extremes(countgauss_apply(t, x), ctx=t._xf.ctx)

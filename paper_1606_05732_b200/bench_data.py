@@ -1,0 +1,55 @@
+"""Seeded synthetic inputs for the BASELINE configs, generated directly in HBM by libcgx's
+generator kernels (csrc/datagen.cu) into torch-allocated device tensors.
+
+The reference measures on no public dataset (BASELINE.json "published": {}); these
+stand in with the configs' shapes and value distributions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import CGX_F32, CGX_F64, CGX_ROW_MAJOR, CGX_COL_MAJOR, check, lib
+from .api import context
+
+
+def dense_normal(n: int, d: int, seed: int, dtype=None, layout: str = "row", device=None, row0: int = 0):
+    """Rows [row0, row0+n) of an N(0,1) matrix with d columns (fp32 quantiles of
+    SplitMix64 uniforms, entry (i, j) = draw i*d + j), row- or column-major."""
+    import torch
+
+    dtype = dtype or torch.float32
+    ctx = context(device)
+    dev = torch.device("cuda", ctx.device)
+    if layout == "row":
+        x = torch.empty((n, d), dtype=dtype, device=dev)
+        lay = CGX_ROW_MAJOR
+    else:
+        x = torch.empty((d, n), dtype=dtype, device=dev).t()
+        lay = CGX_COL_MAJOR
+    dt = CGX_F32 if dtype == torch.float32 else CGX_F64
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    check(lib.cgx_gen_dense_normal(ctx.h, seed, row0, n, d, dt, lay, x.data_ptr(), stream))
+    return x
+
+
+def csr_bernoulli(n: int, d: int, density: float, seed: int, device=None):
+    """CSR n x d, each entry present with probability `density` (sorted distinct columns,
+    int32 columns, fp32 N(0,1) values, int64 row offsets).  Returns a SparseMatrix of
+    device tensors."""
+    import torch
+
+    from .api import SparseMatrix
+
+    ctx = context(device)
+    dev = torch.device("cuda", ctx.device)
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    nnz = C.c_int64()
+    check(lib.cgx_gen_csr_bernoulli(ctx.h, seed, n, d, density, rp.data_ptr(), None, None, C.byref(nnz), stream))
+    cols = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)[: nnz.value]
+    vals = torch.empty(max(nnz.value, 1), dtype=torch.float32, device=dev)[: nnz.value]
+    check(lib.cgx_gen_csr_bernoulli(ctx.h, seed, n, d, density, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+                                    None, stream))
+    return SparseMatrix(n, d, rp, cols, vals)

@@ -1,0 +1,788 @@
+// capi.cu -- the cgx C-ABI (include/cgx.h): contexts, transforms, argument checking that
+// mirrors the reference's std::invalid_argument cases, host<->device staging, and the
+// stage-1 / stage-2 dispatch.  No exception crosses the extern "C" boundary.
+#include "common.cuh"
+#include "internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace cgx {
+
+namespace {
+thread_local std::string g_err;
+}
+
+void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        fail(CGX_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    fail(CGX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void check_launch(const char* what) { check_cuda(cudaGetLastError(), what); }
+
+void* DevBuf::get(size_t need) {
+    if (need == 0) need = 1;
+    if (need <= bytes) return p;
+    if (p) CGX_CUDA(cudaFree(p));  // synchronizes: no in-flight user of the old buffer
+    p = nullptr;
+    bytes = 0;
+    const size_t want = need + need / 8;
+    CGX_CUDA(cudaMalloc(&p, want));
+    bytes = want;
+    return p;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+void Profile::begin(int stage, cudaStream_t s) {
+    if (!on) return;
+    auto& v = ev[stage];
+    if (used[stage] == v.size()) {
+        cudaEvent_t a, b;
+        CGX_CUDA(cudaEventCreate(&a));
+        CGX_CUDA(cudaEventCreate(&b));
+        v.push_back({a, b});
+    }
+    CGX_CUDA(cudaEventRecord(v[used[stage]].first, s));
+}
+
+void Profile::end(int stage, cudaStream_t s) {
+    if (!on) return;
+    CGX_CUDA(cudaEventRecord(ev[stage][used[stage]].second, s));
+    ++used[stage];
+}
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return CGX_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return CGX_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CGX_ECUDA;
+    }
+}
+
+// Serializes a call on its context, binds the device and orders the call's stream after
+// the previous call (which may have used the same scratch on another stream).
+struct CallScope {
+    cgx_ctx* ctx;
+    cudaStream_t st;
+    std::lock_guard<std::recursive_mutex> lock;
+    CallScope(cgx_ctx* c, void* stream) : ctx(c), st(stream ? (cudaStream_t)stream : c->stream), lock(c->mu) {
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        CGX_CUDA(cudaStreamWaitEvent(st, ctx->done, 0));
+    }
+    ~CallScope() { cudaEventRecord(ctx->done, st); }
+    void sync() { CGX_CUDA(cudaStreamSynchronize(st)); }
+};
+
+void need_ctx(cgx_ctx* ctx) {
+    if (!ctx) fail(CGX_EINVAL, "cgx: null context");
+}
+void need_xf(const cgx_xform* xf) {
+    if (!xf) fail(CGX_EINVAL, "cgx: null transform");
+}
+void need_mem(int mem) {
+    if (mem != CGX_MEM_HOST && mem != CGX_MEM_DEVICE) fail(CGX_EINVAL, "cgx: mem must be CGX_MEM_HOST or CGX_MEM_DEVICE");
+}
+size_t dsize(int dtype) {
+    if (dtype == CGX_F32) return 4;
+    if (dtype == CGX_F64) return 8;
+    fail(CGX_EINVAL, "cgx: dtype must be CGX_F32 or CGX_F64");
+}
+
+// A device view of a (possibly host) input array; host arrays land in `buf`.
+const void* to_device(cgx_ctx* ctx, DevBuf& buf, const void* p, size_t bytes, int mem, cudaStream_t s) {
+    if (mem == CGX_MEM_DEVICE || bytes == 0) return p;
+    void* d = buf.get(bytes);
+    CGX_CUDA(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, s));
+    return d;
+}
+
+cgx_xform* new_xform(cgx_ctx* ctx, int64_t B, int64_t n) {
+    if (n >= ((int64_t)1 << 31))
+        fail(CGX_EINVAL, "cgx: input_dim must be < 2^31 on the GPU path (perm entries are 31-bit row indices)");
+    if (B >= ((int64_t)1 << 31)) fail(CGX_EINVAL, "cgx: buckets must be < 2^31 on the GPU path");
+    auto* xf = new cgx_xform;
+    xf->ctx = ctx;
+    xf->B = B;
+    xf->n = n;
+    try {
+        CGX_CUDA(cudaMalloc((void**)&xf->perm, sizeof(uint32_t) * (size_t)n));
+        CGX_CUDA(cudaMalloc((void**)&xf->offsets, sizeof(uint32_t) * (size_t)(B + 1)));
+    } catch (...) {
+        if (xf->perm) cudaFree(xf->perm);
+        delete xf;
+        throw;
+    }
+    return xf;
+}
+
+void free_xform(cgx_xform* xf) {
+    if (!xf) return;
+    if (xf->ctx) cudaSetDevice(xf->ctx->device);
+    if (xf->perm) cudaFree(xf->perm);
+    if (xf->offsets) cudaFree(xf->offsets);
+    if (xf->g_dev) cudaFree(xf->g_dev);
+    delete xf;
+}
+
+// The reference's chunked-CSR branch condition (sketch.cpp:74-82).
+int64_t csr_chunk_rows(int64_t n, int64_t B, int64_t d) {
+    const int64_t chunk_rows = 8192;
+    const int64_t n_chunks = (n + chunk_rows - 1) / chunk_rows;
+    const int64_t out_size = B * d;
+    const bool chunked = n_chunks > 1 && out_size <= ((int64_t)1 << 16) && n_chunks * out_size <= ((int64_t)1 << 25);
+    return chunked ? chunk_rows : 0;
+}
+
+// Stage 1 (dense): SX row-major (B x d) into `sx_dev`.
+void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
+                      int64_t n, int64_t d, int x_mem, double* sx_dev, cudaStream_t s) {
+    const size_t es = dsize(dtype);
+    if (layout != CGX_COL_MAJOR && layout != CGX_ROW_MAJOR) fail(CGX_EINVAL, "cgx: bad layout");
+    if (n != xf->n)
+        fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
+                             std::to_string(xf->n));
+    if (d < 0) fail(CGX_EINVAL, "cgx: negative column count");
+    const int64_t minld = layout == CGX_COL_MAJOR ? n : d;
+    if (ld < std::max<int64_t>(minld, 1)) fail(CGX_EINVAL, "cgx: leading dimension too small");
+    const size_t bytes = layout == CGX_COL_MAJOR ? es * (size_t)(ld * (d ? d - 1 : 0) + n) : es * (size_t)(ld * (n - 1) + d);
+    const void* xd = to_device(ctx, ctx->hstage_dev, x, d ? bytes : 0, x_mem, s);
+    int64_t rld = ld;
+    if (layout == CGX_COL_MAJOR && d > 0) {
+        void* rm = ctx->xstage.get(es * (size_t)(n * d));
+        launch_transpose_x(ctx, xd, dtype, ld, n, d, rm, s);
+        xd = rm;
+        rld = d;
+    }
+    if (d == 0) return;
+    ctx->prof.begin(0, s);
+    launch_sketch_dense(ctx, xf, xd, dtype, rld, n, d, sx_dev, s);
+    ctx->prof.end(0, s);
+}
+
+void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
+                    const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem, double* sx_dev,
+                    cudaStream_t s) {
+    const size_t es = dsize(dtype);
+    if (idx_type != CGX_I32 && idx_type != CGX_I64) fail(CGX_EINVAL, "cgx: idx_type must be CGX_I32 or CGX_I64");
+    if (n != xf->n)
+        fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
+                             std::to_string(xf->n));
+    if (d < 0 || nnz < 0) fail(CGX_EINVAL, "cgx: negative size");
+    if (d >= ((int64_t)1 << 26)) fail(CGX_EINVAL, "cgx: CSR column count must be < 2^26 on the GPU path");
+    if (d == 0) return;
+    const size_t is = idx_type == CGX_I32 ? 4 : 8;
+    DevBuf& b0 = ctx->hstage_dev;
+    // host inputs: one staging allocation, three regions
+    const void* rp = rowptr;
+    const void* cp = cols;
+    const void* vp = vals;
+    if (x_mem == CGX_MEM_HOST) {
+        const size_t r_b = sizeof(int64_t) * (size_t)(n + 1), c_b = is * (size_t)nnz, v_b = es * (size_t)nnz;
+        const size_t a = 256;
+        const size_t off_c = (r_b + a - 1) / a * a, off_v = off_c + (c_b + a - 1) / a * a;
+        char* base = (char*)b0.get(off_v + v_b);
+        CGX_CUDA(cudaMemcpyAsync(base, rowptr, r_b, cudaMemcpyHostToDevice, s));
+        if (c_b) CGX_CUDA(cudaMemcpyAsync(base + off_c, cols, c_b, cudaMemcpyHostToDevice, s));
+        if (v_b) CGX_CUDA(cudaMemcpyAsync(base + off_v, vals, v_b, cudaMemcpyHostToDevice, s));
+        rp = base;
+        cp = base + off_c;
+        vp = base + off_v;
+    }
+    ctx->prof.begin(0, s);
+    launch_sketch_csr(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, sx_dev,
+                      csr_chunk_rows(n, xf->B, d), s);
+    ctx->prof.end(0, s);
+}
+
+void need_g(const cgx_xform* xf) {
+    if (!xf->has_g) fail(CGX_EINVAL, "countgauss_apply: transform has no Gaussian factor (use countgauss_new)");
+}
+
+// Stage 2 + output placement.
+void finish_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_dev, int64_t d, double* z, int z_mem,
+                 CallScope& sc, int64_t b0 = 0, int64_t b1 = -1) {
+    const size_t zb = sizeof(double) * (size_t)(xf->m * d);
+    if (d == 0) return;
+    if (b1 < 0) b1 = xf->B;
+    double* zd = z;
+    if (z_mem == CGX_MEM_HOST) zd = (double*)ctx->tmp.get(zb);  // tmp is free again after the scans
+    ctx->prof.begin(1, sc.st);
+    launch_gauss_gemm(ctx, xf, sx_dev, b0, b1, d, zd, sc.st);
+    ctx->prof.end(1, sc.st);
+    if (z_mem == CGX_MEM_HOST) {
+        CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
+        sc.sync();
+    }
+}
+
+void place_sx(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_dev, int64_t d, double* sx, int sx_layout, int sx_mem,
+              CallScope& sc) {
+    const size_t bytes = sizeof(double) * (size_t)(xf->B * d);
+    if (d == 0) return;
+    const double* src = sx_dev;
+    if (sx_layout == CGX_COL_MAJOR) {
+        double* dst = sx_mem == CGX_MEM_DEVICE ? sx : (double*)ctx->zpart.get(bytes);
+        launch_transpose_sx(ctx, sx_dev, xf->B, d, dst, sc.st);
+        src = dst;
+        if (sx_mem == CGX_MEM_DEVICE) return;
+    } else if (sx_layout != CGX_ROW_MAJOR) {
+        fail(CGX_EINVAL, "cgx: bad sx layout");
+    } else if (sx_mem == CGX_MEM_DEVICE) {
+        if (src != sx) CGX_CUDA(cudaMemcpyAsync(sx, src, bytes, cudaMemcpyDeviceToDevice, sc.st));
+        return;
+    }
+    CGX_CUDA(cudaMemcpyAsync(sx, src, bytes, cudaMemcpyDeviceToHost, sc.st));
+    sc.sync();
+}
+
+void build_explicit(cgx_ctx* ctx, cgx_xform* xf, const int64_t* hash, const double* sign, int mem, CallScope& sc) {
+    const int64_t n = xf->n;
+    const int64_t* hd = (const int64_t*)to_device(ctx, ctx->hstage_dev, hash, sizeof(int64_t) * (size_t)n, mem, sc.st);
+    const double* sd = (const double*)to_device(ctx, ctx->xstage, sign, sizeof(double) * (size_t)n, mem, sc.st);
+    uint32_t* keys = (uint32_t*)ctx->sx.get(sizeof(uint32_t) * (size_t)n * 2);
+    uint32_t* vals = keys + n;
+    if (!prep_explicit(ctx, hd, sd, n, xf->B, keys, vals, sc.st))
+        fail(CGX_EINVAL, "countsketch map: hash must lie in [0, buckets) and sign in {-1, +1}");
+    xf->seeded_map = false;
+    build_perm_explicit(ctx, xf, keys, vals, sc.st);
+    sc.sync();
+}
+
+} // namespace
+} // namespace cgx
+
+using namespace cgx;
+
+extern "C" {
+
+const char* cgx_last_error(void) { return g_err.c_str(); }
+const char* cgx_version(void) { return "cgx 0.1 (sm_100a)"; }
+
+int cgx_init(int device, cgx_ctx** out) {
+    return guard([&] {
+        if (!out) fail(CGX_EINVAL, "cgx_init: null out");
+        int count = 0;
+        CGX_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) fail(CGX_EINVAL, "cgx_init: no such device");
+        CGX_CUDA(cudaSetDevice(device));
+        auto* ctx = new cgx_ctx;
+        ctx->device = device;
+        CGX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+        CGX_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        CGX_CUDA(cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming));
+        CGX_CUDA(cudaEventRecord(ctx->done, ctx->stream));
+        *out = ctx;
+    });
+}
+
+int cgx_free(cgx_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaDeviceSynchronize();
+        for (DevBuf* b : {&ctx->sx, &ctx->zpart, &ctx->xstage, &ctx->tmp, &ctx->sort_k[0], &ctx->sort_k[1],
+                          &ctx->sort_v[0], &ctx->sort_v[1], &ctx->sort_hist, &ctx->counts, &ctx->hstage_dev})
+            b->release();
+        if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        for (int s = 0; s < 2; ++s)
+            for (auto& e : ctx->prof.ev[s]) {
+                cudaEventDestroy(e.first);
+                cudaEventDestroy(e.second);
+            }
+        cudaEventDestroy(ctx->done);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int cgx_synchronize(cgx_ctx* ctx, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        CGX_CUDA(cudaStreamSynchronize(stream ? (cudaStream_t)stream : ctx->stream));
+    });
+}
+
+int cgx_device_alloc(cgx_ctx* ctx, size_t bytes, void** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        CGX_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+    });
+}
+int cgx_device_free(cgx_ctx* ctx, void* p) {
+    return guard([&] {
+        need_ctx(ctx);
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        CGX_CUDA(cudaFree(p));
+    });
+}
+int cgx_host_alloc(cgx_ctx* ctx, size_t bytes, void** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        CGX_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+    });
+}
+int cgx_host_free(cgx_ctx* ctx, void* p) {
+    return guard([&] {
+        need_ctx(ctx);
+        CGX_CUDA(cudaFreeHost(p));
+    });
+}
+int cgx_memcpy(cgx_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        CallScope sc(ctx, stream);
+        CGX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, sc.st));
+        sc.sync();
+    });
+}
+
+uint64_t cgx_mix64(uint64_t a, uint64_t b) { return mix64(a, b); }
+uint64_t cgx_rng_draw(uint64_t seed, uint64_t k) { return rng_draw(seed, k); }
+
+int cgx_countsketch_new(cgx_ctx* ctx, uint64_t map_seed, int64_t buckets, int64_t input_dim, cgx_xform** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (buckets < 1 || input_dim < 1)
+            fail(CGX_EINVAL, "countsketch_new: buckets and input_dim must be >= 1");
+        CallScope sc(ctx, nullptr);
+        cgx_xform* xf = new_xform(ctx, buckets, input_dim);
+        try {
+            xf->map_seed = map_seed;
+            xf->seeded_map = true;
+            build_perm_seeded(ctx, xf, sc.st);
+            sc.sync();
+        } catch (...) {
+            free_xform(xf);
+            throw;
+        }
+        *out = xf;
+    });
+}
+
+
+int cgx_countsketch_explicit(cgx_ctx* ctx, int64_t buckets, int64_t input_dim, const int64_t* hash, const double* sign,
+                             int mem, cgx_xform** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_mem(mem);
+        if (buckets < 1 || input_dim < 1) fail(CGX_EINVAL, "countsketch map: buckets and input_dim must be >= 1");
+        if (!hash || !sign) fail(CGX_EINVAL, "countsketch map: null hash/sign");
+        CallScope sc(ctx, nullptr);
+        cgx_xform* xf = new_xform(ctx, buckets, input_dim);
+        try {
+            build_explicit(ctx, xf, hash, sign, mem, sc);
+        } catch (...) {
+            free_xform(xf);
+            throw;
+        }
+        *out = xf;
+    });
+}
+
+int cgx_countsketch_injective(cgx_ctx* ctx, uint64_t map_seed, int64_t buckets, int64_t input_dim, cgx_xform** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (buckets < input_dim) fail(CGX_EINVAL, "countsketch_injective: needs buckets >= input_dim");
+        if (input_dim < 1) fail(CGX_EINVAL, "countsketch_injective: input_dim must be >= 1 on the GPU path");
+        // Partial Fisher-Yates over [0, buckets) (sketch.cpp:38-48): inherently sequential.
+        std::vector<int64_t> pool((size_t)buckets), hash((size_t)input_dim);
+        std::vector<double> sign((size_t)input_dim);
+        std::iota(pool.begin(), pool.end(), int64_t{0});
+        uint64_t k = 0;
+        for (int64_t i = 0; i < input_dim; ++i) {
+            const int64_t j = i + (int64_t)(rng_draw(map_seed, k++) % (uint64_t)(buckets - i));
+            std::swap(pool[(size_t)i], pool[(size_t)j]);
+            hash[(size_t)i] = pool[(size_t)i];
+            sign[(size_t)i] = (rng_draw(map_seed, k++) & 1ULL) ? 1.0 : -1.0;
+        }
+        CallScope sc(ctx, nullptr);
+        cgx_xform* xf = new_xform(ctx, buckets, input_dim);
+        try {
+            xf->map_seed = map_seed;
+            build_explicit(ctx, xf, hash.data(), sign.data(), CGX_MEM_HOST, sc);
+        } catch (...) {
+            free_xform(xf);
+            throw;
+        }
+        *out = xf;
+    });
+}
+
+int cgx_countgauss_new(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim, cgx_xform** out) {
+    return cgx_countgauss_new_shard(ctx, t_seed, m, buckets, input_dim, 0, input_dim, out);
+}
+
+int cgx_countgauss_new_shard(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
+                             int64_t row0, int64_t rows, cgx_xform** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (m < 1 || buckets < 1 || input_dim < 1)
+            fail(CGX_EINVAL, "countgauss_new: m, buckets and input_dim must be >= 1");
+        if (row0 < 0 || rows < 1 || row0 + rows > input_dim)
+            fail(CGX_EINVAL, "countgauss_new_shard: need 0 <= row0 and 1 <= rows and row0 + rows <= input_dim");
+        CallScope sc(ctx, nullptr);
+        cgx_xform* xf = new_xform(ctx, buckets, rows);
+        try {
+            xf->row0 = row0;
+            xf->t_seed = t_seed;
+            xf->map_seed = rng_draw(mix64(t_seed, 1), 0);  // countsketch_new(..., cs_rng): map.seed
+            xf->g_seed = mix64(t_seed, 2);                 // g_rng = SeededRng(mix64(t.seed, 2))
+            xf->m = m;
+            xf->has_g = true;
+            build_perm_seeded(ctx, xf, sc.st);
+            sc.sync();
+        } catch (...) {
+            free_xform(xf);
+            throw;
+        }
+        *out = xf;
+    });
+}
+
+int cgx_xform_set_gaussian_seeded(cgx_ctx* ctx, cgx_xform* xf, int64_t m, uint64_t g_seed) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        if (m < 1) fail(CGX_EINVAL, "gaussian_matrix: dimensions must be positive");
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+        if (xf->g_dev) {
+            cudaFree(xf->g_dev);
+            xf->g_dev = nullptr;
+        }
+        xf->m = m;
+        xf->g_seed = g_seed;
+        xf->has_g = true;
+        xf->g_explicit = false;
+    });
+}
+
+int cgx_xform_set_gaussian_explicit(cgx_ctx* ctx, cgx_xform* xf, int64_t m, const double* g, int mem) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(mem);
+        if (m < 1) fail(CGX_EINVAL, "gaussian_matrix: dimensions must be positive");
+        CallScope sc(ctx, nullptr);
+        const size_t bytes = sizeof(double) * (size_t)(m * xf->B);
+        double* gd = nullptr;
+        CGX_CUDA(cudaMalloc((void**)&gd, bytes));
+        CGX_CUDA(cudaMemcpyAsync(gd, g, bytes, mem == CGX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                 sc.st));
+        sc.sync();
+        if (xf->g_dev) cudaFree(xf->g_dev);
+        xf->g_dev = gd;
+        xf->m = m;
+        xf->has_g = true;
+        xf->g_explicit = true;
+    });
+}
+
+int cgx_xform_info(const cgx_xform* xf, uint64_t* t_seed, uint64_t* map_seed, uint64_t* g_seed, int64_t* m,
+                   int64_t* buckets, int64_t* input_dim) {
+    return guard([&] {
+        need_xf(xf);
+        if (t_seed) *t_seed = xf->t_seed;
+        if (map_seed) *map_seed = xf->map_seed;
+        if (g_seed) *g_seed = xf->g_seed;
+        if (m) *m = xf->has_g ? xf->m : 0;
+        if (buckets) *buckets = xf->B;
+        if (input_dim) *input_dim = xf->n;
+    });
+}
+
+int cgx_xform_free(cgx_xform* xf) {
+    return guard([&] {
+        if (!xf) return;
+        std::lock_guard<std::recursive_mutex> lk(xf->ctx->mu);
+        cudaSetDevice(xf->ctx->device);
+        cudaStreamSynchronize(xf->ctx->stream);
+        cudaEventSynchronize(xf->ctx->done);
+        free_xform(xf);
+    });
+}
+
+int cgx_fill_hash_sign(cgx_ctx* ctx, const cgx_xform* xf, int64_t* hash, double* sign, int mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(mem);
+        CallScope sc(ctx, stream);
+        const size_t hb = sizeof(int64_t) * (size_t)xf->n, sb = sizeof(double) * (size_t)xf->n;
+        int64_t* hd = hash;
+        double* sd = sign;
+        if (mem == CGX_MEM_HOST) {
+            hd = hash ? (int64_t*)ctx->xstage.get(hb + sb) : nullptr;
+            sd = sign ? (double*)((char*)ctx->xstage.get(hb + sb) + hb) : nullptr;
+        }
+        launch_fill_hash_sign(ctx, xf, hd, sd, sc.st);
+        if (mem == CGX_MEM_HOST) {
+            if (hash) CGX_CUDA(cudaMemcpyAsync(hash, hd, hb, cudaMemcpyDeviceToHost, sc.st));
+            if (sign) CGX_CUDA(cudaMemcpyAsync(sign, sd, sb, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        }
+    });
+}
+
+int cgx_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, int mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(mem);
+        if (!xf->has_g) fail(CGX_EINVAL, "cgx_fill_gaussian: transform has no Gaussian factor");
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)(xf->m * xf->B);
+        double* gd = mem == CGX_MEM_HOST ? (double*)ctx->xstage.get(bytes) : g;
+        launch_fill_gaussian(ctx, xf, gd, sc.st);
+        if (mem == CGX_MEM_HOST) {
+            CGX_CUDA(cudaMemcpyAsync(g, gd, bytes, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        }
+    });
+}
+
+int cgx_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_mem(mem);
+        if (count <= 0) return;
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)count;
+        const double* pd = (const double*)to_device(ctx, ctx->hstage_dev, p, bytes, mem, sc.st);
+        double* od = mem == CGX_MEM_HOST ? (double*)ctx->xstage.get(bytes) : out;
+        int* bad = (int*)ctx->counts.get(sizeof(int));
+        CGX_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), sc.st));
+        launch_inverse_normal_cdf(ctx, pd, od, count, bad, sc.st);
+        int hbad = 0;
+        CGX_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, sc.st));
+        if (mem == CGX_MEM_HOST) CGX_CUDA(cudaMemcpyAsync(out, od, bytes, cudaMemcpyDeviceToHost, sc.st));
+        sc.sync();
+        if (hbad) fail(CGX_EINVAL, "inverse_normal_cdf: p must lie in (0,1)");
+    });
+}
+
+int cgx_countsketch_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
+                                int64_t n, int64_t d, int x_mem, double* sx, int sx_layout, int sx_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(x_mem);
+        need_mem(sx_mem);
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)(xf->B * d);
+        double* sxd = (sx_mem == CGX_MEM_DEVICE && sx_layout == CGX_ROW_MAJOR) ? sx : (double*)ctx->sx.get(bytes);
+        sketch_dense_dev(ctx, xf, x, dtype, layout, ld, n, d, x_mem, sxd, sc.st);
+        place_sx(ctx, xf, sxd, d, sx, sx_layout, sx_mem, sc);
+        if (x_mem == CGX_MEM_HOST) sc.sync();
+    });
+}
+
+int cgx_countsketch_apply_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
+                              const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem, double* sx,
+                              int sx_layout, int sx_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(x_mem);
+        need_mem(sx_mem);
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)(xf->B * d);
+        double* sxd = (sx_mem == CGX_MEM_DEVICE && sx_layout == CGX_ROW_MAJOR) ? sx : (double*)ctx->sx.get(bytes);
+        sketch_csr_dev(ctx, xf, rowptr, cols, idx_type, vals, dtype, n, d, nnz, x_mem, sxd, sc.st);
+        place_sx(ctx, xf, sxd, d, sx, sx_layout, sx_mem, sc);
+        if (x_mem == CGX_MEM_HOST) sc.sync();
+    });
+}
+
+int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
+                               int64_t n, int64_t d, int x_mem, double* z, int z_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(x_mem);
+        need_mem(z_mem);
+        need_g(xf);
+        CallScope sc(ctx, stream);
+        double* sxd = (double*)ctx->sx.get(sizeof(double) * (size_t)(xf->B * d));
+        sketch_dense_dev(ctx, xf, x, dtype, layout, ld, n, d, x_mem, sxd, sc.st);
+        finish_gemm(ctx, xf, sxd, d, z, z_mem, sc);
+        if (x_mem == CGX_MEM_HOST) sc.sync();
+    });
+}
+
+int cgx_countgauss_apply_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
+                             const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem, double* z,
+                             int z_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(x_mem);
+        need_mem(z_mem);
+        need_g(xf);
+        CallScope sc(ctx, stream);
+        double* sxd = (double*)ctx->sx.get(sizeof(double) * (size_t)(xf->B * d));
+        sketch_csr_dev(ctx, xf, rowptr, cols, idx_type, vals, dtype, n, d, nnz, x_mem, sxd, sc.st);
+        finish_gemm(ctx, xf, sxd, d, z, z_mem, sc);
+        if (x_mem == CGX_MEM_HOST) sc.sync();
+    });
+}
+
+int cgx_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int sx_layout, int64_t d, int sx_mem, double* z,
+                   int z_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(sx_mem);
+        need_mem(z_mem);
+        need_g(xf);
+        if (d < 0) fail(CGX_EINVAL, "gemm: negative column count");
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)(xf->B * d);
+        const double* sd = (const double*)to_device(ctx, ctx->hstage_dev, sx, bytes, sx_mem, sc.st);
+        if (sx_layout == CGX_COL_MAJOR && d > 0) {
+            // col-major B x d == row-major d x B -> transpose into row-major B x d
+            double* rm = (double*)ctx->sx.get(bytes);
+            launch_transpose_x(ctx, sd, CGX_F64, xf->B, xf->B, d, rm, sc.st);
+            sd = rm;
+        }
+        finish_gemm(ctx, xf, sd, d, z, z_mem, sc);
+    });
+}
+
+int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_rows, int64_t b0, int64_t b1, int64_t d,
+                         int sx_mem, double* z, int z_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(sx_mem);
+        need_mem(z_mem);
+        need_g(xf);
+        if (d < 0 || b0 < 0 || b1 < b0 || b1 > xf->B) fail(CGX_EINVAL, "gemm: bad bucket range");
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)((b1 - b0) * d);
+        const double* sd = (const double*)to_device(ctx, ctx->hstage_dev, sx_rows, bytes, sx_mem, sc.st);
+        finish_gemm(ctx, xf, sd, d, z, z_mem, sc, b0, b1);
+    });
+}
+
+int cgx_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d, int mem, int64_t* amax, int64_t* amin,
+                        int64_t* tie_rows, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_mem(mem);
+        if (m < 1) fail(CGX_EINVAL, "anchor extraction: m must be >= 1");
+        if (d < 1) fail(CGX_EINVAL, "anchor extraction: X must have at least one column");
+        CallScope sc(ctx, stream);
+        const double* zd = (const double*)to_device(ctx, ctx->hstage_dev, z, sizeof(double) * (size_t)(m * d), mem, sc.st);
+        int64_t* outs = (int64_t*)ctx->counts.get(sizeof(int64_t) * (size_t)(3 * m));
+        launch_select_extremes(ctx, zd, m, d, outs, outs + m, outs + 2 * m, sc.st);
+        std::vector<int64_t> h((size_t)(3 * m));
+        CGX_CUDA(cudaMemcpyAsync(h.data(), outs, sizeof(int64_t) * (size_t)(3 * m), cudaMemcpyDeviceToHost, sc.st));
+        sc.sync();
+        if (mem == CGX_MEM_HOST) {
+            std::copy(h.begin(), h.begin() + m, amax);
+            std::copy(h.begin() + m, h.begin() + 2 * m, amin);
+        } else {
+            CGX_CUDA(cudaMemcpyAsync(amax, outs, sizeof(int64_t) * (size_t)m, cudaMemcpyDeviceToDevice, sc.st));
+            CGX_CUDA(cudaMemcpyAsync(amin, outs + m, sizeof(int64_t) * (size_t)m, cudaMemcpyDeviceToDevice, sc.st));
+            sc.sync();
+        }
+        int64_t t = 0;
+        for (int64_t r = 0; r < m; ++r) t += h[(size_t)(2 * m + r)];
+        if (tie_rows) *tie_rows = t;
+    });
+}
+
+int cgx_gen_dense_normal(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype, int layout,
+                         void* x_dev, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        dsize(dtype);
+        if (n < 0 || d < 0) fail(CGX_EINVAL, "cgx_gen_dense_normal: negative size");
+        if (n * d == 0) return;
+        CallScope sc(ctx, stream);
+        if (row0 < 0) fail(CGX_EINVAL, "cgx_gen_dense_normal: negative row0");
+        launch_gen_dense(ctx, seed, row0, n, d, dtype, layout, x_dev, sc.st);
+    });
+}
+
+int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double density, int64_t* rowptr_dev,
+                          int32_t* cols_dev, float* vals_dev, int64_t* nnz_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (n < 1 || d < 1) fail(CGX_EINVAL, "cgx_gen_csr_bernoulli: n and d must be >= 1");
+        if (!(density >= 0.0 && density <= 1.0)) fail(CGX_EINVAL, "cgx_gen_csr_bernoulli: density must lie in [0,1]");
+        CallScope sc(ctx, stream);
+        if (!cols_dev || !vals_dev) {
+            launch_gen_csr_counts(ctx, seed, n, d, density, rowptr_dev, sc.st);
+            int64_t nnz = 0;
+            CGX_CUDA(cudaMemcpyAsync(&nnz, rowptr_dev + n, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+            if (nnz_out) *nnz_out = nnz;
+            return;
+        }
+        launch_gen_csr_fill(ctx, seed, n, d, density, rowptr_dev, cols_dev, vals_dev, sc.st);
+    });
+}
+
+uint64_t cgx_launch_count(const cgx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cgx_profile_enable(cgx_ctx* ctx, int on) {
+    return guard([&] {
+        need_ctx(ctx);
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+        ctx->prof.on = on != 0;
+        ctx->prof.used[0] = ctx->prof.used[1] = 0;
+    });
+}
+
+int cgx_profile_read(cgx_ctx* ctx, int stage, double* total_ms, int64_t* launches) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (stage < 0 || stage > 1) fail(CGX_EINVAL, "cgx_profile_read: stage must be 0 or 1");
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        double tot = 0.0;
+        auto& v = ctx->prof.ev[stage];
+        for (size_t i = 0; i < ctx->prof.used[stage]; ++i) {
+            CGX_CUDA(cudaEventSynchronize(v[i].second));
+            float ms = 0.f;
+            CGX_CUDA(cudaEventElapsedTime(&ms, v[i].first, v[i].second));
+            tot += ms;
+        }
+        if (total_ms) *total_ms = tot;
+        if (launches) *launches = (int64_t)ctx->prof.used[stage];
+        ctx->prof.used[stage] = 0;
+    });
+}
+
+} // extern "C"

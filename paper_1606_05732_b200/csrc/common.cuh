@@ -1,0 +1,133 @@
+// common.cuh -- device-side primitives shared by every kernel of the CountGauss path.
+//
+//  * SplitMix64 counter map: draw k of SeededRng(seed) is F(seed + (k+1)*gamma)
+//    (reference include/countgauss/rng.hpp:31-37), so hashes, signs and G entries are
+//    pure functions of (seed, index) and are computed where they are consumed.
+//  * Exact 64-bit "mod B" through a 64x64->128 high multiply (no software division).
+//  * The reference's N(0,1) quantile: Acklam's rational approximation followed by one
+//    Halley step against erfc (reference src/rng.cpp:13-55).  The arithmetic is written
+//    with explicit _rn intrinsics so nvcc cannot contract it into FMAs that the x86
+//    reference (built without FMA) does not perform; only erfc/exp/log differ (CUDA libm
+//    vs glibc), which is why G parity is stated as a tolerance.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cgx {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+
+__host__ __device__ __forceinline__ uint64_t fin64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// Draw k (0-based) of SeededRng(seed).
+__host__ __device__ __forceinline__ uint64_t rng_draw(uint64_t seed, uint64_t k) {
+    return fin64(seed + (k + 1) * kGamma);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t a, uint64_t b) {
+    return fin64(a + kGamma + b * 0xBF58476D1CE4E5B9ULL);
+}
+
+// z mod B for 1 <= B < 2^63 with magic = floor((2^64-1)/B): q = hi(z*magic) is floor(z/B)
+// or one less, so one conditional subtraction finishes the job.
+struct FastMod {
+    uint64_t B;
+    uint64_t magic;
+    __host__ explicit FastMod(uint64_t b) : B(b), magic(~0ULL / b) {}
+    __device__ __forceinline__ uint64_t operator()(uint64_t z) const {
+        uint64_t q = __umul64hi(z, magic);
+        uint64_t r = z - q * B;
+        return r >= B ? r - B : r;
+    }
+};
+
+// Row i of a seeded CountSketch (sketch.cpp:21-26): bucket = draw 2i mod B,
+// sign = + iff draw 2i+1 is odd.  Returned as (bucket, negative?).
+__device__ __forceinline__ uint32_t cs_bucket(uint64_t cs_seed, uint64_t i, const FastMod& mod) {
+    return (uint32_t)mod(rng_draw(cs_seed, 2 * i));
+}
+__device__ __forceinline__ uint32_t cs_negative(uint64_t cs_seed, uint64_t i) {
+    return (uint32_t)((rng_draw(cs_seed, 2 * i + 1) & 1ULL) ^ 1ULL);
+}
+
+// next_uniform (rng.hpp:40-42): exact in fp64.
+__host__ __device__ __forceinline__ double uniform53(uint64_t u) {
+    return ((double)(u >> 11) + 0.5) * 0x1.0p-53;
+}
+
+#define CGX_M(a, b) __dmul_rn((a), (b))
+#define CGX_A(a, b) __dadd_rn((a), (b))
+
+// Acklam's rational approximation (rng.cpp:13-41), evaluated in the reference's order.
+__device__ __forceinline__ double acklam(double p) {
+    const double a0 = -3.969683028665376e+01, a1 = 2.209460984245205e+02, a2 = -2.759285104469687e+02,
+                 a3 = 1.383577518672690e+02, a4 = -3.066479806614716e+01, a5 = 2.506628277459239e+00;
+    const double b0 = -5.447609879822406e+01, b1 = 1.615858368580409e+02, b2 = -1.556989798598866e+02,
+                 b3 = 6.680131188771972e+01, b4 = -1.328068155288572e+01;
+    const double c0 = -7.784894002430293e-03, c1 = -3.223964580411365e-01, c2 = -2.400758277161838e+00,
+                 c3 = -2.549732539343734e+00, c4 = 4.374664141464968e+00, c5 = 2.938163982698783e+00;
+    const double d0 = 7.784695709041462e-03, d1 = 3.224671290700398e-01, d2 = 2.445134137142996e+00,
+                 d3 = 3.754408661907416e+00;
+    const double p_low = 0.02425;
+    if (p >= p_low && p <= 1.0 - p_low) {
+        double q = __dadd_rn(p, -0.5);
+        double r = CGX_M(q, q);
+        double num = CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(a0, r), a1), r), a2), r), a3), r), a4), r), a5);
+        num = CGX_M(num, q);
+        double den = CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(b0, r), b1), r), b2), r), b3), r), b4), r), 1.0);
+        return __ddiv_rn(num, den);
+    }
+    // Tails: q = sqrt(-2 log(p)) for p < p_low, sqrt(-2 log(1-p)) (negated result) above.
+    const bool upper = p > 1.0 - p_low;
+    double t = upper ? __dadd_rn(1.0, -p) : p;
+    double q = __dsqrt_rn(CGX_M(-2.0, log(t)));
+    double num = CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(c0, q), c1), q), c2), q), c3), q), c4), q), c5);
+    double den = CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(CGX_A(CGX_M(d0, q), d1), q), d2), q), d3), q), 1.0);
+    double x = __ddiv_rn(num, den);
+    return upper ? -x : x;
+}
+
+// inverse_normal_cdf (rng.cpp:45-55) for p in (0,1): Acklam + one Halley step.
+__device__ __forceinline__ double inverse_normal_cdf(double p) {
+    double x = acklam(p);
+    const double sqrt2pi = 2.5066282746310005024;
+    const double sqrt2 = 1.41421356237309504880;
+    double e = __dadd_rn(CGX_M(0.5, erfc(__ddiv_rn(-x, sqrt2))), -p);
+    double u = CGX_M(CGX_M(e, sqrt2pi), exp(CGX_M(CGX_M(0.5, x), x)));
+    x = __dadd_rn(x, -__ddiv_rn(u, CGX_A(1.0, CGX_M(CGX_M(0.5, x), u))));
+    return x;
+}
+
+// G(r, c) of gaussian_matrix(m, B, SeededRng(g_seed)) (matrix.cpp:199-207): draw c*m + r.
+__device__ __forceinline__ double gauss_entry(uint64_t g_seed, uint64_t m, uint64_t r, uint64_t c) {
+    return inverse_normal_cdf(uniform53(rng_draw(g_seed, c * m + r)));
+}
+
+// Synthetic-input normal (oracle/cgoracle.c cgo_normal_f32): fp32 rounding of the Acklam
+// quantile; the Halley step is below fp32 resolution.
+__device__ __forceinline__ float datagen_normal(uint64_t seed, uint64_t e) {
+    return (float)acklam(uniform53(rng_draw(seed, e)));
+}
+
+#undef CGX_M
+#undef CGX_A
+
+// Perm entries: row index in bits 0..30, "negative sign" flag in bit 31.
+constexpr uint32_t kRowMask = 0x7FFFFFFFu;
+constexpr uint32_t kNegBit = 0x80000000u;
+
+__device__ __forceinline__ int warp_incl_scan(int v, unsigned lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if ((int)lane >= o) v += t;
+    }
+    return v;
+}
+
+} // namespace cgx

@@ -1,0 +1,181 @@
+// gauss_gemm.cu -- stage 2, Z = G . (S.X), with G generated inside the GEMM.
+//
+// Replaces gemm(t.g, SX) (reference src/matrix.cpp:111-129) and the materialized
+// t.g = gaussian_matrix(m, B, g_rng) (matrix.cpp:199-207, rng.cpp:13-59).  G(r, c) is a
+// pure function of (g_seed, c*m + r) -- SplitMix64 draw, 53-bit uniform, Acklam quantile,
+// one Halley step -- so each CTA generates exactly the m-tile x K-chunk of G it consumes,
+// in shared memory, and G never exists in HBM.
+//
+// The contraction is FP64 on the tensor pipe: warp-level DMMA (mma.sync m8n8k4 f64;
+// tcgen05 has no f64 kind on sm_100a).  3xTF32 would miss the reference's 1e-8
+// composite tolerance, so the fp64 drop-in stays fp64.
+//
+// Work split: CTA tile 64 (rows of Z) x 32 (columns of Z) x a K-range of buckets
+// (split-K).  Each split writes its partial tile; a second kernel sums the partials in
+// ascending split order, so Z is deterministic run to run.
+#include "common.cuh"
+#include "internal.h"
+
+namespace cgx {
+namespace {
+
+constexpr int MT = 64, NT = 32, KC = 32;
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// sx holds buckets [gcol0, gcol0 + B) (row-major, row k = bucket gcol0 + k).
+__global__ void __launch_bounds__(256) gauss_gemm_kernel(const double* __restrict__ sx, int64_t B, int64_t d,
+                                                         int64_t m, uint64_t g_seed,
+                                                         const double* __restrict__ g_explicit, int64_t gcol0,
+                                                         int64_t k_per_split, double* __restrict__ zpart) {
+    __shared__ double Gs[MT][KC + 1];
+    __shared__ double Ss[KC][NT + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps, 16 x 16 each
+    const int64_t m0 = (int64_t)blockIdx.x * MT, n0 = (int64_t)blockIdx.y * NT;
+    const int64_t split = blockIdx.z;
+    const int64_t kb = split * k_per_split;
+    const int64_t ke = min(B, kb + k_per_split);
+
+    double acc[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int64_t k0 = kb; k0 < ke; k0 += KC) {
+        // G tile: rows m0.., columns k0..  (column-major draw order c*m + r)
+#pragma unroll
+        for (int i = 0; i < (MT * KC) / 256; ++i) {
+            const int e = tid + 256 * i;
+            const int r = e % MT, c = e / MT;
+            const int64_t gr = m0 + r, gc = k0 + c;
+            double g = 0.0;
+            if (gr < m && gc < ke) {
+                const int64_t col = gcol0 + gc;
+                g = g_explicit ? g_explicit[col * m + gr] : gauss_entry(g_seed, (uint64_t)m, (uint64_t)gr, (uint64_t)col);
+            }
+            Gs[r][c] = g;
+        }
+        // SX tile: rows k0.., columns n0..   (row-major B x d)
+#pragma unroll
+        for (int i = 0; i < (KC * NT) / 256; ++i) {
+            const int e = tid + 256 * i;
+            const int c = e % NT, r = e / NT;
+            const int64_t gk = k0 + r, gn = n0 + c;
+            Ss[r][c] = (gk < ke && gn < d) ? sx[gk * d + gn] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < KC; kk += 4) {
+            double a[2], b[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) a[i] = Gs[wm * 16 + i * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) b[j] = Ss[kk + (lane & 3)][wn * 16 + j * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+        __syncthreads();
+    }
+    // partial tile -> zpart[split] (column-major m x d)
+    double* zp = zpart + split * m * d;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t r = m0 + wm * 16 + i * 8 + (lane >> 2);
+                const int64_t c = n0 + wn * 16 + j * 8 + (lane & 3) * 2 + h;
+                if (r < m && c < d) zp[c * m + r] = acc[i][j][h];
+            }
+}
+
+__global__ void reduce_splits(const double* __restrict__ zpart, int64_t splits, int64_t md, double* __restrict__ z) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < md; e += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t k = 0; k < splits; ++k) s += zpart[k * md + e];
+        z[e] = s;
+    }
+}
+
+__global__ void fill_gaussian_kernel(uint64_t g_seed, int64_t m, int64_t total, double* g) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / m, r = e - c * m;
+        g[e] = gauss_entry(g_seed, (uint64_t)m, (uint64_t)r, (uint64_t)c);
+    }
+}
+
+__global__ void inverse_normal_cdf_kernel(const double* p, double* out, int64_t count, int* bad) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+        const double v = p[e];
+        if (!(v > 0.0 && v < 1.0)) {
+            atomicExch(bad, 1);
+            out[e] = __longlong_as_double(0x7ff8000000000000LL);
+        } else {
+            out[e] = inverse_normal_cdf(v);
+        }
+    }
+}
+
+} // namespace
+
+void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d,
+                       double* z, cudaStream_t s) {
+    const int64_t m = xf->m, B = b1 - b0;
+    if (B <= 0) {
+        CGX_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)(m * d), s));
+        return;
+    }
+    const int64_t tm = (m + MT - 1) / MT, tn = (d + NT - 1) / NT;
+    const int64_t kchunks = (B + KC - 1) / KC;
+    int64_t want = (2 * (int64_t)ctx->num_sms + tm * tn - 1) / (tm * tn);
+    if (want < 1) want = 1;
+    if (want > kchunks) want = kchunks;
+    if (want > 65535) want = 65535;
+    const int64_t chunks_per_split = (kchunks + want - 1) / want;
+    const int64_t k_per_split = chunks_per_split * KC;
+    const int64_t splits = (B + k_per_split - 1) / k_per_split;
+    double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
+    gauss_gemm_kernel<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)splits), 256, 0, s>>>(
+        sx, B, d, m, xf->g_seed, xf->g_explicit ? xf->g_dev : nullptr, b0, k_per_split, zpart);
+    count_launch(ctx);
+    check_launch("gauss_gemm");
+    const int64_t md = m * d;
+    int64_t blocks = (md + 255) / 256;
+    if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
+    reduce_splits<<<(unsigned)blocks, 256, 0, s>>>(zpart, splits, md, z);
+    count_launch(ctx);
+    check_launch("reduce_splits");
+}
+
+void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStream_t s) {
+    const int64_t total = xf->m * xf->B;
+    if (xf->g_explicit) {
+        CGX_CUDA(cudaMemcpyAsync(g, xf->g_dev, sizeof(double) * (size_t)total, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
+    fill_gaussian_kernel<<<(unsigned)blocks, 256, 0, s>>>(xf->g_seed, xf->m, total, g);
+    count_launch(ctx);
+    check_launch("fill_gaussian");
+}
+
+void launch_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int* bad, cudaStream_t s) {
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
+    if (blocks < 1) blocks = 1;
+    inverse_normal_cdf_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, out, count, bad);
+    count_launch(ctx);
+    check_launch("inverse_normal_cdf");
+}
+
+} // namespace cgx

@@ -1,0 +1,123 @@
+// internal.h -- host-side structures and kernel launchers behind the cgx C-ABI.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/cgx.h"
+
+namespace cgx {
+
+// Status-carrying error used inside the library; converted to a CGX_* code at the ABI.
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+#define CGX_CUDA(call) ::cgx::check_cuda((call), #call)
+
+// A grow-only device buffer owned by a context.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need);
+    void release();
+};
+
+struct Profile {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];
+    size_t used[2] = {0, 0};
+    void begin(int stage, cudaStream_t s);
+    void end(int stage, cudaStream_t s);
+};
+
+} // namespace cgx
+
+struct cgx_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;        // last call's completion, for cross-stream scratch reuse
+    std::recursive_mutex mu;
+    uint64_t launches = 0;
+    cgx::DevBuf sx, zpart, xstage, tmp;     // scratch (tmp: scan.cu only)
+    cgx::DevBuf sort_k[2], sort_v[2], sort_hist, counts;  // transform construction
+    cgx::DevBuf hstage_dev;                 // device landing zone for host inputs
+    void* pinned = nullptr;                 // pinned staging for pageable host inputs
+    size_t pinned_bytes = 0;
+    cgx::Profile prof;
+};
+
+struct cgx_xform {
+    cgx_ctx* ctx = nullptr;
+    int64_t B = 0, n = 0, m = 0;
+    int64_t row0 = 0;              // global index of local row 0 (row shards, multi-GPU)
+    uint64_t t_seed = 0, map_seed = 0, g_seed = 0;
+    bool seeded_map = true;        // hash/sign are the index functions of map_seed
+    bool has_g = false;
+    bool g_explicit = false;
+    double* g_dev = nullptr;       // explicit G only (m x B col-major)
+    uint32_t* perm = nullptr;      // n entries: row | neg<<31, sorted by (bucket, row)
+    uint32_t* offsets = nullptr;   // B+1 bucket boundaries into perm
+};
+
+namespace cgx {
+
+// construct.cu
+void build_perm_seeded(cgx_ctx* ctx, cgx_xform* xf, cudaStream_t s);
+void build_perm_explicit(cgx_ctx* ctx, cgx_xform* xf, const uint32_t* keys_dev, const uint32_t* vals_dev,
+                         cudaStream_t s);
+bool prep_explicit(cgx_ctx* ctx, const int64_t* hash, const double* sign, int64_t n, int64_t B, uint32_t* keys,
+                   uint32_t* vals, cudaStream_t s);
+void launch_fill_hash_sign(cgx_ctx* ctx, const cgx_xform* xf, int64_t* hash, double* sign, cudaStream_t s);
+
+// sketch_dense.cu: SX (row-major B x d, fp64) from row-major X.
+void launch_sketch_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int64_t ld, int64_t n,
+                         int64_t d, double* sx, cudaStream_t s);
+// col-major -> row-major copy of X (any dtype) into dst
+void launch_transpose_x(cgx_ctx* ctx, const void* x, int dtype, int64_t ld, int64_t n, int64_t d, void* dst,
+                        cudaStream_t s);
+// row-major B x d (fp64) -> col-major
+void launch_transpose_sx(cgx_ctx* ctx, const double* src, int64_t B, int64_t d, double* dst, cudaStream_t s);
+
+// sketch_csr.cu
+void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
+                       const void* vals, int dtype, int64_t n, int64_t d, double* sx, int64_t chunk_rows,
+                       cudaStream_t s);
+
+// gauss_gemm.cu: z (col-major m x d) = G . sx (row-major B x d)
+// Buckets [b0, b1) only: sx points at row b0 (split-K across ranks).
+void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d,
+                       double* z, cudaStream_t s);
+void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStream_t s);
+void launch_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int* bad,
+                               cudaStream_t s);
+
+// extremes.cu
+void launch_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d, int64_t* amax, int64_t* amin,
+                            int64_t* tie_flags, cudaStream_t s);
+
+// datagen.cu
+void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype, int layout, void* x,
+                      cudaStream_t s);
+void launch_gen_csr_counts(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double density, int64_t* rowptr,
+                           cudaStream_t s);
+void launch_gen_csr_fill(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double density, const int64_t* rowptr,
+                         int32_t* cols, float* vals, cudaStream_t s);
+
+// scan.cu: exclusive scans (in place allowed), total written to out[count] when requested
+void exclusive_scan_u32(cgx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t count, cudaStream_t s);
+void exclusive_scan_i64(cgx_ctx* ctx, const int64_t* in, int64_t* out, int64_t count, cudaStream_t s);
+
+inline void count_launch(cgx_ctx* ctx, int k = 1) { ctx->launches += (uint64_t)k; }
+void check_launch(const char* what);
+
+} // namespace cgx

@@ -1,0 +1,206 @@
+// sketch_csr.cu -- S.X for CSR X: bucket-ordered gather with an on-chip accumulator.
+//
+// Replaces countsketch_apply(map, SparseMatrix) (reference src/sketch.cpp:68-113).  The
+// reference runs a serial row loop (every BASELINE CSR config takes that branch) or,
+// when B*d <= 2^16, 8192-row chunks whose partial buffers are reduced in ascending
+// chunk order.  Both orders are reproduced here bit-for-bit.
+//
+// B200 design: one warp owns bucket b's output row SX[b, 0..d) as an fp64 accumulator in
+// shared memory (or in the output row itself when d is too large for shared memory).
+// It walks the bucket's rows in ascending order (perm, construct.cu) 32 at a time:
+//   1. lane k fetches row k's [rowptr[r], rowptr[r+1]) -- one random 16 B read each;
+//   2. a warp prefix sum flattens the 32 rows' nonzeros into one item range, which the
+//      warp then reads in coalesced 32-item waves (consecutive items of a row are
+//      consecutive in memory), several waves in flight at once;
+//   3. each wave is applied in item order: items that hit the same column (only
+//      possible across rows) are serialized by lane rank via __match_any_sync, so
+//      every (bucket, column) sums its rows in ascending row order -- the reference's.
+// No atomics, deterministic, bit-identical to the reference.
+#include "common.cuh"
+#include "internal.h"
+
+#include <climits>
+
+namespace cgx {
+namespace {
+
+constexpr int kWaves = 4;  // item waves loaded before they are applied
+
+template <typename TV, typename TI, bool CHUNKED>
+__global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restrict__ rowptr,
+                                                         const TI* __restrict__ cols, const TV* __restrict__ vals,
+                                                         const uint32_t* __restrict__ perm,
+                                                         const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
+                                                         double* __restrict__ sx, double* __restrict__ gpart,
+                                                         int64_t chunk_rows, int use_smem) {
+    extern __shared__ double smem[];
+    __shared__ int s_incl[8][32];
+    __shared__ int64_t s_beg[8][32];
+    __shared__ uint32_t s_pe[8][32];
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int warps_per_cta = blockDim.x >> 5;
+    double* my = smem + (size_t)wid * d * (CHUNKED ? 2 : 1);
+
+    for (int64_t b = (int64_t)blockIdx.x * warps_per_cta + wid; b < B; b += (int64_t)gridDim.x * warps_per_cta) {
+        double* acc = use_smem ? my : sx + b * d;
+        double* part = CHUNKED ? (use_smem ? my + d : gpart + b * d) : nullptr;
+        for (int64_t j = lane; j < d; j += 32) {
+            acc[j] = 0.0;
+            if (CHUNKED) part[j] = 0.0;
+        }
+        double* tgt = CHUNKED ? part : acc;
+        int64_t cur_chunk = -1;
+        __syncwarp();
+        const uint32_t beg = offsets[b], end = offsets[b + 1];
+        for (uint32_t base = beg; base < end; base += 32) {
+            const int cnt = (int)min(32u, end - base);
+            uint32_t pe = 0;
+            int64_t rb = 0, re = 0;
+            if ((int)lane < cnt) {
+                pe = __ldg(perm + base + lane);
+                const int64_t row = pe & kRowMask;
+                rb = __ldg(rowptr + row);
+                re = __ldg(rowptr + row + 1);
+            }
+            const int incl = warp_incl_scan((int)(re - rb), lane);
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            s_incl[wid][lane] = incl;
+            s_beg[wid][lane] = rb;
+            s_pe[wid][lane] = pe;
+            __syncwarp();
+            for (int q0 = 0; q0 < total; q0 += 32 * kWaves) {
+                TI c[kWaves];
+                TV v[kWaves];
+                int kk[kWaves];
+#pragma unroll
+                for (int w = 0; w < kWaves; ++w) {
+                    const int q = q0 + w * 32 + (int)lane;
+                    kk[w] = -1;
+                    if (q < total) {
+                        int lo = 0;  // first k with incl[k] > q
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1)
+                            if (s_incl[wid][lo + step - 1] <= q) lo += step;
+                        const int start = lo ? s_incl[wid][lo - 1] : 0;
+                        const int64_t pos = s_beg[wid][lo] + (q - start);
+                        c[w] = __ldcs(cols + pos);
+                        v[w] = __ldcs(vals + pos);
+                        kk[w] = lo;
+                    }
+                }
+#pragma unroll
+                for (int w = 0; w < kWaves; ++w) {
+                    const bool valid = kk[w] >= 0;
+                    if (!__any_sync(0xffffffffu, valid)) break;
+                    const uint32_t pe_k = valid ? s_pe[wid][kk[w]] : 0u;
+                    double val = valid ? (double)v[w] : 0.0;
+                    if (pe_k & kNegBit) val = -val;
+                    const int64_t col = valid ? (int64_t)c[w] : -1 - (int64_t)lane;
+                    bool todo = valid;
+                    if (CHUNKED) {
+                        const int64_t ch = valid ? (int64_t)(pe_k & kRowMask) / chunk_rows : LLONG_MAX;
+                        while (__any_sync(0xffffffffu, todo)) {
+                            const int64_t cmin = __reduce_min_sync(0xffffffffu, todo ? (unsigned)ch : UINT_MAX);
+                            if (cmin != cur_chunk) {
+                                if (cur_chunk >= 0) {
+                                    for (int64_t j = lane; j < d; j += 32) {
+                                        acc[j] += part[j];
+                                        part[j] = 0.0;
+                                    }
+                                }
+                                cur_chunk = cmin;
+                                __syncwarp();
+                            }
+                            const bool mine = todo && ch == cmin;
+                            const int64_t key = mine ? col : -1 - (int64_t)lane;
+                            const unsigned peers = __match_any_sync(0xffffffffu, key);
+                            const unsigned rank = __popc(peers & lt_mask);
+                            const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
+                            for (unsigned r = 0; r <= maxr; ++r) {
+                                if (mine && rank == r) tgt[key] += val;
+                                __syncwarp();
+                            }
+                            if (mine) todo = false;
+                        }
+                    } else {
+                        const unsigned peers = __match_any_sync(0xffffffffu, col);
+                        const unsigned rank = __popc(peers & lt_mask);
+                        const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
+                        for (unsigned r = 0; r <= maxr; ++r) {
+                            if (valid && rank == r) acc[col] += val;
+                            __syncwarp();
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (CHUNKED && cur_chunk >= 0) {
+            for (int64_t j = lane; j < d; j += 32) acc[j] += part[j];
+            __syncwarp();
+        }
+        if (use_smem) {
+            for (int64_t j = lane; j < d; j += 32) sx[b * d + j] = acc[j];
+        }
+        __syncwarp();
+    }
+}
+
+template <typename TV, typename TI, bool CHUNKED>
+void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* cols, const TV* vals, int64_t d,
+            double* sx, int64_t chunk_rows, cudaStream_t s) {
+    const size_t per_warp = sizeof(double) * (size_t)d * (CHUNKED ? 2 : 1);
+    const size_t budget = 96 * 1024;
+    int warps = (int)(budget / per_warp);
+    if (warps > 8) warps = 8;
+    int use_smem = warps >= 1;
+    double* gpart = nullptr;
+    size_t smem = 0;
+    if (use_smem) {
+        smem = per_warp * warps;
+    } else {
+        warps = 8;
+        CGX_CUDA(cudaMemsetAsync(sx, 0, sizeof(double) * (size_t)(xf->B * d), s));
+        if (CHUNKED) gpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(xf->B * d));
+    }
+    auto kern = sketch_csr_kernel<TV, TI, CHUNKED>;
+    if (smem > 48 * 1024) CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int64_t blocks = (xf->B + warps - 1) / warps;
+    const int64_t cap = (int64_t)ctx->num_sms * 32;
+    if (blocks > cap) blocks = cap;
+    kern<<<(unsigned)blocks, warps * 32, smem, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, gpart,
+                                                   chunk_rows, use_smem);
+    count_launch(ctx);
+    check_launch("sketch_csr");
+}
+
+template <typename TV, typename TI>
+void dispatch_chunk(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, const void* vals,
+                    int64_t d, double* sx, int64_t chunk_rows, cudaStream_t s) {
+    if (chunk_rows > 0)
+        launch<TV, TI, true>(ctx, xf, rowptr, (const TI*)cols, (const TV*)vals, d, sx, chunk_rows, s);
+    else
+        launch<TV, TI, false>(ctx, xf, rowptr, (const TI*)cols, (const TV*)vals, d, sx, 0, s);
+}
+
+} // namespace
+
+void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
+                       const void* vals, int dtype, int64_t n, int64_t d, double* sx, int64_t chunk_rows,
+                       cudaStream_t s) {
+    (void)n;
+    if (dtype == CGX_F32) {
+        if (idx_type == CGX_I32)
+            dispatch_chunk<float, int32_t>(ctx, xf, rowptr, cols, vals, d, sx, chunk_rows, s);
+        else
+            dispatch_chunk<float, int64_t>(ctx, xf, rowptr, cols, vals, d, sx, chunk_rows, s);
+    } else {
+        if (idx_type == CGX_I32)
+            dispatch_chunk<double, int32_t>(ctx, xf, rowptr, cols, vals, d, sx, chunk_rows, s);
+        else
+            dispatch_chunk<double, int64_t>(ctx, xf, rowptr, cols, vals, d, sx, chunk_rows, s);
+    }
+}
+
+} // namespace cgx

@@ -1,0 +1,68 @@
+"""Multi-GPU CountGauss: rows of X sharded over ranks (one process per GPU).
+
+S.X = sum_p S_p.X_p where S_p is the CountSketch restricted to rank p's rows -- each rank
+derives its hashes/signs from the shared seed for its *global* row indices
+(cgx_countgauss_new_shard), so nothing but the seed is exchanged to build the transform.
+T.X is linear, so the partials combine after either stage:
+
+* ``"z"`` (default): every rank computes Z_p = G.(S_p.X_p) (G regenerated locally from
+  the seed) and the m x d partials are summed with one all-reduce.  Communication is
+  m*d*8 bytes; stage 2 is replicated.
+* ``"sx"``: the B x d partial sketches (row-major, so a bucket range is contiguous) are
+  reduce-scattered; rank p owns buckets [b_p, b_{p+1}) of the summed S.X and computes
+  Z_p = G[:, b_p:b_{p+1}) . S.X[b_p:b_{p+1}) (split-K: stage 2 and G generation divided
+  by P), then Z = sum_p Z_p by all-reduce.  Communication is (P-1)/P * B*d*8 per rank.
+
+The collectives go through ``torch.distributed`` (NCCL on the GPUs; gloo in the CPU
+tests).  Results equal the single-GPU T.X up to fp reassociation across ranks.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced row range [r0, r1) of rank `rank` (first n % world ranks get one
+    extra row)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("shard_range: need 0 <= rank < world")
+    base, extra = divmod(n, world)
+    r0 = rank * base + min(rank, extra)
+    return r0, r0 + base + (1 if rank < extra else 0)
+
+
+def bucket_range(B: int, world: int, rank: int) -> tuple[int, int]:
+    """Bucket slice owned by `rank` after the S.X reduce-scatter."""
+    return shard_range(B, world, rank)
+
+
+def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None, partial_z=None,
+            stage2: Optional[Callable] = None, group=None):
+    """Combine one rank's partial results into the full Z (every rank returns Z).
+
+    mode "z":  partial_z (m x d) is all-reduced.
+    mode "sx": partial_sx (B x d, row-major) is reduce-scattered by bucket range; the
+               owned slice goes through stage2(sx_slice, b0, b1) -> Z_p (m x d), which is
+               then all-reduced.
+    """
+    import torch
+    import torch.distributed as dist
+
+    if mode == "z":
+        dist.all_reduce(partial_z, group=group)
+        return partial_z
+    if mode != "sx":
+        raise ValueError("combine: mode must be 'z' or 'sx'")
+    # reduce_scatter_tensor needs equal chunks: pad B up to a multiple of world.
+    per = (B + world - 1) // world
+    flat = partial_sx.reshape(B, d)
+    if per * world != B:
+        pad = torch.zeros((per * world - B, d), dtype=flat.dtype, device=flat.device)
+        flat = torch.cat([flat, pad], 0)
+    out = torch.empty((per, d), dtype=flat.dtype, device=flat.device)
+    dist.reduce_scatter_tensor(out, flat.contiguous(), group=group)
+    b0 = rank * per
+    b1 = min(B, b0 + per)
+    z = stage2(out[: max(b1 - b0, 0)], b0, max(b1, b0))
+    dist.all_reduce(z, group=group)
+    return z
