@@ -336,9 +336,13 @@ def _is_torch(x) -> bool:
 
 
 def _stream_of(x):
+    """torch's current stream on x's device as a cudaStream_t.  torch's default stream is
+    the legacy stream (handle 0); pass cudaStreamLegacy (0x1) for it, since a NULL stream
+    means the context's own stream at the C-ABI."""
     import torch
 
-    return C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+    h = torch.cuda.current_stream(x.device).cuda_stream
+    return C.c_void_p(h if h else 1)
 
 
 def _dense_args(x):

@@ -29,7 +29,7 @@ def dense_normal(n: int, d: int, seed: int, dtype=None, layout: str = "row", dev
         x = torch.empty((d, n), dtype=dtype, device=dev).t()
         lay = CGX_COL_MAJOR
     dt = CGX_F32 if dtype == torch.float32 else CGX_F64
-    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream or 1)  # 1 = cudaStreamLegacy
     check(lib.cgx_gen_dense_normal(ctx.h, seed, row0, n, d, dt, lay, x.data_ptr(), stream))
     return x
 
@@ -44,7 +44,7 @@ def csr_bernoulli(n: int, d: int, density: float, seed: int, device=None):
 
     ctx = context(device)
     dev = torch.device("cuda", ctx.device)
-    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream or 1)  # 1 = cudaStreamLegacy
     rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
     nnz = C.c_int64()
     check(lib.cgx_gen_csr_bernoulli(ctx.h, seed, n, d, density, rp.data_ptr(), None, None, C.byref(nnz), stream))

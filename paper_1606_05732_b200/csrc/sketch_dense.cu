@@ -53,6 +53,13 @@ __device__ __forceinline__ float negate_if(float v, uint32_t neg) {
 __device__ __forceinline__ double negate_if(double v, uint32_t neg) {
     return __longlong_as_double(__double_as_longlong(v) ^ ((long long)(neg & kNegBit) << 32));
 }
+// bit in {0,1}: exact negation by flipping the IEEE sign bit
+__device__ __forceinline__ float flip_sign(float v, uint32_t bit) {
+    return __int_as_float(__float_as_int(v) ^ (int)(bit << 31));
+}
+__device__ __forceinline__ double flip_sign(double v, uint32_t bit) {
+    return __longlong_as_double(__double_as_longlong(v) ^ ((long long)bit << 63));
+}
 
 // R rows per warp-wide load step (L = 32/R lanes per row), V elements per lane.
 template <typename T, int V, int R>
@@ -89,18 +96,18 @@ __global__ void __launch_bounds__(256) sketch_dense_kernel(const T* __restrict__
                 for (int u = 0; u < U; ++u) {
                     const int t = (s0 + u) * R + (int)g;
                     const uint32_t e = __shfl_sync(0xffffffffu, pe, t & 31);
-                    const bool ok = colok && t < cnt;
-                    if (ok) {
-                        load_vec<T, V>(x + (int64_t)(e & kRowMask) * ld + col0, v[u]);
-#pragma unroll
-                        for (int k = 0; k < V; ++k) v[u][k] = negate_if(v[u][k], e);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < V; ++k) v[u][k] = T(0);
-                    }
+                    // unconditional load (padding entries read row 0, column 0) so that
+                    // nothing consumes a loaded register before the whole batch is issued
+                    load_vec<T, V>(x + (int64_t)(e & kRowMask) * ld + (colok ? col0 : 0), v[u]);
                 }
+                // signs applied only here, after every load of the batch is in flight
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
+                    const int t = (s0 + u) * R + (int)g;
+                    const uint32_t e = __shfl_sync(0xffffffffu, pe, t & 31);
+                    const bool ok = colok && t < cnt;
+#pragma unroll
+                    for (int k = 0; k < V; ++k) v[u][k] = ok ? negate_if(v[u][k], e) : T(0);
                     if (R == 1) {
 #pragma unroll
                         for (int k = 0; k < V; ++k) acc[k] += (double)v[u][k];
@@ -120,6 +127,89 @@ __global__ void __launch_bounds__(256) sketch_dense_kernel(const T* __restrict__
             for (int k = 0; k < V; ++k) sx[b * d + col0 + k] = acc[k];
         }
     }
+}
+
+// Wide rows (one row chunk spans the warp): the streaming form.  A warp owns G
+// consecutive buckets, whose rows are one contiguous stretch of perm; it streams that
+// stretch 32 entries at a time (the next 32 perm entries prefetched while the current
+// rows are in flight), issues U row loads back to back (4 KB per warp in flight), and
+// adds them in order, flushing the accumulator to SX whenever the stretch crosses a
+// bucket boundary (bucket boundaries come from one coalesced load of the G+1 offsets).
+// Per row and lane: one shuffle, one load, one convert, one add -- the warp's
+// instruction stream no longer restarts per bucket, so rows keep flowing.
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restrict__ x, int64_t ld, int64_t d,
+                                                           const uint32_t* __restrict__ perm,
+                                                           const uint32_t* __restrict__ offsets, int64_t B,
+                                                           int64_t nchunks, int G, double* __restrict__ sx) {
+    constexpr int CW = 32 * V;
+    constexpr int U = 64 / (V * (int)sizeof(T));  // rows per load batch: 2 KB per warp
+    const unsigned lane = threadIdx.x & 31;
+    const int64_t ngroups = (B + G - 1) / G;
+    const int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (task >= ngroups * nchunks) return;
+    const int64_t bg = task / nchunks;
+    const int64_t col0 = (task - bg * nchunks) * CW + (int64_t)lane * V;
+    const bool colok = col0 < d;
+    const int64_t b0 = bg * G;
+    const int nb = (int)min((int64_t)G, B - b0);
+    const uint32_t offk = (int)lane <= nb ? __ldg(offsets + b0 + lane) : 0u;
+    const uint32_t P0 = __shfl_sync(0xffffffffu, offk, 0);
+    const uint32_t P1 = __shfl_sync(0xffffffffu, offk, nb);
+    double* out = sx + b0 * d + col0;
+    int cur = 0;
+    uint32_t nextb = __shfl_sync(0xffffffffu, offk, 1);
+    double acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.0;
+
+    auto flush = [&]() {
+        if (colok) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) out[(int64_t)cur * d + k] = acc[k];
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = 0.0;
+        ++cur;
+        nextb = __shfl_sync(0xffffffffu, offk, min(cur + 1, 31));
+    };
+
+    uint32_t pe_next = P0 + lane < P1 ? __ldg(perm + P0 + lane) : 0u;
+    for (uint32_t base = P0; base < P1; base += 32) {
+        const uint32_t pe = pe_next;
+        if (base + 32 + lane < P1) pe_next = __ldg(perm + base + 32 + lane);
+        const int cnt = (int)min(32u, P1 - base);
+        const uint32_t negmask = __ballot_sync(0xffffffffu, pe & kNegBit);  // bit t: row t negative
+        // common case: a full chunk with no bucket boundary inside -> branch-free adds
+        const bool fast = cnt == 32 && nextb >= base + 32;
+#pragma unroll 1
+        for (int s0 = 0; s0 < cnt; s0 += U) {
+            T v[U][V];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = __shfl_sync(0xffffffffu, pe, (s0 + u) & 31);
+                load_vec<T, V>(x + (int64_t)(e & kRowMask) * ld + (colok ? col0 : 0), v[u]);
+            }
+            const uint32_t nm = negmask >> s0;
+            if (fast) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int k = 0; k < V; ++k) acc[k] += (double)flip_sign(v[u][k], (nm >> u) & 1u);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (s0 + u < cnt) {
+                        const uint32_t pos = base + s0 + u;
+                        while (pos == nextb) flush();
+#pragma unroll
+                        for (int k = 0; k < V; ++k) acc[k] += (double)flip_sign(v[u][k], (nm >> u) & 1u);
+                    }
+                }
+            }
+        }
+    }
+    while (cur < nb) flush();
 }
 
 template <typename E>
@@ -157,6 +247,20 @@ template <typename T, int V, int R>
 void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* sx, int accumulate,
             cudaStream_t s) {
     constexpr int CW = (32 / R) * V;
+    if (R == 1 && !accumulate) {
+        // ~1K rows per warp task, at most 31 buckets (one offsets load)
+        const int64_t rows_per_bucket = xf->n / xf->B + 1;
+        int64_t G = 1024 / rows_per_bucket;
+        G = G < 1 ? 1 : (G > 31 ? 31 : G);
+        const int64_t nchunks = (d + CW - 1) / CW;
+        const int64_t tasks = (xf->B + G - 1) / G * nchunks;
+        const int64_t blocks = (tasks + 7) / 8;
+        sketch_dense_stream<T, V><<<(unsigned)blocks, 256, 0, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks,
+                                                                   (int)G, sx);
+        count_launch(ctx);
+        check_launch("sketch_dense_stream");
+        return;
+    }
     const int64_t nchunks = (d + CW - 1) / CW;
     const int64_t warps = xf->B * nchunks;
     int64_t blocks = (warps + 7) / 8;
