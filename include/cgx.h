@@ -159,6 +159,10 @@ int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, dou
                           void* stream);
 
 /* ---- instrumentation ---------------------------------------------------------------- */
+/* Context options.  "fuse" (default 1): countgauss_apply on dense wide-row X runs the
+ * one-pass sketch+G+contraction kernel; 0 forces the two-stage path (S.X to HBM, then
+ * the Gaussian GEMM).  Both give the same S.X bits; Z agrees to rounding. */
+int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched so far. */
 uint64_t cgx_launch_count(const cgx_ctx* ctx);
 /* When enabled, the sketch (stage 1) and gemm (stage 2) kernels of every apply are

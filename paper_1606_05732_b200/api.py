@@ -106,6 +106,9 @@ class Context:
     def launches(self) -> int:
         return int(lib.cgx_launch_count(self.h))
 
+    def set_option(self, key: str, value: int):
+        check(lib.cgx_set_option(self.h, key.encode(), int(value)))
+
     def synchronize(self, stream=None):
         check(lib.cgx_synchronize(self.h, stream))
 

@@ -160,6 +160,30 @@ int64_t csr_chunk_rows(int64_t n, int64_t B, int64_t d) {
     return chunked ? chunk_rows : 0;
 }
 
+// Dense input -> device-resident row-major view (stages host X, transposes column-major X).
+const void* dense_rowmajor(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
+                           int64_t n, int64_t d, int x_mem, int64_t* rld_out, cudaStream_t s) {
+    const size_t es = dsize(dtype);
+    if (layout != CGX_COL_MAJOR && layout != CGX_ROW_MAJOR) fail(CGX_EINVAL, "cgx: bad layout");
+    if (n != xf->n)
+        fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
+                             std::to_string(xf->n));
+    if (d < 0) fail(CGX_EINVAL, "cgx: negative column count");
+    const int64_t minld = layout == CGX_COL_MAJOR ? n : d;
+    if (ld < std::max<int64_t>(minld, 1)) fail(CGX_EINVAL, "cgx: leading dimension too small");
+    if (d == 0) return x;
+    const size_t bytes = layout == CGX_COL_MAJOR ? es * (size_t)(ld * (d - 1) + n) : es * (size_t)(ld * (n - 1) + d);
+    const void* xd = to_device(ctx, ctx->hstage_dev, x, bytes, x_mem, s);
+    *rld_out = ld;
+    if (layout == CGX_COL_MAJOR) {
+        void* rm = ctx->xstage.get(es * (size_t)(n * d));
+        launch_transpose_x(ctx, xd, dtype, ld, n, d, rm, s);
+        xd = rm;
+        *rld_out = d;
+    }
+    return xd;
+}
+
 // Stage 1 (dense): SX row-major (B x d) into `sx_dev`.
 void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
                       int64_t n, int64_t d, int x_mem, double* sx_dev, cudaStream_t s) {
@@ -308,7 +332,8 @@ int cgx_free(cgx_ctx* ctx) {
         cudaSetDevice(ctx->device);
         cudaDeviceSynchronize();
         for (DevBuf* b : {&ctx->sx, &ctx->zpart, &ctx->xstage, &ctx->tmp, &ctx->sort_k[0], &ctx->sort_k[1],
-                          &ctx->sort_v[0], &ctx->sort_v[1], &ctx->sort_hist, &ctx->counts, &ctx->hstage_dev})
+                          &ctx->sort_v[0], &ctx->sort_v[1], &ctx->sort_hist, &ctx->counts, &ctx->hstage_dev,
+                          &ctx->sched})
             b->release();
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         for (int s = 0; s < 2; ++s)
@@ -632,8 +657,28 @@ int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x,
         need_mem(z_mem);
         need_g(xf);
         CallScope sc(ctx, stream);
+        int64_t rld = ld;
+        const void* xd = dense_rowmajor(ctx, xf, x, dtype, layout, ld, n, d, x_mem, &rld, sc.st);
+        if (d == 0) return;
+        // one-pass kernel (sketch + G generation + contraction) when the shape allows
+        if (!ctx->no_fuse) {
+            const size_t zb = sizeof(double) * (size_t)(xf->m * d);
+            double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
+            ctx->prof.begin(0, sc.st);
+            const bool fused = launch_countgauss_dense_fused(ctx, xf, xd, dtype, rld, d, zd, sc.st);
+            ctx->prof.end(0, sc.st);
+            if (fused) {
+                if (z_mem == CGX_MEM_HOST) {
+                    CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
+                    sc.sync();
+                }
+                return;
+            }
+        }
         double* sxd = (double*)ctx->sx.get(sizeof(double) * (size_t)(xf->B * d));
-        sketch_dense_dev(ctx, xf, x, dtype, layout, ld, n, d, x_mem, sxd, sc.st);
+        ctx->prof.begin(0, sc.st);
+        launch_sketch_dense(ctx, xf, xd, dtype, rld, n, d, sxd, sc.st);
+        ctx->prof.end(0, sc.st);
         finish_gemm(ctx, xf, sxd, d, z, z_mem, sc);
         if (x_mem == CGX_MEM_HOST) sc.sync();
     });
@@ -755,6 +800,21 @@ int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, dou
 }
 
 uint64_t cgx_launch_count(const cgx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!key) fail(CGX_EINVAL, "cgx_set_option: null key");
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+        const std::string k(key);
+        if (k == "fuse")
+            ctx->no_fuse = value == 0;
+        else if (k == "fuse_mode")
+            ctx->fuse_mode = (int)value;
+        else
+            fail(CGX_EINVAL, "cgx_set_option: unknown key '" + k + "'");
+    });
+}
 
 int cgx_profile_enable(cgx_ctx* ctx, int on) {
     return guard([&] {

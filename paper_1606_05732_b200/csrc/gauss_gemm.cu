@@ -148,7 +148,10 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
         sx, B, d, m, xf->g_seed, xf->g_explicit ? xf->g_dev : nullptr, b0, k_per_split, zpart);
     count_launch(ctx);
     check_launch("gauss_gemm");
-    const int64_t md = m * d;
+    launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
+}
+
+void launch_reduce_splits(cgx_ctx* ctx, const double* zpart, int64_t splits, int64_t md, double* z, cudaStream_t s) {
     int64_t blocks = (md + 255) / 256;
     if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
     reduce_splits<<<(unsigned)blocks, 256, 0, s>>>(zpart, splits, md, z);

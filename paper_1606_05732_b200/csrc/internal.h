@@ -51,9 +51,12 @@ struct cgx_ctx {
     cgx::DevBuf sx, zpart, xstage, tmp;     // scratch (tmp: scan.cu only)
     cgx::DevBuf sort_k[2], sort_v[2], sort_hist, counts;  // transform construction
     cgx::DevBuf hstage_dev;                 // device landing zone for host inputs
+    cgx::DevBuf sched;                      // work-queue counters of persistent kernels
     void* pinned = nullptr;                 // pinned staging for pageable host inputs
     size_t pinned_bytes = 0;
     cgx::Profile prof;
+    bool no_fuse = false;                   // option "fuse"=0: always run the two stages
+    int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps fused, 2 warp-specialized
 };
 
 struct cgx_xform {
@@ -82,6 +85,12 @@ void launch_fill_hash_sign(cgx_ctx* ctx, const cgx_xform* xf, int64_t* hash, dou
 // sketch_dense.cu: SX (row-major B x d, fp64) from row-major X.
 void launch_sketch_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int64_t ld, int64_t n,
                          int64_t d, double* sx, cudaStream_t s);
+// Whole countgauss_apply in one kernel (+ the partial reduction) for row-major X with
+// wide rows; false when the shape is not covered (caller runs the two stages).
+bool launch_countgauss_dense_fused(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int64_t ld,
+                                   int64_t d, double* z, cudaStream_t s);
+// Deterministic sum of `splits` column-major partials (gauss_gemm.cu).
+void launch_reduce_splits(cgx_ctx* ctx, const double* zpart, int64_t splits, int64_t md, double* z, cudaStream_t s);
 // col-major -> row-major copy of X (any dtype) into dst
 void launch_transpose_x(cgx_ctx* ctx, const void* x, int dtype, int64_t ld, int64_t n, int64_t d, void* dst,
                         cudaStream_t s);

@@ -165,7 +165,7 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
         if (CHUNKED) gpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(xf->B * d));
     }
     auto kern = sketch_csr_kernel<TV, TI, CHUNKED>;
-    if (smem > 48 * 1024) CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 40 * 1024) CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int64_t blocks = (xf->B + warps - 1) / warps;
     const int64_t cap = (int64_t)ctx->num_sms * 32;
     if (blocks > cap) blocks = cap;

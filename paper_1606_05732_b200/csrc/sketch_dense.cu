@@ -19,6 +19,8 @@
 // X must be row-major here (row stride ld); column-major inputs are first transposed on
 // the device (launch_transpose_x), because a gathered column-major row touches d
 // separate sectors.
+#include <cuda/barrier>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -129,34 +131,26 @@ __global__ void __launch_bounds__(256) sketch_dense_kernel(const T* __restrict__
     }
 }
 
-// Wide rows (one row chunk spans the warp): the streaming form.  A warp owns G
+// Wide rows (one row chunk spans the warp): the streaming form.  A warp owns nb <= 31
 // consecutive buckets, whose rows are one contiguous stretch of perm; it streams that
 // stretch 32 entries at a time (the next 32 perm entries prefetched while the current
-// rows are in flight), issues U row loads back to back (4 KB per warp in flight), and
-// adds them in order, flushing the accumulator to SX whenever the stretch crosses a
-// bucket boundary (bucket boundaries come from one coalesced load of the G+1 offsets).
-// Per row and lane: one shuffle, one load, one convert, one add -- the warp's
-// instruction stream no longer restarts per bucket, so rows keep flowing.
-template <typename T, int V>
-__global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restrict__ x, int64_t ld, int64_t d,
-                                                           const uint32_t* __restrict__ perm,
-                                                           const uint32_t* __restrict__ offsets, int64_t B,
-                                                           int64_t nchunks, int G, double* __restrict__ sx) {
-    constexpr int CW = 32 * V;
-    constexpr int U = 64 / (V * (int)sizeof(T));  // rows per load batch: 2 KB per warp
+// rows are in flight), issues U row loads back to back (2 KB per warp in flight), and
+// adds them in order, handing the accumulator to `sink(i, acc)` whenever the stretch
+// crosses the end of bucket b0+i (boundaries come from one coalesced load of the nb+1
+// offsets).  Signs are applied only after a batch's loads are all issued (a consumer of
+// a loaded register placed between the loads would serialize them), and a full chunk
+// with no boundary inside takes a branch-free path: per row and lane one shuffle, one
+// load, one sign flip, one convert, one add.
+template <typename T, int V, int INFLIGHT = 2048, typename Sink>
+__device__ __forceinline__ void stream_buckets(const T* __restrict__ x, int64_t ld, int64_t col0, bool colok,
+                                               const uint32_t* __restrict__ perm,
+                                               const uint32_t* __restrict__ offsets, int64_t b0, int nb,
+                                               Sink&& sink) {
+    constexpr int U = INFLIGHT / (32 * V * (int)sizeof(T));  // rows per load batch (INFLIGHT B per warp)
     const unsigned lane = threadIdx.x & 31;
-    const int64_t ngroups = (B + G - 1) / G;
-    const int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (task >= ngroups * nchunks) return;
-    const int64_t bg = task / nchunks;
-    const int64_t col0 = (task - bg * nchunks) * CW + (int64_t)lane * V;
-    const bool colok = col0 < d;
-    const int64_t b0 = bg * G;
-    const int nb = (int)min((int64_t)G, B - b0);
     const uint32_t offk = (int)lane <= nb ? __ldg(offsets + b0 + lane) : 0u;
     const uint32_t P0 = __shfl_sync(0xffffffffu, offk, 0);
     const uint32_t P1 = __shfl_sync(0xffffffffu, offk, nb);
-    double* out = sx + b0 * d + col0;
     int cur = 0;
     uint32_t nextb = __shfl_sync(0xffffffffu, offk, 1);
     double acc[V];
@@ -164,22 +158,23 @@ __global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restric
     for (int k = 0; k < V; ++k) acc[k] = 0.0;
 
     auto flush = [&]() {
-        if (colok) {
-#pragma unroll
-            for (int k = 0; k < V; ++k) out[(int64_t)cur * d + k] = acc[k];
-        }
+        sink(cur, acc);
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] = 0.0;
         ++cur;
         nextb = __shfl_sync(0xffffffffu, offk, min(cur + 1, 31));
     };
 
+    // per row: one shuffle, one IMAD.WIDE (row * row_bytes + column base), one load
+    const char* xcol = reinterpret_cast<const char*>(x + (colok ? col0 : 0));
+    const uint32_t row_bytes = (uint32_t)(ld * (int64_t)sizeof(T));  // host guarantees < 2^32
     uint32_t pe_next = P0 + lane < P1 ? __ldg(perm + P0 + lane) : 0u;
     for (uint32_t base = P0; base < P1; base += 32) {
         const uint32_t pe = pe_next;
         if (base + 32 + lane < P1) pe_next = __ldg(perm + base + 32 + lane);
         const int cnt = (int)min(32u, P1 - base);
         const uint32_t negmask = __ballot_sync(0xffffffffu, pe & kNegBit);  // bit t: row t negative
+        const uint32_t prow = pe & kRowMask;
         // common case: a full chunk with no bucket boundary inside -> branch-free adds
         const bool fast = cnt == 32 && nextb >= base + 32;
 #pragma unroll 1
@@ -187,15 +182,18 @@ __global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restric
             T v[U][V];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const uint32_t e = __shfl_sync(0xffffffffu, pe, (s0 + u) & 31);
-                load_vec<T, V>(x + (int64_t)(e & kRowMask) * ld + (colok ? col0 : 0), v[u]);
+                // padding rows read row 0 (a valid address) and are skipped when added
+                const uint32_t r = __shfl_sync(0xffffffffu, prow, (s0 + u) & 31);
+                load_vec<T, V>(reinterpret_cast<const T*>(xcol + (size_t)r * row_bytes), v[u]);
             }
             const uint32_t nm = negmask >> s0;
             if (fast) {
 #pragma unroll
                 for (int u = 0; u < U; ++u)
 #pragma unroll
-                    for (int k = 0; k < V; ++k) acc[k] += (double)flip_sign(v[u][k], (nm >> u) & 1u);
+                    for (int k = 0; k < V; ++k) {
+                        acc[k] += (double)flip_sign(v[u][k], (nm >> u) & 1u);
+                    }
             } else {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -203,13 +201,164 @@ __global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restric
                         const uint32_t pos = base + s0 + u;
                         while (pos == nextb) flush();
 #pragma unroll
-                        for (int k = 0; k < V; ++k) acc[k] += (double)flip_sign(v[u][k], (nm >> u) & 1u);
+                        for (int k = 0; k < V; ++k) {
+                        acc[k] += (double)flip_sign(v[u][k], (nm >> u) & 1u);
+                        }
                     }
                 }
             }
         }
     }
     while (cur < nb) flush();
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restrict__ x, int64_t ld, int64_t d,
+                                                              const uint32_t* __restrict__ perm,
+                                                              const uint32_t* __restrict__ offsets, int64_t B,
+                                                              int64_t nchunks, int G, double* __restrict__ sx,
+                                                              unsigned* __restrict__ next_task) {
+    // Persistent warps pull (bucket group, column chunk) tasks from a counter: no warp
+    // idles while a slow sibling holds its CTA slot.  Every bucket is still summed by one
+    // warp in ascending row order, so S.X does not depend on the assignment.
+    constexpr int CW = 32 * V;
+    const unsigned lane = threadIdx.x & 31;
+    const int64_t ngroups = (B + G - 1) / G;
+    const int64_t ntasks = ngroups * nchunks;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(next_task, 1u);
+        const int64_t task = __shfl_sync(0xffffffffu, t, 0);
+        if (task >= ntasks) break;
+        const int64_t bg = task / nchunks;
+        const int64_t col0 = (task - bg * nchunks) * CW + (int64_t)lane * V;
+        const bool colok = col0 < d;
+        const int64_t b0 = bg * G;
+        const int nb = (int)min((int64_t)G, B - b0);
+        double* out = sx + b0 * d + col0;
+        stream_buckets<T, V>(x, ld, col0, colok, perm, offsets, b0, nb, [&](int i, const double (&acc)[V]) {
+            if (colok) {
+#pragma unroll
+                for (int k = 0; k < V; ++k) out[(int64_t)i * d + k] = acc[k];
+            }
+        });
+    }
+}
+
+// countgauss_apply in one pass (dense, wide rows): sketch + G generation + G.(S.X).
+// A persistent CTA of 8 warps takes bucket tiles of 8*Gw consecutive buckets (static
+// round-robin, so the summation grouping -- and Z -- is deterministic).  Each warp
+// streams Gw buckets (stream_buckets) into the tile's S.X slab in shared memory and
+// generates the m x Gw slab of G for its buckets (SplitMix64 + Acklam + Halley, the
+// reference's quantile) -- FP64 work that hides under the other warps' HBM traffic.
+// After a CTA barrier, warp w adds G[rows_w, tile] . SX[tile, :] into its own Z rows
+// (RW = ceil(m/8) rows x V columns per lane, kept in registers across tiles) in a fixed
+// order.  At the end each CTA writes its m x d partial; reduce_splits sums the partials
+// in CTA order.  G and S.X never touch HBM; X is read exactly once.
+template <typename T, int V, int RW>
+__global__ void __launch_bounds__(256, 4) countgauss_dense_fused(const T* __restrict__ x, int64_t ld, int64_t d,
+                                                                 const uint32_t* __restrict__ perm,
+                                                                 const uint32_t* __restrict__ offsets, int64_t B,
+                                                                 int64_t m, uint64_t g_seed,
+                                                                 const double* __restrict__ g_explicit, int Gw,
+                                                                 double* __restrict__ zpart) {
+    constexpr int CW = 32 * V;
+    extern __shared__ double fsm[];
+    __shared__ cuda::barrier<cuda::thread_scope_block> full[2], freed[2];
+    const int TB = 8 * Gw;                           // buckets per tile
+    const int slab_sz = TB * CW + (int)m * TB;       // S.X [TB][CW] then G [m][TB]
+    double* sZ = fsm + 2 * slab_sz;                  // [m][CW]: Z rows, each owned by one warp
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t col0 = (int64_t)lane * V;
+    const bool colok = col0 < d;
+    const int64_t ntiles = (B + TB - 1) / TB;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            init(&full[i], blockDim.x);
+            init(&freed[i], blockDim.x);
+        }
+    }
+    for (int e = threadIdx.x; e < (int)m * CW; e += blockDim.x) sZ[e] = 0.0;
+    __syncthreads();
+    cuda::barrier<cuda::thread_scope_block>::arrival_token tok_full[2], tok_freed[2];
+
+    // Z rows of this warp += G[rows, tile] . SX[tile, my columns]   (fixed order)
+    auto consume = [&](int buf) {
+        const double* sSX = fsm + buf * slab_sz;
+        const double* sG = sSX + TB * CW;
+#pragma unroll
+        for (int rr = 0; rr < RW; ++rr) {
+            const int r = (int)warp * RW + rr;
+            if (r < m) {
+                const double* grow = sG + (int64_t)r * TB;
+                double zr[V];
+#pragma unroll
+                for (int k = 0; k < V; ++k) zr[k] = sZ[r * CW + lane * V + k];
+                for (int s = 0; s < TB; ++s) {
+                    const double gv = grow[s];
+#pragma unroll
+                    for (int k = 0; k < V; ++k) zr[k] = fma(gv, sSX[s * CW + lane * V + k], zr[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < V; ++k) sZ[r * CW + lane * V + k] = zr[k];
+            }
+        }
+    };
+
+    int64_t k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int buf = (int)(k & 1);
+        if (k >= 2) freed[buf].wait(std::move(tok_freed[buf]));  // slab buf consumed (tile k-2)
+        double* sSX = fsm + buf * slab_sz;
+        double* sG = sSX + TB * CW;
+        const int64_t tb0 = tile * TB;
+        const int64_t b0 = tb0 + (int64_t)warp * Gw;
+        const int nb = b0 < B ? (int)min((int64_t)Gw, B - b0) : 0;
+        // S.X rows of this warp's buckets -> shared slab (zero rows for absent buckets)
+        double* slab = sSX + (int64_t)warp * Gw * CW + lane * V;
+        if (nb > 0) {
+            stream_buckets<T, V>(x, ld, col0, colok, perm, offsets, b0, nb, [&](int i, const double (&acc)[V]) {
+#pragma unroll
+                for (int k = 0; k < V; ++k) slab[i * CW + k] = colok ? acc[k] : 0.0;
+            });
+        }
+        for (int i = nb; i < Gw; ++i)
+#pragma unroll
+            for (int k = 0; k < V; ++k) slab[i * CW + k] = 0.0;
+        // G[:, b0 .. b0+Gw) -> sG[r][warp*Gw + i]  (zero for absent buckets / rows)
+        for (int e = lane; e < m * Gw; e += 32) {
+            const int i = e / (int)m, r = e - i * (int)m;
+            const int64_t b = b0 + i;
+            double g = 0.0;
+            if (i < nb) g = g_explicit ? g_explicit[b * m + r] : gauss_entry(g_seed, (uint64_t)m, (uint64_t)r, (uint64_t)b);
+            sG[(int64_t)r * TB + warp * Gw + i] = g;
+        }
+        tok_full[buf] = full[buf].arrive();
+        // Deferred by one tile: the previous slab is (nearly always) complete by now, so
+        // warps rarely wait here and never idle at a full CTA barrier.
+        if (k >= 1) {
+            const int pb = buf ^ 1;
+            full[pb].wait(std::move(tok_full[pb]));
+            consume(pb);
+            tok_freed[pb] = freed[pb].arrive();
+        }
+    }
+    if (k >= 1) {
+        const int lb = (int)((k - 1) & 1);
+        full[lb].wait(std::move(tok_full[lb]));
+        consume(lb);
+    }
+    __syncwarp();
+    // partial Z of this CTA, column-major m x d (each warp writes the rows it owns)
+    double* zp = zpart + (int64_t)blockIdx.x * m * d;
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+        const int r = (int)warp * RW + rr;
+        if (r < m && colok) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) zp[(col0 + k) * m + r] = sZ[r * CW + lane * V + k];
+        }
+    }
 }
 
 template <typename E>
@@ -247,16 +396,21 @@ template <typename T, int V, int R>
 void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* sx, int accumulate,
             cudaStream_t s) {
     constexpr int CW = (32 / R) * V;
-    if (R == 1 && !accumulate) {
+    if (R == 1 && !accumulate && ld * (int64_t)sizeof(T) < ((int64_t)1 << 32)) {
         // ~1K rows per warp task, at most 31 buckets (one offsets load)
         const int64_t rows_per_bucket = xf->n / xf->B + 1;
         int64_t G = 1024 / rows_per_bucket;
         G = G < 1 ? 1 : (G > 31 ? 31 : G);
         const int64_t nchunks = (d + CW - 1) / CW;
         const int64_t tasks = (xf->B + G - 1) / G * nchunks;
-        const int64_t blocks = (tasks + 7) / 8;
-        sketch_dense_stream<T, V><<<(unsigned)blocks, 256, 0, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks,
-                                                                   (int)G, sx);
+        auto kern = sketch_dense_stream<T, V>;
+        int per_sm = 0;
+        CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+        int64_t blocks = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);
+        if (blocks > (tasks + 7) / 8) blocks = (tasks + 7) / 8;
+        unsigned* ctr = (unsigned*)ctx->sched.get(sizeof(unsigned));
+        CGX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+        kern<<<(unsigned)blocks, 256, 0, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks, (int)G, sx, ctr);
         count_launch(ctx);
         check_launch("sketch_dense_stream");
         return;
@@ -291,7 +445,200 @@ void dispatch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t
     return launch<T, 1, 32>(ctx, xf, x, ld, d, sx, accumulate, s);
 }
 
+// Warp-specialized one-pass countgauss_apply.  CTA = 8 sketch warps + 4 math warps.
+//  * sketch warps only stream X (4 KB of row loads in flight per warp) and deposit each
+//    bucket's S.X row into a double-buffered shared slab; they never stop to compute,
+//    so the CTA's HBM request stream stays full;
+//  * math warps generate the m x TB slab of G for the tile ahead of time (G does not
+//    depend on X), wait for the tile's S.X slab, and accumulate Z += G_tile . SX_tile
+//    into registers (MR rows x V columns per thread), fixed order -> deterministic.
+// Hand-off: mbarrier `full[buf]` (256 sketch arrivals) and `freed[buf]` (128 math
+// arrivals) per slab; a named barrier orders the math warps' G slab reuse.
+template <typename T, int V, int MR>
+__global__ void __launch_bounds__(384, 2) countgauss_dense_ws(const T* __restrict__ x, int64_t ld, int64_t d,
+                                                              const uint32_t* __restrict__ perm,
+                                                              const uint32_t* __restrict__ offsets, int64_t B,
+                                                              int64_t m, uint64_t g_seed,
+                                                              const double* __restrict__ g_explicit, int Gw,
+                                                              double* __restrict__ zpart) {
+    constexpr int CW = 32 * V;
+    extern __shared__ double fsm[];
+    __shared__ uint64_t full[2], freed[2];
+    const int TB = 8 * Gw;
+    const int slab_sz = TB * CW + (int)m * TB;  // S.X [TB][CW], then G [m][TB]
+    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ntiles = (B + TB - 1) / TB;
+    if (tid == 0) {
+        mbar_init(&full[0], 256);
+        mbar_init(&full[1], 256);
+        mbar_init(&freed[0], 128);
+        mbar_init(&freed[1], 128);
+    }
+    __syncthreads();
+
+    if (warp < 8) {  // ---------------------------------------------------------- sketch
+        const int64_t col0 = (int64_t)lane * V;
+        const bool colok = col0 < d;
+        int64_t k = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+            const int buf = (int)(k & 1);
+            if (k >= 2) mbar_wait(&freed[buf], (unsigned)(((k - 2) >> 1) & 1));
+            double* slab = fsm + buf * slab_sz + (int64_t)warp * Gw * CW + lane * V;
+            const int64_t b0 = tile * TB + (int64_t)warp * Gw;
+            const int nb = b0 < B ? (int)min((int64_t)Gw, B - b0) : 0;
+            if (nb > 0) {
+                stream_buckets<T, V, 4096>(x, ld, col0, colok, perm, offsets, b0, nb,
+                                           [&](int i, const double (&acc)[V]) {
+#pragma unroll
+                                               for (int q = 0; q < V; ++q) slab[i * CW + q] = colok ? acc[q] : 0.0;
+                                           });
+            }
+            for (int i = nb; i < Gw; ++i)
+#pragma unroll
+                for (int q = 0; q < V; ++q) slab[i * CW + q] = 0.0;
+            mbar_arrive(&full[buf]);
+        }
+        return;
+    }
+    // ------------------------------------------------------------------------------ math
+    const unsigned mt = tid - 256, mw = mt >> 5;  // 128 threads, 4 warps
+    double z[MR][V];
+#pragma unroll
+    for (int q = 0; q < MR; ++q)
+#pragma unroll
+        for (int c = 0; c < V; ++c) z[q][c] = 0.0;
+    int64_t k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int buf = (int)(k & 1);
+        const double* sSX = fsm + buf * slab_sz;
+        double* sG = fsm + buf * slab_sz + TB * CW;
+        const int64_t tb0 = tile * TB;
+        for (int e = (int)mt; e < (int)m * TB; e += 128) {
+            const int s = e / (int)m, r = e - s * (int)m;
+            const int64_t b = tb0 + s;
+            double g = 0.0;
+            if (b < B) g = g_explicit ? g_explicit[b * m + r] : gauss_entry(g_seed, (uint64_t)m, (uint64_t)r, (uint64_t)b);
+            sG[r * TB + s] = g;
+        }
+        named_sync(1, 128);
+        mbar_wait(&full[buf], (unsigned)((k >> 1) & 1));
+        for (int s = 0; s < TB; ++s) {
+            double sx[V];
+#pragma unroll
+            for (int c = 0; c < V; ++c) sx[c] = sSX[s * CW + lane * V + c];
+#pragma unroll
+            for (int q = 0; q < MR; ++q) {
+                const int r = (int)mw + 4 * q;
+                if (r < m) {
+                    const double g = sG[r * TB + s];
+#pragma unroll
+                    for (int c = 0; c < V; ++c) z[q][c] = fma(g, sx[c], z[q][c]);
+                }
+            }
+        }
+        mbar_arrive(&freed[buf]);
+    }
+    double* zp = zpart + (int64_t)blockIdx.x * m * d;
+#pragma unroll
+    for (int q = 0; q < MR; ++q) {
+        const int r = (int)mw + 4 * q;
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+            const int64_t col = (int64_t)lane * V + c;
+            if (r < m && col < d) zp[col * m + r] = z[q][c];
+        }
+    }
+}
+
+template <typename T, int V, int MR>
+void launch_ws(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
+    constexpr int CW = 32 * V;
+    const int64_t B = xf->B, m = xf->m;
+    auto kern = countgauss_dense_ws<T, V, MR>;
+    int64_t Gw = B / (64 * (int64_t)ctx->num_sms * 2);
+    Gw = Gw < 1 ? 1 : (Gw > 8 ? 8 : Gw);
+    const int64_t TB = 8 * Gw;
+    const int64_t ntiles = (B + TB - 1) / TB;
+    const size_t smem = sizeof(double) * (size_t)(2 * (TB * CW + m * TB));
+    CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 384, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid_cap = (int64_t)ctx->num_sms * per_sm;
+    const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
+    double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(grid * m * d));
+    kern<<<(unsigned)grid, 384, smem, s>>>(x, ld, d, xf->perm, xf->offsets, B, m, xf->g_seed,
+                                           xf->g_explicit ? xf->g_dev : nullptr, (int)Gw, zpart);
+    count_launch(ctx);
+    check_launch("countgauss_dense_ws");
+    launch_reduce_splits(ctx, zpart, grid, m * d, z, s);
+}
+
+template <typename T, int V, int RW>
+void launch_fused(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
+    constexpr int CW = 32 * V;
+    const int64_t B = xf->B, m = xf->m;
+    auto kern = countgauss_dense_fused<T, V, RW>;
+    // persistent grid: every CTA resident (occupancy-limited), >= ~8 tiles per CTA
+    int64_t Gw = B / (64 * (int64_t)ctx->num_sms * 4);
+    Gw = Gw < 1 ? 1 : (Gw > 8 ? 8 : Gw);
+    const int64_t TB = 8 * Gw;
+    const int64_t ntiles = (B + TB - 1) / TB;
+    const size_t smem = sizeof(double) * (size_t)(2 * (TB * CW + m * TB) + m * CW);
+    CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid_cap = (int64_t)ctx->num_sms * per_sm;
+    const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
+    double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(grid * m * d));
+    kern<<<(unsigned)grid, 256, smem, s>>>(x, ld, d, xf->perm, xf->offsets, B, m, xf->g_seed,
+                                           xf->g_explicit ? xf->g_dev : nullptr, (int)Gw, zpart);
+    count_launch(ctx);
+    check_launch("countgauss_dense_fused");
+    launch_reduce_splits(ctx, zpart, grid, m * d, z, s);
+}
+
+template <typename T, int V>
+bool fused_rw(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
+    const int64_t m = xf->m;
+    if (ctx->fuse_mode == 2) {  // warp-specialized
+        if (m <= 4) return launch_ws<T, V, 1>(ctx, xf, x, ld, d, z, s), true;
+        if (m <= 8) return launch_ws<T, V, 2>(ctx, xf, x, ld, d, z, s), true;
+        if (m <= 16) return launch_ws<T, V, 4>(ctx, xf, x, ld, d, z, s), true;
+        if constexpr (V <= 2) {
+            if (m <= 32) return launch_ws<T, V, 8>(ctx, xf, x, ld, d, z, s), true;
+        }
+        if constexpr (V == 1) {
+            if (m <= 64) return launch_ws<T, V, 16>(ctx, xf, x, ld, d, z, s), true;
+        }
+    }
+    if (m <= 8) return launch_fused<T, V, 1>(ctx, xf, x, ld, d, z, s), true;
+    if (m <= 16) return launch_fused<T, V, 2>(ctx, xf, x, ld, d, z, s), true;
+    if (m <= 32) return launch_fused<T, V, 4>(ctx, xf, x, ld, d, z, s), true;
+    if (V <= 2 && m <= 64) return launch_fused<T, V, 8>(ctx, xf, x, ld, d, z, s), true;
+    if (V == 1 && m <= 128) return launch_fused<T, V, 16>(ctx, xf, x, ld, d, z, s), true;
+    return false;
+}
+
+template <typename T>
+bool fused_dispatch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
+    auto aligned = [&](int v) { return ((uintptr_t)x % (sizeof(T) * v)) == 0 && ld % v == 0 && d % v == 0; };
+    if (d < 17) return false;  // narrow rows: several rows per warp load, two-stage path
+    if (ld * (int64_t)sizeof(T) >= ((int64_t)1 << 32)) return false;  // 32-bit row pitch in stream_buckets
+    if (d <= 32) return fused_rw<T, 1>(ctx, xf, x, ld, d, z, s);
+    if (d <= 64 && aligned(2)) return fused_rw<T, 2>(ctx, xf, x, ld, d, z, s);
+    if (sizeof(T) == 4 && d <= 128 && aligned(4)) return fused_rw<T, (sizeof(T) == 4 ? 4 : 2)>(ctx, xf, x, ld, d, z, s);
+    return false;
+}
+
 } // namespace
+
+bool launch_countgauss_dense_fused(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int64_t ld,
+                                   int64_t d, double* z, cudaStream_t s) {
+    if (dtype == CGX_F32) return fused_dispatch<float>(ctx, xf, (const float*)x, ld, d, z, s);
+    return fused_dispatch<double>(ctx, xf, (const double*)x, ld, d, z, s);
+}
 
 void launch_sketch_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int64_t ld, int64_t n,
                          int64_t d, double* sx, cudaStream_t s) {

@@ -300,6 +300,39 @@ def test_device_tensors_match_host(cg, restatement):
     assert np.array_equal(cg.countsketch_apply(t, xs).cpu().numpy(), sx_ref)
 
 
+@pytest.mark.parametrize("d,m,dtype", [(32, 64, np.float32), (24, 16, np.float32), (64, 32, np.float32),
+                                       (128, 32, np.float32), (100, 8, np.float32), (32, 64, np.float64),
+                                       (64, 64, np.float64), (40, 100, np.float32), (33, 5, np.float64)])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fused_matches_two_stage(cg, restatement, d, m, dtype, mode):
+    """The one-pass kernels (sketch + G + contraction; mode 1 all-warps, mode 2
+    warp-specialized) vs the two-stage path and the oracle."""
+    import torch
+
+    rng = np.random.default_rng(d * 1000 + m)
+    n, B = 40000, 777
+    x = rng.standard_normal((n, d)).astype(dtype)
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(d + m))
+    ctx = cg.context()
+    xd = torch.from_numpy(x).cuda()
+    ctx.set_option("fuse_mode", mode)
+    try:
+        z_fused = cg.countgauss_apply(t, xd).cpu().numpy()
+        z_again = cg.countgauss_apply(t, xd).cpu().numpy()
+    finally:
+        ctx.set_option("fuse_mode", 2)
+    ctx.set_option("fuse", 0)
+    try:
+        z_two = cg.countgauss_apply(t, xd).cpu().numpy()
+    finally:
+        ctx.set_option("fuse", 1)
+    z_ref, _ = restatement.countgauss(d + m, m, B, x=x)
+    assert np.array_equal(z_fused, z_again)  # deterministic
+    assert rel_fro(z_fused, z_ref) <= Z_TOL
+    assert rel_fro(z_two, z_ref) <= Z_TOL
+    assert rel_fro(z_fused, z_two) <= Z_TOL
+
+
 def test_deterministic_across_runs(cg):
     rng = np.random.default_rng(12)
     x = rng.standard_normal((50000, 24))
