@@ -92,6 +92,9 @@ class ClockSampler:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # the timed region starts only once sampling is live
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -111,7 +114,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        for line in self.lines[1:]:  # lines[0] was taken before the timed region began
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -159,7 +162,9 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     c = CONFIGS[args.config]
-    r = cpu_reference_run(args.config, c, args.steps, args.warmup)
+    # each CPU step is a full c2 countgauss_apply (~0.1-0.3 s on a multi-core host): bound
+    # the sample so the whole arm ends within a few minutes
+    r = cpu_reference_run(args.config, c, min(args.steps, 20), min(max(args.warmup, 1), 2))
     line = {
         "metric": METRIC, "impl": "reference", "value": r["value"], "unit": "nnz/s", "n_gpus": args.gpus,
         "steps": len(r["ms"]), "warmup": args.warmup, "ms_per_step": r["median_ms"], "higher_is_better": True,
@@ -346,7 +351,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))

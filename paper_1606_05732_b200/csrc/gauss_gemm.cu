@@ -98,11 +98,25 @@ __global__ void __launch_bounds__(256) gauss_gemm_kernel(const double* __restric
             }
 }
 
-__global__ void reduce_splits(const double* __restrict__ zpart, int64_t splits, int64_t md, double* __restrict__ z) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < md; e += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int64_t k = 0; k < splits; ++k) s += zpart[k * md + e];
-        z[e] = s;
+// z[e] = sum_k zpart[k][e].  Block = 32 entries x 16 split groups: group g sums splits
+// g, g+16, ... in order, then the 16 group sums are added in group order -- a fixed
+// association, so Z is bit-reproducible; loads stay coalesced along e.
+constexpr int kRedGroups = 16;
+__global__ void __launch_bounds__(32 * kRedGroups) reduce_splits(const double* __restrict__ zpart, int64_t splits,
+                                                                 int64_t md, double* __restrict__ z) {
+    __shared__ double part[kRedGroups][33];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (e < md)
+        for (int64_t k = g; k < splits; k += kRedGroups) s += zpart[k * md + e];
+    part[g][lane] = s;
+    __syncthreads();
+    if (g == 0 && e < md) {
+        double t = part[0][lane];
+#pragma unroll
+        for (int q = 1; q < kRedGroups; ++q) t += part[q][lane];
+        z[e] = t;
     }
 }
 
@@ -152,9 +166,8 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
 }
 
 void launch_reduce_splits(cgx_ctx* ctx, const double* zpart, int64_t splits, int64_t md, double* z, cudaStream_t s) {
-    int64_t blocks = (md + 255) / 256;
-    if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
-    reduce_splits<<<(unsigned)blocks, 256, 0, s>>>(zpart, splits, md, z);
+    const int64_t blocks = (md + 31) / 32;
+    reduce_splits<<<(unsigned)blocks, 32 * kRedGroups, 0, s>>>(zpart, splits, md, z);
     count_launch(ctx);
     check_launch("reduce_splits");
 }
