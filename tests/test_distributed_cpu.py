@@ -1,0 +1,78 @@
+"""CPU, world_size 2 over gloo: the multi-GPU host logic (paper_1606_05732_b200/distributed.py)
+-- contiguous row shards, per-rank transforms from the shared seed over *global* row
+indices, and both combine modes ("z": all-reduce of Z; "sx": bucket-range
+reduce-scatter of S.X, split-K stage 2, all-reduce) -- reproduces the single-device T.X.
+The per-rank compute is the oracle here (no GPU); on the box it is libcgx."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1606_05732_b200.distributed import bucket_range, combine, shard_range
+
+N, D, B, M, SEED = 5003, 7, 67, 5, 424242
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem():
+    rng = np.random.default_rng(0)
+    return rng.standard_normal((N, D))
+
+
+def _worker(rank, world, port, mode, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    O = oracle.Restatement()
+    x = _problem()
+    r0, r1 = shard_range(N, world, rank)
+    _, cs_seed, g_seed = O.countgauss_seeds(SEED)
+    h, s = O.hash_sign(cs_seed, B, r1 - r0, i0=r0)  # global row indices, shared seed
+    sx_p = O.sketch_dense(h, s, B, x[r0:r1])  # (B, D) partial
+    if mode == "z":
+        G = O.gaussian(g_seed, M, B)
+        z = torch.from_numpy(np.ascontiguousarray(O.gemm(G, sx_p)))
+        z = combine("z", world=world, rank=rank, B=B, d=D, partial_z=z)
+    else:
+        def stage2(sx_slice, b0, b1):
+            if b1 <= b0:
+                return torch.zeros((M, D), dtype=torch.float64)
+            Gs = O.gaussian(g_seed, M, b1 - b0, c0=b0)
+            return torch.from_numpy(np.ascontiguousarray(O.gemm(Gs, sx_slice.numpy())))
+        z = combine("sx", world=world, rank=rank, B=B, d=D,
+                    partial_sx=torch.from_numpy(np.ascontiguousarray(sx_p)), stage2=stage2)
+    if rank == 0:
+        np.save(out_path, z.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["z", "sx"])
+def test_two_rank_combine_matches_single_device(tmp_path, mode):
+    out = str(tmp_path / f"z_{mode}.npy")
+    mp.spawn(_worker, args=(2, _free_port(), mode, out), nprocs=2, join=True)
+    z = np.load(out)
+    z_ref, _ = oracle.Restatement().countgauss(SEED, M, B, x=_problem())
+    assert np.linalg.norm(z - z_ref) / np.linalg.norm(z_ref) <= 1e-13
+
+
+def test_shard_ranges_cover_rows():
+    for n in (1, 7, 5003, 1 << 24):
+        for w in (1, 2, 3, 8):
+            spans = [shard_range(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+    assert bucket_range(65536, 8, 7) == (57344, 65536)
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
