@@ -120,6 +120,78 @@ __global__ void __launch_bounds__(32 * kRedGroups) reduce_splits(const double* _
     }
 }
 
+// Wide tile: a CTA owns WM rows of Z and ALL d (<= 1024) columns for a K-range, so each
+// G(r, c) is generated exactly once over the whole grid (the narrow kernel above
+// regenerates G once per 32-column tile -- 8x for d = 256).  The WM x d tile is
+// (WM/8) x (dp/8) m8n8k4 fragments spread over the 8 warps (<= 16 per warp, 2 fp64
+// accumulators each).  Per K-chunk: 256 threads generate WM x KW normals into smem, the
+// KW x d slab of S.X is staged in smem, then every warp issues its DMMAs.
+template <int WM, int KW>
+__global__ void __launch_bounds__(256, 2) gauss_gemm_wide(const double* __restrict__ sx, int64_t B, int64_t d, int64_t m,
+                                                       uint64_t g_seed, const double* __restrict__ g_explicit,
+                                                       int64_t gcol0, int64_t k_per_split, double* __restrict__ zpart) {
+    extern __shared__ double wsm[];
+    const int dp = (int)((d + 7) & ~7);
+    double* Gs = wsm;                      // [WM][KW + 1]
+    double* Ss = wsm + WM * (KW + 1);      // [KW][dp + 1]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int RF = WM / 8, F = RF * (dp / 8);
+    const int64_t m0 = (int64_t)blockIdx.x * WM;
+    const int64_t split = blockIdx.y;
+    const int64_t kb = split * k_per_split, ke = min(B, kb + k_per_split);
+    double acc[16][2];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q][0] = acc[q][1] = 0.0;
+
+    for (int64_t k0 = kb; k0 < ke; k0 += KW) {
+#pragma unroll 1
+        for (int e = tid; e < WM * KW; e += 256) {
+            const int r = e % WM, c = e / WM;
+            const int64_t gr = m0 + r, gc = k0 + c;
+            double g = 0.0;
+            if (gr < m && gc < ke) {
+                const int64_t col = gcol0 + gc;
+                g = g_explicit ? g_explicit[col * m + gr] : gauss_entry(g_seed, (uint64_t)m, (uint64_t)gr, (uint64_t)col);
+            }
+            Gs[r * (KW + 1) + c] = g;
+        }
+        for (int e = tid; e < KW * dp; e += 256) {
+            const int c = e % dp, r = e / dp;
+            const int64_t gk = k0 + r;
+            Ss[r * (dp + 1) + c] = (gk < ke && c < d) ? sx[gk * d + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int kk = 0; kk < KW; kk += 4) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int f = warp + 8 * q;
+                if (f < F) {
+                    const int rf = f % RF, cf = f / RF;
+                    const double a = Gs[(rf * 8 + (lane >> 2)) * (KW + 1) + kk + (lane & 3)];
+                    const double b = Ss[(kk + (lane & 3)) * (dp + 1) + cf * 8 + (lane >> 2)];
+                    dmma884(acc[q][0], acc[q][1], a, b);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double* zp = zpart + split * m * d;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int f = warp + 8 * q;
+        if (f < F) {
+            const int rf = f % RF, cf = f / RF;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t r = m0 + rf * 8 + (lane >> 2);
+                const int64_t c = (int64_t)cf * 8 + (lane & 3) * 2 + h;
+                if (r < m && c < d) zp[c * m + r] = acc[q][h];
+            }
+        }
+    }
+}
+
 __global__ void fill_gaussian_kernel(uint64_t g_seed, int64_t m, int64_t total, double* g) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = e / m, r = e - c * m;
@@ -146,6 +218,37 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
     const int64_t m = xf->m, B = b1 - b0;
     if (B <= 0) {
         CGX_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)(m * d), s));
+        return;
+    }
+    if (d <= 1024) {
+        // wide tile: WM rows x all columns, WM * dp <= 8192 (<= 16 fragments per warp)
+        const int64_t dp = (d + 7) & ~int64_t(7);
+        const int WM = dp <= 128 ? 64 : dp <= 256 ? 32 : dp <= 512 ? 16 : 8;
+        const int KW = dp <= 512 ? 32 : 16;
+        const int64_t tm = (m + WM - 1) / WM;
+        const int64_t kchunks = (B + KW - 1) / KW;
+        int64_t want = (2 * (int64_t)ctx->num_sms + tm - 1) / tm;
+        want = want < 1 ? 1 : (want > kchunks ? kchunks : (want > 65535 ? 65535 : want));
+        const int64_t k_per_split = (kchunks + want - 1) / want * KW;
+        const int64_t splits = (B + k_per_split - 1) / k_per_split;
+        const size_t smem = sizeof(double) * (size_t)(WM * (KW + 1) + KW * (dp + 1));
+        double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
+        const double* gex = xf->g_explicit ? xf->g_dev : nullptr;
+        const dim3 grid((unsigned)tm, (unsigned)splits);
+#define CGX_WIDE(WM_, KW_)                                                                                       \
+    do {                                                                                                         \
+        auto kern = gauss_gemm_wide<WM_, KW_>;                                                                   \
+        CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));          \
+        kern<<<grid, 256, smem, s>>>(sx, B, d, m, xf->g_seed, gex, b0, k_per_split, zpart);                     \
+    } while (0)
+        if (WM == 64) CGX_WIDE(64, 32);
+        else if (WM == 32) CGX_WIDE(32, 32);
+        else if (WM == 16) CGX_WIDE(16, 32);
+        else CGX_WIDE(8, 16);
+#undef CGX_WIDE
+        count_launch(ctx);
+        check_launch("gauss_gemm_wide");
+        launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
         return;
     }
     const int64_t tm = (m + MT - 1) / MT, tn = (d + NT - 1) / NT;
