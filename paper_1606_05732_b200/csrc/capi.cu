@@ -43,6 +43,31 @@ void* DevBuf::get(size_t need) {
     return p;
 }
 
+void* pool_alloc(cgx_ctx* ctx, size_t bytes) {
+    size_t cls = 256;
+    while (cls < bytes) cls <<= 1;
+    auto& fl = ctx->pool_free[cls];
+    if (!fl.empty()) {
+        void* p = fl.back();
+        fl.pop_back();
+        return p;
+    }
+    void* p = nullptr;
+    CGX_CUDA(cudaMalloc(&p, cls));
+    ctx->pool_class[p] = cls;
+    return p;
+}
+
+void pool_free(cgx_ctx* ctx, void* p) {
+    if (!p) return;
+    auto it = ctx->pool_class.find(p);
+    if (it == ctx->pool_class.end()) {
+        cudaFree(p);
+        return;
+    }
+    ctx->pool_free[it->second].push_back(p);
+}
+
 void DevBuf::release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -132,21 +157,24 @@ cgx_xform* new_xform(cgx_ctx* ctx, int64_t B, int64_t n) {
     xf->B = B;
     xf->n = n;
     try {
-        CGX_CUDA(cudaMalloc((void**)&xf->perm, sizeof(uint32_t) * (size_t)n));
-        CGX_CUDA(cudaMalloc((void**)&xf->offsets, sizeof(uint32_t) * (size_t)(B + 1)));
+        xf->perm = (uint32_t*)pool_alloc(ctx, sizeof(uint32_t) * (size_t)n);
+        xf->offsets = (uint32_t*)pool_alloc(ctx, sizeof(uint32_t) * (size_t)(B + 1));
     } catch (...) {
-        if (xf->perm) cudaFree(xf->perm);
+        pool_free(ctx, xf->perm);
         delete xf;
         throw;
     }
     return xf;
 }
 
+// Caller holds ctx->mu.  The device is drained first: kernels of this (or a failed)
+// call may still read xf's arrays, and pooled blocks are reused immediately.
 void free_xform(cgx_xform* xf) {
     if (!xf) return;
-    if (xf->ctx) cudaSetDevice(xf->ctx->device);
-    if (xf->perm) cudaFree(xf->perm);
-    if (xf->offsets) cudaFree(xf->offsets);
+    cudaSetDevice(xf->ctx->device);
+    cudaDeviceSynchronize();
+    pool_free(xf->ctx, xf->perm);
+    pool_free(xf->ctx, xf->offsets);
     if (xf->g_dev) cudaFree(xf->g_dev);
     delete xf;
 }
@@ -288,15 +316,25 @@ void place_sx(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_dev, int64_t d
 
 void build_explicit(cgx_ctx* ctx, cgx_xform* xf, const int64_t* hash, const double* sign, int mem, CallScope& sc) {
     const int64_t n = xf->n;
-    const int64_t* hd = (const int64_t*)to_device(ctx, ctx->hstage_dev, hash, sizeof(int64_t) * (size_t)n, mem, sc.st);
-    const double* sd = (const double*)to_device(ctx, ctx->xstage, sign, sizeof(double) * (size_t)n, mem, sc.st);
     uint32_t* keys = (uint32_t*)ctx->sx.get(sizeof(uint32_t) * (size_t)n * 2);
     uint32_t* vals = keys + n;
-    if (!prep_explicit(ctx, hd, sd, n, xf->B, keys, vals, sc.st))
+    if (mem == CGX_MEM_HOST) {
+        // validate and pack on the host: 8 B/row cross the bus instead of 16, no device sync
+        std::vector<uint32_t> hk((size_t)(2 * n));
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t h = hash[i];
+            const double s = sign[i];
+            if (h < 0 || h >= xf->B || !(s == 1.0 || s == -1.0))
+                fail(CGX_EINVAL, "countsketch map: hash must lie in [0, buckets) and sign in {-1, +1}");
+            hk[(size_t)i] = (uint32_t)h;
+            hk[(size_t)(n + i)] = (uint32_t)i | (s < 0 ? kNegBit : 0u);
+        }
+        CGX_CUDA(cudaMemcpyAsync(keys, hk.data(), sizeof(uint32_t) * (size_t)(2 * n), cudaMemcpyHostToDevice, sc.st));
+    } else if (!prep_explicit(ctx, hash, sign, n, xf->B, keys, vals, sc.st)) {
         fail(CGX_EINVAL, "countsketch map: hash must lie in [0, buckets) and sign in {-1, +1}");
+    }
     xf->seeded_map = false;
     build_perm_explicit(ctx, xf, keys, vals, sc.st);
-    sc.sync();
 }
 
 } // namespace
@@ -335,6 +373,7 @@ int cgx_free(cgx_ctx* ctx) {
                           &ctx->sort_v[0], &ctx->sort_v[1], &ctx->sort_hist, &ctx->counts, &ctx->hstage_dev,
                           &ctx->sched})
             b->release();
+        for (auto& kv : ctx->pool_class) cudaFree(kv.first);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         for (int s = 0; s < 2; ++s)
             for (auto& e : ctx->prof.ev[s]) {
@@ -404,8 +443,7 @@ int cgx_countsketch_new(cgx_ctx* ctx, uint64_t map_seed, int64_t buckets, int64_
         try {
             xf->map_seed = map_seed;
             xf->seeded_map = true;
-            build_perm_seeded(ctx, xf, sc.st);
-            sc.sync();
+            build_perm_seeded(ctx, xf, sc.st);  // stream-ordered: no host wait
         } catch (...) {
             free_xform(xf);
             throw;
@@ -484,8 +522,7 @@ int cgx_countgauss_new_shard(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t b
             xf->g_seed = mix64(t_seed, 2);                 // g_rng = SeededRng(mix64(t.seed, 2))
             xf->m = m;
             xf->has_g = true;
-            build_perm_seeded(ctx, xf, sc.st);
-            sc.sync();
+            build_perm_seeded(ctx, xf, sc.st);  // stream-ordered: no host wait
         } catch (...) {
             free_xform(xf);
             throw;
@@ -549,9 +586,6 @@ int cgx_xform_free(cgx_xform* xf) {
     return guard([&] {
         if (!xf) return;
         std::lock_guard<std::recursive_mutex> lk(xf->ctx->mu);
-        cudaSetDevice(xf->ctx->device);
-        cudaStreamSynchronize(xf->ctx->stream);
-        cudaEventSynchronize(xf->ctx->done);
         free_xform(xf);
     });
 }

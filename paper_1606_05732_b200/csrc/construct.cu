@@ -237,15 +237,13 @@ void build_perm_explicit(cgx_ctx* ctx, cgx_xform* xf, const uint32_t* keys_dev, 
 // entry is out of range.
 bool prep_explicit(cgx_ctx* ctx, const int64_t* hash, const double* sign, int64_t n, int64_t B, uint32_t* keys,
                    uint32_t* vals, cudaStream_t s) {
-    int* bad = nullptr;
-    CGX_CUDA(cudaMallocAsync((void**)&bad, sizeof(int), s));
+    int* bad = (int*)ctx->sched.get(sizeof(int));
     CGX_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
     explicit_prep<<<ctx->num_sms * 4, 256, 0, s>>>(hash, sign, n, B, keys, vals, bad);
     count_launch(ctx);
     check_launch("explicit_prep");
     int hbad = 0;
     CGX_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CGX_CUDA(cudaFreeAsync(bad, s));
     CGX_CUDA(cudaStreamSynchronize(s));
     return hbad == 0;
 }

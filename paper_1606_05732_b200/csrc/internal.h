@@ -3,8 +3,10 @@
 
 #include <cstdint>
 #include <cstddef>
+#include <map>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -55,7 +57,12 @@ struct cgx_ctx {
     void* pinned = nullptr;                 // pinned staging for pageable host inputs
     size_t pinned_bytes = 0;
     cgx::Profile prof;
-    bool no_fuse = false;                   // option "fuse"=0: always run the two stages
+    // Caching pool for per-transform device arrays: transforms are built and dropped at
+    // high rates by Monte-Carlo callers (distcheck), and cudaMalloc/cudaFree cost more
+    // than a small sketch.  Blocks are size-classed (powers of two) and reused.
+    std::map<size_t, std::vector<void*>> pool_free;
+    std::unordered_map<void*, size_t> pool_class;
+    bool no_fuse = false;                  // option "fuse"=0: always run the two stages
     int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps fused, 2 warp-specialized
 };
 
@@ -127,6 +134,8 @@ void exclusive_scan_u32(cgx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t
 void exclusive_scan_i64(cgx_ctx* ctx, const int64_t* in, int64_t* out, int64_t count, cudaStream_t s);
 
 inline void count_launch(cgx_ctx* ctx, int k = 1) { ctx->launches += (uint64_t)k; }
+void* pool_alloc(cgx_ctx* ctx, size_t bytes);
+void pool_free(cgx_ctx* ctx, void* p);
 void check_launch(const char* what);
 
 } // namespace cgx
