@@ -42,6 +42,7 @@ CONFIGS = {
     "c2": dict(kind="dense", n=1 << 24, d=32, B=65536, m=64, dtype="f32"),
     "c3": dict(kind="csr", n=1 << 26, d=256, B=262144, m=128, density=0.01),
     "c4": dict(kind="dense", n=1 << 25, d=128, B=131072, m=32, dtype="f32"),
+    "c5": dict(kind="csr", n=1 << 27, d=512, B=1 << 20, m=256, zipf=(1.5, 512, 1.1)),
 }
 
 
@@ -57,6 +58,10 @@ def workload_name(cfg_name, c):
     if c["kind"] == "dense":
         return (f"{cfg_name}: dense X {c['n']}x{c['d']} {c['dtype']} row-major, CountGauss B={c['B']}, "
                 f"m={c['m']}")
+    if "zipf" in c:
+        s_len, cap, s_col = c["zipf"]
+        return (f"{cfg_name}: CSR X {c['n']}x{c['d']} row lengths Zipf({s_len}) cap {cap}, columns Zipf({s_col}), "
+                f"fp32/int32, B={c['B']}, m={c['m']}")
     return f"{cfg_name}: CSR X {c['n']}x{c['d']} Bernoulli({c['density']}) fp32/int32, B={c['B']}, m={c['m']}"
 
 
@@ -212,7 +217,12 @@ def run_ours(args):
         nnz_local = rows * d
         x_bytes = rows * d * x.element_size()
     else:
-        x = bench_data.csr_bernoulli(rows, d, c["density"], seed=mix64(SEED, 3) + r0, device=local)
+        if "zipf" in c:
+            s_len, cap, s_col = c["zipf"]
+            x = bench_data.csr_zipf(rows, d, seed=mix64(SEED, 5) + r0, s_len=s_len, cap=cap, s_col=s_col,
+                                    device=local)
+        else:
+            x = bench_data.csr_bernoulli(rows, d, c["density"], seed=mix64(SEED, 3) + r0, device=local)
         nnz_local = x.nnz()
         x_bytes = nnz_local * 8 + (rows + 1) * 8
     torch.cuda.synchronize()
@@ -225,13 +235,14 @@ def run_ours(args):
     construct_ms = (time.perf_counter() - t0) * 1e3
 
     stream = torch.cuda.current_stream(dev)
-    z = torch.empty((d, m), dtype=torch.float64, device=dev).t()
+    zbuf = torch.empty((d, m), dtype=torch.float64, device=dev)  # contiguous storage of Z^T
+    z = zbuf.t()  # column-major m x d view (the reference layout)
 
     def step():
-        zz = cg.api.countgauss_apply_into(t, x, z)
+        cg.api.countgauss_apply_into(t, x, z)
         if world > 1:
-            dist.all_reduce(zz)
-        return zz
+            dist.all_reduce(zbuf)  # partial Z of every row shard -> full Z on every rank
+        return z
 
     for _ in range(args.warmup):
         step()
@@ -328,7 +339,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": workload_name(args.config, c), "n": n, "d": d, "B": B, "m": m,
-                "rows_per_rank": rows, "parallelism": f"rows sharded x{world}" + (", NCCL all-reduce of Z" if world > 1 else ""),
+                "rows_per_rank": rows, "nnz_per_rank": int(nnz_local), "mean_row_nnz": nnz_local / rows, "parallelism": f"rows sharded x{world}" + (", NCCL all-reduce of Z" if world > 1 else ""),
                 "input_dtype": c.get("dtype", "f32"), "accumulate": "f64 (S.X and G.(S.X))",
                 "l2": f"inputs larger than L2 ({x_bytes / 1e9:.2f} GB X per rank), no flush",
                 "construct_ms": construct_ms,

@@ -158,6 +158,12 @@ int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, dou
                           int64_t* rowptr_dev, int32_t* cols_dev, float* vals_dev, int64_t* nnz_out,
                           void* stream);
 
+/* Config-5 style heavy-tailed CSR: row i draws a target length L from Zipf(s_len) on
+ * [1, cap]; column j is kept with probability min(1, L * w_j), w_j ~ (j+1)^-s_col
+ * normalized (Zipf-skewed columns, sorted and distinct).  Same two-phase protocol. */
+int cgx_gen_csr_zipf(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double s_len, int64_t cap, double s_col,
+                     int64_t* rowptr_dev, int32_t* cols_dev, float* vals_dev, int64_t* nnz_out, void* stream);
+
 /* ---- instrumentation ---------------------------------------------------------------- */
 /* Context options.  "fuse" (default 1): countgauss_apply on dense wide-row X runs the
  * one-pass sketch+G+contraction kernel; 0 forces the two-stage path (S.X to HBM, then

@@ -34,6 +34,27 @@ def dense_normal(n: int, d: int, seed: int, dtype=None, layout: str = "row", dev
     return x
 
 
+def csr_zipf(n: int, d: int, seed: int, s_len: float = 1.5, cap: int = 512, s_col: float = 1.1, device=None):
+    """Config-5 style heavy-tailed CSR (see cgx_gen_csr_zipf): Zipf(s_len) target row
+    lengths capped at `cap`, Zipf(s_col)-skewed columns, fp32 N(0,1) values."""
+    import torch
+
+    from .api import SparseMatrix
+
+    ctx = context(device)
+    dev = torch.device("cuda", ctx.device)
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream or 1)  # 1 = cudaStreamLegacy
+    rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    nnz = C.c_int64()
+    check(lib.cgx_gen_csr_zipf(ctx.h, seed, n, d, s_len, cap, s_col, rp.data_ptr(), None, None, C.byref(nnz),
+                               stream))
+    cols = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)[: nnz.value]
+    vals = torch.empty(max(nnz.value, 1), dtype=torch.float32, device=dev)[: nnz.value]
+    check(lib.cgx_gen_csr_zipf(ctx.h, seed, n, d, s_len, cap, s_col, rp.data_ptr(), cols.data_ptr(),
+                               vals.data_ptr(), None, stream))
+    return SparseMatrix(n, d, rp, cols, vals)
+
+
 def csr_bernoulli(n: int, d: int, density: float, seed: int, device=None):
     """CSR n x d, each entry present with probability `density` (sorted distinct columns,
     int32 columns, fp32 N(0,1) values, int64 row offsets).  Returns a SparseMatrix of

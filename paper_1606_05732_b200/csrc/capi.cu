@@ -337,6 +337,21 @@ void build_explicit(cgx_ctx* ctx, cgx_xform* xf, const int64_t* hash, const doub
     build_perm_explicit(ctx, xf, keys, vals, sc.st);
 }
 
+// Two-phase CSR generation: without cols/vals, row offsets + nnz; with them, the fill.
+void gen_csr(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, const CsrGenSpec& spec, int64_t* rowptr_dev,
+             int32_t* cols_dev, float* vals_dev, int64_t* nnz_out, void* stream) {
+    CallScope sc(ctx, stream);
+    if (!cols_dev || !vals_dev) {
+        launch_gen_csr_counts(ctx, seed, n, d, spec, rowptr_dev, sc.st);
+        int64_t nnz = 0;
+        CGX_CUDA(cudaMemcpyAsync(&nnz, rowptr_dev + n, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.st));
+        sc.sync();
+        if (nnz_out) *nnz_out = nnz;
+        return;
+    }
+    launch_gen_csr_fill(ctx, seed, n, d, spec, rowptr_dev, cols_dev, vals_dev, sc.st);
+}
+
 } // namespace
 } // namespace cgx
 
@@ -371,7 +386,7 @@ int cgx_free(cgx_ctx* ctx) {
         cudaDeviceSynchronize();
         for (DevBuf* b : {&ctx->sx, &ctx->zpart, &ctx->xstage, &ctx->tmp, &ctx->sort_k[0], &ctx->sort_k[1],
                           &ctx->sort_v[0], &ctx->sort_v[1], &ctx->sort_hist, &ctx->counts, &ctx->hstage_dev,
-                          &ctx->sched})
+                          &ctx->sched, &ctx->gen_tables})
             b->release();
         for (auto& kv : ctx->pool_class) cudaFree(kv.first);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -820,16 +835,24 @@ int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, dou
         need_ctx(ctx);
         if (n < 1 || d < 1) fail(CGX_EINVAL, "cgx_gen_csr_bernoulli: n and d must be >= 1");
         if (!(density >= 0.0 && density <= 1.0)) fail(CGX_EINVAL, "cgx_gen_csr_bernoulli: density must lie in [0,1]");
-        CallScope sc(ctx, stream);
-        if (!cols_dev || !vals_dev) {
-            launch_gen_csr_counts(ctx, seed, n, d, density, rowptr_dev, sc.st);
-            int64_t nnz = 0;
-            CGX_CUDA(cudaMemcpyAsync(&nnz, rowptr_dev + n, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.st));
-            sc.sync();
-            if (nnz_out) *nnz_out = nnz;
-            return;
-        }
-        launch_gen_csr_fill(ctx, seed, n, d, density, rowptr_dev, cols_dev, vals_dev, sc.st);
+        CsrGenSpec spec;
+        spec.density = density;
+        gen_csr(ctx, seed, n, d, spec, rowptr_dev, cols_dev, vals_dev, nnz_out, stream);
+    });
+}
+
+int cgx_gen_csr_zipf(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double s_len, int64_t cap, double s_col,
+                     int64_t* rowptr_dev, int32_t* cols_dev, float* vals_dev, int64_t* nnz_out, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (n < 1 || d < 1 || cap < 1 || cap > d) fail(CGX_EINVAL, "cgx_gen_csr_zipf: need n, d >= 1 and 1 <= cap <= d");
+        if (!(s_len > 0.0) || !(s_col >= 0.0)) fail(CGX_EINVAL, "cgx_gen_csr_zipf: bad exponents");
+        CsrGenSpec spec;
+        spec.zipf = true;
+        spec.s_len = s_len;
+        spec.s_col = s_col;
+        spec.cap = (int)cap;
+        gen_csr(ctx, seed, n, d, spec, rowptr_dev, cols_dev, vals_dev, nnz_out, stream);
     });
 }
 

@@ -54,6 +54,7 @@ struct cgx_ctx {
     cgx::DevBuf sort_k[2], sort_v[2], sort_hist, counts;  // transform construction
     cgx::DevBuf hstage_dev;                 // device landing zone for host inputs
     cgx::DevBuf sched;                      // work-queue counters of persistent kernels
+    cgx::DevBuf gen_tables;                 // synthetic-input generator tables
     void* pinned = nullptr;                 // pinned staging for pageable host inputs
     size_t pinned_bytes = 0;
     cgx::Profile prof;
@@ -124,10 +125,16 @@ void launch_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d,
 // datagen.cu
 void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype, int layout, void* x,
                       cudaStream_t s);
-void launch_gen_csr_counts(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double density, int64_t* rowptr,
-                           cudaStream_t s);
-void launch_gen_csr_fill(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double density, const int64_t* rowptr,
-                         int32_t* cols, float* vals, cudaStream_t s);
+struct CsrGenSpec {
+    bool zipf = false;
+    double density = 0.0;                      // Bernoulli
+    double s_len = 1.5, s_col = 1.1;           // Zipf exponents (row length, column popularity)
+    int cap = 512;                             // row-length cap
+};
+void launch_gen_csr_counts(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, const CsrGenSpec& spec,
+                           int64_t* rowptr, cudaStream_t s);
+void launch_gen_csr_fill(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, const CsrGenSpec& spec,
+                         const int64_t* rowptr, int32_t* cols, float* vals, cudaStream_t s);
 
 // scan.cu: exclusive scans (in place allowed), total written to out[count] when requested
 void exclusive_scan_u32(cgx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t count, cudaStream_t s);

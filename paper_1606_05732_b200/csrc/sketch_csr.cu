@@ -26,6 +26,25 @@ namespace {
 
 constexpr int kWaves = 4;  // item waves loaded before they are applied
 
+// Random short reads: a plain global load that does not allocate in L1 (the gathered
+// rows are never re-read by this SM), so only the touched 32 B sectors move.
+template <typename T>
+__device__ __forceinline__ T ld_na(const T* p) {
+    if constexpr (sizeof(T) == 8) {
+        unsigned long long v;
+        asm volatile("ld.global.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+        T out;
+        memcpy(&out, &v, 8);
+        return out;
+    } else {
+        unsigned v;
+        asm volatile("ld.global.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+        T out;
+        memcpy(&out, &v, 4);
+        return out;
+    }
+}
+
 template <typename TV, typename TI, bool CHUNKED>
 __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restrict__ rowptr,
                                                          const TI* __restrict__ cols, const TV* __restrict__ vals,
@@ -60,8 +79,8 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
             if ((int)lane < cnt) {
                 pe = __ldg(perm + base + lane);
                 const int64_t row = pe & kRowMask;
-                rb = __ldg(rowptr + row);
-                re = __ldg(rowptr + row + 1);
+                rb = ld_na(rowptr + row);
+                re = ld_na(rowptr + row + 1);
             }
             const int incl = warp_incl_scan((int)(re - rb), lane);
             const int total = __shfl_sync(0xffffffffu, incl, 31);
@@ -84,8 +103,8 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
                             if (s_incl[wid][lo + step - 1] <= q) lo += step;
                         const int start = lo ? s_incl[wid][lo - 1] : 0;
                         const int64_t pos = s_beg[wid][lo] + (q - start);
-                        c[w] = __ldcs(cols + pos);
-                        v[w] = __ldcs(vals + pos);
+                        c[w] = ld_na(cols + pos);
+                        v[w] = ld_na(vals + pos);
                         kk[w] = lo;
                     }
                 }

@@ -245,6 +245,29 @@ def test_csr_long_rows(cg, restatement):
     assert np.array_equal(cg.countsketch_apply(t, cg.SparseMatrix(n, d, rp, cols, vals)), sx_ref)
 
 
+def test_csr_zipf_config5_shape(cg, restatement):
+    """Config-5 generator (heavy-tailed rows, skewed columns) at reduced n, full d/cap:
+    CSR invariants, realized mean row length, S.X bit-exact, Z within tolerance."""
+    from paper_1606_05732_b200 import bench_data
+
+    n, d, B, m = 60000, 512, 4096, 32
+    x = bench_data.csr_zipf(n, d, seed=99)
+    rp = x.row_offsets.cpu().numpy()
+    c = x.col_indices.cpu().numpy()
+    v = x.values.cpu().numpy()
+    lens = np.diff(rp)
+    assert rp[0] == 0 and rp[-1] == len(c) and (lens >= 0).all() and lens.max() <= d
+    for i in range(0, n, 997):  # sorted distinct columns within each row
+        seg = c[rp[i]:rp[i + 1]]
+        assert (np.diff(seg) > 0).all() and (seg >= 0).all() and (seg < d).all()
+    assert 8 < lens.mean() < 40  # Zipf(1.5) capped at 512: target mean 17.4
+    assert np.bincount(c, minlength=d)[:8].sum() > np.bincount(c, minlength=d)[-8:].sum()  # skewed columns
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(5))
+    z_ref, sx_ref = restatement.countgauss(5, m, B, csr=(rp, c, v, d))
+    assert np.array_equal(cg.countsketch_apply(t, x).cpu().numpy(), sx_ref)
+    assert rel_fro(cg.countgauss_apply(t, x).cpu().numpy(), z_ref) <= Z_TOL
+
+
 # ------------------------------------------------------------------------- anchors
 def test_cg_nmf_golden(cg, golden):
     a = cg.cg_nmf(np.asfortranarray(golden["nmf_x"]), 12, 60, cg.SeededRng(7006))
