@@ -1,0 +1,197 @@
+// dgemm.cu -- stage 2 for large m x d: Z = G . (S.X) as G super-chunks + a pipelined
+// FP64 tensor-core GEMM.
+//
+// When Z is large (config 3: 128 x 256, config 5: 256 x 512) a CTA cannot hold a full
+// row of Z tiles, so generating G inside the GEMM would regenerate every G(r, c) once per
+// column tile.  Instead G is produced in super-chunks of S bucket-columns (m x S fp64,
+// sized to stay resident in L2, ~48 MB) by the high-occupancy generator (53 G normals/s
+// on B200), and each chunk is consumed right away by a cp.async-pipelined DMMA GEMM
+// (mma.sync.m8n8k4.f64 -- the only FP64 tensor-core path on sm_100a, 37.2 TFLOP/s
+// measured by tools/microbench/fp64_peak.cu).  G never exists in full anywhere: at most
+// one chunk, in L2.
+//
+// GEMM: CTA tile BM x BN, BK = 16, 3-stage cp.async pipeline; 8 warps, 32 x 32 warp tiles
+// (4 x 4 m8n8 fragments, 32 fp64 accumulators per thread).  Split-K across CTAs; each CTA
+// accumulates its partial tile across super-chunks (kernel launches are stream-ordered,
+// so the read-modify-write is race-free and the order is fixed) and reduce_splits sums
+// the partials in split order: Z is deterministic.
+#include "common.cuh"
+#include "internal.h"
+
+namespace cgx {
+namespace {
+
+constexpr int BK = 16, STAGES = 3;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+    const unsigned dst = smem_addr(smem);
+    const int sz = pred ? 8 : 0;  // src-size 0 zero-fills
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(pred ? gmem : nullptr), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// C[split] (+)= A . Bm over k in [split*kps, min(K, (split+1)*kps)).
+// A: m x K column-major (element (r,k) at k*m + r); Bm: K x d row-major; C: col-major d x m.
+template <int WGM, int WGN>  // warp grid (WGM x WGN = 8); CTA tile = 32*WGM x 32*WGN
+__global__ void __launch_bounds__(256, 2) gemm_dmma(const double* __restrict__ A, int64_t m,
+                                                    const double* __restrict__ Bm, int64_t d, int64_t K,
+                                                    int64_t kps, double* __restrict__ C, int accumulate) {
+    constexpr int BM = 32 * WGM, BN = 32 * WGN;
+    constexpr int LDA = BM + 4, LDB = BN + 4;  // padding: 2-wavefront fragment loads
+    extern __shared__ double dsm[];
+    double* As = dsm;                          // [STAGES][BK][LDA]
+    double* Bs = dsm + STAGES * BK * LDA;      // [STAGES][BK][LDB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp % WGM, wn = warp / WGM;
+    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+    const int64_t split = blockIdx.z;
+    const int64_t kb = split * kps, ke = min(K, kb + kps);
+    const int ntiles = (int)((ke - kb + BK - 1) / BK);
+
+    auto load_tile = [&](int stage, int t) {
+        const int64_t k0 = kb + (int64_t)t * BK;
+        double* as = As + stage * BK * LDA;
+        double* bs = Bs + stage * BK * LDB;
+        for (int e = tid; e < BK * BM; e += 256) {
+            const int kk = e / BM, r = e - kk * BM;
+            const int64_t gk = k0 + kk, gr = m0 + r;
+            const bool ok = gk < ke && gr < m;
+            cp_async8(as + kk * LDA + r, A + gk * m + gr, ok);
+        }
+        for (int e = tid; e < BK * BN; e += 256) {
+            const int kk = e / BN, c = e - kk * BN;
+            const int64_t gk = k0 + kk, gc = n0 + c;
+            const bool ok = gk < ke && gc < d;
+            cp_async8(bs + kk * LDB + c, Bm + gk * d + gc, ok);
+        }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ntiles) load_tile(s, s);
+        cp_commit();
+    }
+    for (int t = 0; t < ntiles; ++t) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        const int stage = t % STAGES;
+        const double* as = As + stage * BK * LDA + wm * 32 + (lane >> 2);
+        const double* bs = Bs + stage * BK * LDB + wn * 32 + (lane >> 2);
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = as[(k4 + (lane & 3)) * LDA + i * 8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = bs[(k4 + (lane & 3)) * LDB + j * 8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+        const int nt = t + STAGES - 1;
+        if (nt < ntiles) load_tile(nt % STAGES, nt);
+        cp_commit();
+    }
+    cp_wait<0>();
+    double* cp = C + split * m * d;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t r = m0 + wm * 32 + i * 8 + (lane >> 2);
+                const int64_t c = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + h;
+                if (r < m && c < d) {
+                    double* p = cp + c * m + r;
+                    *p = accumulate ? *p + acc[i][j][h] : acc[i][j][h];
+                }
+            }
+}
+
+// G columns [c0, c0 + cols) -> out (m x cols, column-major).
+__global__ void gen_gauss_cols(uint64_t g_seed, int64_t m, int64_t c0, int64_t cols, double* __restrict__ out) {
+    const int64_t total = m * cols;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / m, r = e - c * m;
+        out[e] = gauss_entry(g_seed, (uint64_t)m, (uint64_t)r, (uint64_t)(c0 + c));
+    }
+}
+
+template <int WGM, int WGN>
+void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d, double* z,
+                cudaStream_t s) {
+    constexpr int BM = 32 * WGM, BN = 32 * WGN;
+    const int64_t m = xf->m, K = b1 - b0;
+    // super-chunk of S bucket-columns: m x S fp64 <= 48 MB (L2-resident), multiple of BK
+    int64_t S = (48ll << 20) / (8 * m);
+    S = S < BK ? BK : S / BK * BK;
+    if (S > K) S = (K + BK - 1) / BK * BK;
+    const int64_t tm = (m + BM - 1) / BM, tn = (d + BN - 1) / BN;
+    int64_t splits = (2 * (int64_t)ctx->num_sms + tm * tn - 1) / (tm * tn);
+    const int64_t max_splits = (S + 4 * BK - 1) / (4 * BK);  // >= 4 K-tiles per split per chunk
+    splits = splits < 1 ? 1 : (splits > max_splits ? max_splits : splits);
+    const int64_t kps = ((S + splits - 1) / splits + BK - 1) / BK * BK;
+    splits = (S + kps - 1) / kps;
+    double* gbuf = (double*)ctx->xstage.get(sizeof(double) * (size_t)(m * S));
+    double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
+    auto kern = gemm_dmma<WGM, WGN>;
+    const size_t smem = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
+    CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bool first = true;
+    for (int64_t c0 = 0; c0 < K; c0 += S) {
+        const int64_t cols = K - c0 < S ? K - c0 : S;
+        const double* Ach;
+        if (xf->g_explicit) {
+            Ach = xf->g_dev + (b0 + c0) * m;  // explicit G is already m x B column-major
+        } else {
+            int64_t blocks = (m * cols + 255) / 256;
+            if (blocks > ctx->num_sms * 32) blocks = ctx->num_sms * 32;
+            gen_gauss_cols<<<(unsigned)blocks, 256, 0, s>>>(xf->g_seed, m, b0 + c0, cols, gbuf);
+            count_launch(ctx);
+            check_launch("gen_gauss_cols");
+            Ach = gbuf;
+        }
+        const int64_t sp = (cols + kps - 1) / kps;  // splits that have work in this chunk
+        kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), 256, smem, s>>>(Ach, m, sx + c0 * d, d, cols, kps,
+                                                                                zpart, first ? 0 : 1);
+        count_launch(ctx);
+        check_launch("gemm_dmma");
+        if (first && sp < splits)  // splits without work in the first chunk start at zero
+            CGX_CUDA(cudaMemsetAsync(zpart + sp * m * d, 0, sizeof(double) * (size_t)((splits - sp) * m * d), s));
+        first = false;
+    }
+    launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
+}
+
+} // namespace
+
+bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
+                               int64_t d, double* z, cudaStream_t s) {
+    const int64_t m = xf->m;
+    if (m * d <= 64 * 128) return false;  // small Z: the wide in-kernel-generation GEMM is better
+    if (m >= 2 * d)
+        run_chunks<4, 2>(ctx, xf, sx, b0, b1, d, z, s);  // 128 x 64 tiles
+    else
+        run_chunks<2, 4>(ctx, xf, sx, b0, b1, d, z, s);  // 64 x 128 tiles
+    return true;
+}
+
+} // namespace cgx

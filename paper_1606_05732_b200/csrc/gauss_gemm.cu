@@ -220,11 +220,13 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
         CGX_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)(m * d), s));
         return;
     }
+    if (launch_gauss_gemm_chunked(ctx, xf, sx, b0, b1, d, z, s)) return;  // large Z (dgemm.cu)
     if (d <= 1024) {
         // wide tile: WM rows x all columns, WM * dp <= 8192 (<= 16 fragments per warp)
         const int64_t dp = (d + 7) & ~int64_t(7);
         const int WM = dp <= 128 ? 64 : dp <= 256 ? 32 : dp <= 512 ? 16 : 8;
-        const int KW = dp <= 512 ? 32 : 16;
+        // K-chunk sized so the S.X slab stays <= ~34 KB: two CTAs per SM fit in smem
+        const int KW = dp <= 128 ? 32 : dp <= 256 ? 16 : 8;
         const int64_t tm = (m + WM - 1) / WM;
         const int64_t kchunks = (B + KW - 1) / KW;
         int64_t want = (2 * (int64_t)ctx->num_sms + tm - 1) / tm;
@@ -242,9 +244,9 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
         kern<<<grid, 256, smem, s>>>(sx, B, d, m, xf->g_seed, gex, b0, k_per_split, zpart);                     \
     } while (0)
         if (WM == 64) CGX_WIDE(64, 32);
-        else if (WM == 32) CGX_WIDE(32, 32);
-        else if (WM == 16) CGX_WIDE(16, 32);
-        else CGX_WIDE(8, 16);
+        else if (WM == 32) CGX_WIDE(32, 16);
+        else if (WM == 16) CGX_WIDE(16, 8);
+        else CGX_WIDE(8, 8);
 #undef CGX_WIDE
         count_launch(ctx);
         check_launch("gauss_gemm_wide");

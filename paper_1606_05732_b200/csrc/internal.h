@@ -115,6 +115,9 @@ void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr,
 void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d,
                        double* z, cudaStream_t s);
 void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStream_t s);
+// dgemm.cu: G super-chunks + pipelined DMMA GEMM; false when Z is small (not used)
+bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
+                               int64_t d, double* z, cudaStream_t s);
 void launch_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int* bad,
                                cudaStream_t s);
 

@@ -268,6 +268,33 @@ def test_csr_zipf_config5_shape(cg, restatement):
     assert rel_fro(cg.countgauss_apply(t, x).cpu().numpy(), z_ref) <= Z_TOL
 
 
+@pytest.mark.parametrize("m,d,B", [(96, 300, 20011), (256, 512, 40000), (130, 70, 9000), (64, 129, 33333)])
+def test_stage2_large_z(cg, restatement, m, d, B):
+    """Stage 2 on its own (gemm(t.g, SX), matrix.cpp:111-129) for Z shapes that take the
+    G-super-chunk + pipelined DMMA path, with G seeded (generated) and explicit."""
+    import ctypes as C
+
+    from paper_1606_05732_b200._lib import CGX_COL_MAJOR, CGX_MEM_HOST, check, lib
+
+    rng = np.random.default_rng(m + d)
+    sx = np.asfortranarray(rng.standard_normal((B, d)))
+    t = cg.countgauss_new(m, B, 10, cg.SeededRng(m * d))
+    _, _, gs = restatement.countgauss_seeds(m * d)
+    G = restatement.gaussian(gs, m, B)
+    ref = restatement.gemm(G, sx)
+    ctx = cg.context()
+    z = np.empty((m, d), np.float64, order="F")
+    check(lib.cgx_gauss_gemm(ctx.h, t._xf.h, sx.ctypes.data, CGX_COL_MAJOR, d, CGX_MEM_HOST, z.ctypes.data,
+                             CGX_MEM_HOST, None))
+    assert rel_fro(z, ref) <= Z_TOL
+    Gf = np.asfortranarray(G)
+    check(lib.cgx_xform_set_gaussian_explicit(ctx.h, t._xf.h, m, Gf.ctypes.data, CGX_MEM_HOST))
+    z2 = np.empty((m, d), np.float64, order="F")
+    check(lib.cgx_gauss_gemm(ctx.h, t._xf.h, sx.ctypes.data, CGX_COL_MAJOR, d, CGX_MEM_HOST, z2.ctypes.data,
+                             CGX_MEM_HOST, None))
+    assert rel_fro(z2, ref) <= 1e-14
+
+
 # ------------------------------------------------------------------------- anchors
 def test_cg_nmf_golden(cg, golden):
     a = cg.cg_nmf(np.asfortranarray(golden["nmf_x"]), 12, 60, cg.SeededRng(7006))
