@@ -322,6 +322,25 @@ def run_ours(args):
                "how": "cgx_countgauss_apply_dense with x_mem=HOST (pinned), wall clock, median"}
         del xh
 
+    # Ablation (the reference's bench reports it too, countgauss_main.cpp:535-547): the
+    # dense-Gaussian projection G~.X (m x n Gaussian, generated on the GPU in L2-sized
+    # chunks) on the same X, untimed by the main metric.
+    ablation = None
+    if c["kind"] == "dense" and world == 1 and not args.no_ablation:
+        rng = cg.SeededRng(SEED)
+        cg.gaussian_project(x, m, rng)  # warm-up
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        e0.record(stream)
+        for _ in range(reps):
+            cg.gaussian_project(x, m, rng)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dense_ms = e0.elapsed_time(e1) / reps
+        ablation = {"dense_gaussian_ms": dense_ms, "countgauss_ms": ms_per_step,
+                    "speedup_vs_dense": dense_ms / ms_per_step,
+                    "what": f"G~.X with G~ = gaussian_matrix({m}, {n}, rng) generated in-GPU (gp_nmf, nmf.cpp:155-159)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and c["kind"] == "dense":
         try:
@@ -351,6 +370,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
+            "ablation": ablation,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -368,6 +388,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the dense-Gaussian G~.X ablation")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3", file=sys.stderr)

@@ -141,6 +141,14 @@ int cgx_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int sx_l
 int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_rows, int64_t b0, int64_t b1,
                          int64_t d, int sx_mem, double* z, int z_mem, void* stream);
 
+/* Dense-Gaussian baseline (SURVEY 8f, config-5 ablation): z = G~ . X with G~ the m x n
+ * i.i.d. N(0,1) matrix gaussian_matrix(m, n, rng) would draw (matrix.cpp:199-207) from a
+ * SeededRng whose current state is `rng_state` -- the product gp_nmf computes
+ * (nmf.cpp:155-159).  G~ is generated in L2-resident chunks, never stored whole.  The
+ * caller advances its rng by m*n draws. */
+int cgx_gaussian_project_dense(cgx_ctx* ctx, uint64_t rng_state, int64_t m, const void* x, int dtype, int layout,
+                               int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem, void* stream);
+
 /* select_extremes(Z)  -- nmf.cpp:99-118: per row argmax/argmin of an m x d column-major
  * Z, strict compares (ties to the lowest column), tie_rows = rows whose max or min is
  * attained more than once.  amax/amin: m entries each (unsorted, per row). */

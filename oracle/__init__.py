@@ -211,6 +211,7 @@ class Reference:
         L.cgref_materialized_sketch.argtypes = [_P, _P, _I64, _I64, _P]
         L.cgref_cg_nmf.argtypes = [_P, C.c_int, _I64, _I64, _U64] + [_P] * 7
         L.cgref_random_sparse.argtypes = [_I64, _I64, _I64, _U64, _P, _P, _P]
+        L.cgref_gp_nmf.argtypes = [_P, _I64, _U64] + [_P] * 7
         L.cgref_generate_separable.argtypes = [_I64, _I64, _I64, _U64, _P]
 
     def _check(self, rc):
@@ -308,6 +309,15 @@ class Reference:
                                           _ptr(bufs[0]), C.byref(cnt[0]), _ptr(bufs[1]),
                                           C.byref(cnt[1]), _ptr(bufs[2]), C.byref(cnt[2]),
                                           C.byref(cnt[3])))
+        return dict(i_max=bufs[0][:cnt[0].value].copy(), i_min=bufs[1][:cnt[1].value].copy(),
+                    unioned=bufs[2][:cnt[2].value].copy(), tie_rows=cnt[3].value)
+
+    def gp_nmf(self, xm, m, caller_seed):
+        cap = max(2 * m, 1)
+        bufs = [np.empty(cap, np.int64) for _ in range(3)]
+        cnt = [_I64() for _ in range(4)]
+        self._check(self.lib.cgref_gp_nmf(xm.h, m, caller_seed, _ptr(bufs[0]), C.byref(cnt[0]), _ptr(bufs[1]),
+                                          C.byref(cnt[1]), _ptr(bufs[2]), C.byref(cnt[2]), C.byref(cnt[3])))
         return dict(i_max=bufs[0][:cnt[0].value].copy(), i_min=bufs[1][:cnt[1].value].copy(),
                     unioned=bufs[2][:cnt[2].value].copy(), tie_rows=cnt[3].value)
 

@@ -296,6 +296,23 @@ int cgref_cg_nmf(void* xh, int sparse, int64_t m, int64_t B, uint64_t caller_see
     });
 }
 
+// gp_nmf(X, m, SeededRng(caller_seed))  (nmf.cpp:155-159), dense X only; same outputs as
+// cgref_cg_nmf.
+int cgref_gp_nmf(void* xh, int64_t m, uint64_t caller_seed, int64_t* i_max, int64_t* n_max, int64_t* i_min,
+                 int64_t* n_min, int64_t* unioned, int64_t* n_union, int64_t* tie_rows) {
+    return guard([&] {
+        SeededRng rng(caller_seed);
+        AnchorSet a = gp_nmf(*static_cast<DenseMatrix*>(xh), m, rng);
+        std::copy(a.i_max.begin(), a.i_max.end(), i_max);
+        std::copy(a.i_min.begin(), a.i_min.end(), i_min);
+        std::copy(a.unioned.begin(), a.unioned.end(), unioned);
+        *n_max = static_cast<int64_t>(a.i_max.size());
+        *n_min = static_cast<int64_t>(a.i_min.size());
+        *n_union = static_cast<int64_t>(a.unioned.size());
+        *tie_rows = a.tie_rows;
+    });
+}
+
 // random_sparse(rows, cols, per_row, SeededRng(seed))  (matrix.cpp:209-233): the reference's own
 // bench input generator; output sized rows*per_row.
 int cgref_random_sparse(int64_t rows, int64_t cols, int64_t per_row, uint64_t seed, int64_t* rowptr,

@@ -7,10 +7,12 @@ host-side mirror of the reference library's API (see :mod:`.api`).
 """
 from .api import (AnchorSet, Context, CountGaussTransform, CountSketchMap, SeededRng, SparseMatrix, cg_nmf,
                   context, countgauss_apply, countgauss_new, countsketch_apply, countsketch_injective,
-                  countsketch_new, inverse_normal_cdf, inverse_normal_cdf_array, mix64, select_extremes)
+                  countsketch_new, gaussian_project, gp_nmf, inverse_normal_cdf, inverse_normal_cdf_array, mix64,
+                  select_extremes)
 
 __all__ = [
     "AnchorSet", "Context", "CountGaussTransform", "CountSketchMap", "SeededRng", "SparseMatrix", "cg_nmf",
     "context", "countgauss_apply", "countgauss_new", "countsketch_apply", "countsketch_injective",
-    "countsketch_new", "inverse_normal_cdf", "inverse_normal_cdf_array", "mix64", "select_extremes",
+    "countsketch_new", "gaussian_project", "gp_nmf", "inverse_normal_cdf", "inverse_normal_cdf_array", "mix64",
+    "select_extremes",
 ]

@@ -529,6 +529,34 @@ def select_extremes(z, ctx: Optional[Context] = None) -> AnchorSet:
     return AnchorSet(i_max, i_min, sorted(set(i_max) | set(i_min)), int(ties.value))
 
 
+def gaussian_project(x, m: int, rng: SeededRng, ctx: Optional[Context] = None):
+    """Dense-Gaussian baseline Z = G~.X with G~ = gaussian_matrix(m, n, rng) (matrix.cpp:199-207,
+    the product gp_nmf forms, nmf.cpp:155-159).  G~ is generated on the GPU in L2-sized
+    chunks (never stored whole); rng advances by m*n draws exactly as in the reference."""
+    if m < 1:
+        raise ValueError("anchor extraction: m must be >= 1")
+    ctx = ctx or context()
+    ptr, dt, layout, ld, n, d, mem, keep, dev = _dense_args(x)
+    if d < 1:
+        raise ValueError("anchor extraction: X must have at least one column")
+    out, optr = _out(m, d, dev, keep)
+    check(lib.cgx_gaussian_project_dense(ctx.h, rng._state, int(m), ptr, dt, layout, ld, n, d, mem, optr, mem,
+                                         _stream_of(keep) if dev else None))
+    rng._state = (rng._state + m * n * GAMMA) & _MASK
+    return out
+
+
+def gp_nmf(x, m: int, rng: SeededRng, ctx: Optional[Context] = None) -> AnchorSet:
+    """Gaussian-projection anchor extraction (nmf.cpp:155-159): extremes of G~.X."""
+    n, d = x.shape
+    if m < 1:
+        raise ValueError("anchor extraction: m must be >= 1")
+    if d < 1:
+        raise ValueError("anchor extraction: X must have at least one column")
+    ctx = ctx or context()
+    return select_extremes(gaussian_project(x, m, rng, ctx=ctx), ctx=ctx)
+
+
 def cg_nmf(x, m: int, buckets: int, rng: SeededRng, ctx: Optional[Context] = None) -> AnchorSet:
     """CountGauss anchor extraction (nmf.cpp:141-153): Z = G.(S.X) with a fresh transform
     from rng, then per-row extremes.  buckets < 1 selects 5m."""

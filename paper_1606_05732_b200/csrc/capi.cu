@@ -374,6 +374,9 @@ int cgx_init(int device, cgx_ctx** out) {
         CGX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
         CGX_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         CGX_CUDA(cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming));
+        CGX_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+        CGX_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CGX_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         CGX_CUDA(cudaEventRecord(ctx->done, ctx->stream));
         *out = ctx;
     });
@@ -396,6 +399,11 @@ int cgx_free(cgx_ctx* ctx) {
                 cudaEventDestroy(e.second);
             }
         cudaEventDestroy(ctx->done);
+        cudaEventDestroy(ctx->ev_fork);
+        cudaEventDestroy(ctx->ev_join);
+        cudaStreamDestroy(ctx->aux);
+        ctx->gfull.release();
+        ctx->gchunk.release();
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -709,6 +717,34 @@ int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x,
         int64_t rld = ld;
         const void* xd = dense_rowmajor(ctx, xf, x, dtype, layout, ld, n, d, x_mem, &rld, sc.st);
         if (d == 0) return;
+        // Overlapped stages: G (m x B, <= 64 MB, L2-resident) is generated on the side
+        // stream while the streaming sketch kernel reads X on the caller's stream -- the
+        // FP64-bound generator and the HBM-bound gather share the SMs -- then one small
+        // DMMA GEMM contracts the two.  The join is an event: no kernel waits on another.
+        const bool wide = d >= 17 && (dtype == CGX_F32 ? d % 4 == 0 || d <= 64 : d <= 64 || d % 2 == 0);
+        if (!ctx->no_fuse && ctx->fuse_mode == 3 && !xf->g_explicit && wide &&
+            xf->m * xf->B * 8 <= (int64_t(64) << 20)) {
+            const size_t zb = sizeof(double) * (size_t)(xf->m * d);
+            double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
+            double* gbuf = (double*)ctx->gfull.get(sizeof(double) * (size_t)(xf->m * xf->B));
+            double* sxd = (double*)ctx->sx.get(sizeof(double) * (size_t)(xf->B * d));
+            CGX_CUDA(cudaEventRecord(ctx->ev_fork, sc.st));
+            CGX_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+            launch_gen_gauss(ctx, xf, 0, xf->B, gbuf, ctx->aux);
+            CGX_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux));
+            ctx->prof.begin(0, sc.st);
+            launch_sketch_dense(ctx, xf, xd, dtype, rld, n, d, sxd, sc.st);
+            ctx->prof.end(0, sc.st);
+            CGX_CUDA(cudaStreamWaitEvent(sc.st, ctx->ev_join, 0));
+            ctx->prof.begin(1, sc.st);
+            launch_gemm_g_ready(ctx, xf, gbuf, sxd, d, zd, sc.st);
+            ctx->prof.end(1, sc.st);
+            if (z_mem == CGX_MEM_HOST) {
+                CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
+                sc.sync();
+            }
+            return;
+        }
         // one-pass kernel (sketch + G generation + contraction) when the shape allows
         if (!ctx->no_fuse) {
             const size_t zb = sizeof(double) * (size_t)(xf->m * d);
@@ -785,6 +821,49 @@ int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_row
         const size_t bytes = sizeof(double) * (size_t)((b1 - b0) * d);
         const double* sd = (const double*)to_device(ctx, ctx->hstage_dev, sx_rows, bytes, sx_mem, sc.st);
         finish_gemm(ctx, xf, sd, d, z, z_mem, sc, b0, b1);
+    });
+}
+
+int cgx_gaussian_project_dense(cgx_ctx* ctx, uint64_t rng_state, int64_t m, const void* x, int dtype, int layout,
+                               int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_mem(x_mem);
+        need_mem(z_mem);
+        if (m < 1) fail(CGX_EINVAL, "anchor extraction: m must be >= 1");
+        if (n < 1) fail(CGX_EINVAL, "gaussian_matrix: dimensions must be positive");
+        if (d < 1) fail(CGX_EINVAL, "anchor extraction: X must have at least one column");
+        CallScope sc(ctx, stream);
+        // G~(r, i) = draw i*m + r of the caller's stream (gaussian_matrix, matrix.cpp:199-207):
+        // the generator seed is the rng's current state.  A stack transform carries (m, n, seed).
+        cgx_xform gx;
+        gx.ctx = ctx;
+        gx.B = n;
+        gx.n = n;
+        gx.m = m;
+        gx.g_seed = rng_state;
+        gx.has_g = true;
+        int64_t rld = ld;
+        const void* xd = dense_rowmajor(ctx, &gx, x, dtype, layout, ld, n, d, x_mem, &rld, sc.st);
+        const double* x64 = (const double*)xd;
+        if (dtype == CGX_F32 || rld != d) {
+            double* w = (double*)ctx->sx.get(sizeof(double) * (size_t)(n * d));
+            if (dtype == CGX_F32)
+                launch_widen_f32(ctx, (const float*)xd, rld, n, d, w, sc.st);
+            else
+                CGX_CUDA(cudaMemcpy2DAsync(w, sizeof(double) * d, xd, sizeof(double) * rld, sizeof(double) * d, n,
+                                           cudaMemcpyDeviceToDevice, sc.st));
+            x64 = w;
+        }
+        const size_t zb = sizeof(double) * (size_t)(m * d);
+        double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
+        ctx->prof.begin(1, sc.st);
+        launch_gauss_gemm_chunked(ctx, &gx, x64, 0, n, d, zd, sc.st, true);
+        ctx->prof.end(1, sc.st);
+        if (z_mem == CGX_MEM_HOST) {
+            CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        }
     });
 }
 
@@ -868,6 +947,10 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->no_fuse = value == 0;
         else if (k == "fuse_mode")
             ctx->fuse_mode = (int)value;
+        else if (k == "rows_per_task" && value >= 1)
+            ctx->opt_rows_per_task = value;
+        else if (k == "grid_waves" && value >= 1)
+            ctx->opt_grid_waves = value;
         else
             fail(CGX_EINVAL, "cgx_set_option: unknown key '" + k + "'");
     });

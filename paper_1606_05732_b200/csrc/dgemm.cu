@@ -135,9 +135,10 @@ __global__ void gen_gauss_cols(uint64_t g_seed, int64_t m, int64_t c0, int64_t c
     }
 }
 
+// gready: all of G[:, b0:b1) already materialized (m x K column-major), or nullptr.
 template <int WGM, int WGN>
 void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d, double* z,
-                cudaStream_t s) {
+                cudaStream_t s, const double* gready = nullptr) {
     constexpr int BM = 32 * WGM, BN = 32 * WGN;
     const int64_t m = xf->m, K = b1 - b0;
     // super-chunk of S bucket-columns: m x S fp64 <= 48 MB (L2-resident), multiple of BK
@@ -150,7 +151,8 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     splits = splits < 1 ? 1 : (splits > max_splits ? max_splits : splits);
     const int64_t kps = ((S + splits - 1) / splits + BK - 1) / BK * BK;
     splits = (S + kps - 1) / kps;
-    double* gbuf = (double*)ctx->xstage.get(sizeof(double) * (size_t)(m * S));
+    // own buffer: xstage may hold the (transposed) X this GEMM is about to read
+    double* gbuf = gready ? nullptr : (double*)ctx->gchunk.get(sizeof(double) * (size_t)(m * S));
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
     auto kern = gemm_dmma<WGM, WGN>;
     const size_t smem = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
@@ -159,7 +161,9 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     for (int64_t c0 = 0; c0 < K; c0 += S) {
         const int64_t cols = K - c0 < S ? K - c0 : S;
         const double* Ach;
-        if (xf->g_explicit) {
+        if (gready) {
+            Ach = gready + c0 * m;
+        } else if (xf->g_explicit) {
             Ach = xf->g_dev + (b0 + c0) * m;  // explicit G is already m x B column-major
         } else {
             int64_t blocks = (m * cols + 255) / 256;
@@ -184,14 +188,49 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
 } // namespace
 
 bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
-                               int64_t d, double* z, cudaStream_t s) {
+                               int64_t d, double* z, cudaStream_t s, bool force) {
     const int64_t m = xf->m;
-    if (m * d <= 64 * 128) return false;  // small Z: the wide in-kernel-generation GEMM is better
+    if (!force && m * d <= 64 * 128) return false;  // small Z: the wide in-kernel-generation GEMM is better
     if (m >= 2 * d)
         run_chunks<4, 2>(ctx, xf, sx, b0, b1, d, z, s);  // 128 x 64 tiles
     else
         run_chunks<2, 4>(ctx, xf, sx, b0, b1, d, z, s);  // 64 x 128 tiles
     return true;
+}
+
+namespace {
+__global__ void widen_f32_kernel(const float* __restrict__ src, int64_t ld, int64_t n, int64_t d,
+                                 double* __restrict__ dst) {
+    const int64_t total = n * d;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / d, j = e - i * d;
+        dst[e] = (double)src[i * ld + j];
+    }
+}
+} // namespace
+
+void launch_widen_f32(cgx_ctx* ctx, const float* src, int64_t ld, int64_t n, int64_t d, double* dst, cudaStream_t s) {
+    widen_f32_kernel<<<ctx->num_sms * 16, 256, 0, s>>>(src, ld, n, d, dst);
+    count_launch(ctx);
+    check_launch("widen_f32");
+}
+
+void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t cols, double* out, cudaStream_t s) {
+    int64_t blocks = (xf->m * cols + 255) / 256;
+    if (blocks > ctx->num_sms * 32) blocks = ctx->num_sms * 32;
+    gen_gauss_cols<<<(unsigned)blocks, 256, 0, s>>>(xf->g_seed, xf->m, c0, cols, out);
+    count_launch(ctx);
+    check_launch("gen_gauss_cols");
+}
+
+void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, const double* sx, int64_t d, double* z,
+                         cudaStream_t s) {
+    if (xf->m >= 8 * d)
+        run_chunks<8, 1>(ctx, xf, sx, 0, xf->B, d, z, s, g);  // 256 x 32 tiles
+    else if (xf->m >= 2 * d)
+        run_chunks<4, 2>(ctx, xf, sx, 0, xf->B, d, z, s, g);
+    else
+        run_chunks<2, 4>(ctx, xf, sx, 0, xf->B, d, z, s, g);
 }
 
 } // namespace cgx

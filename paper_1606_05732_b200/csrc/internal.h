@@ -55,6 +55,10 @@ struct cgx_ctx {
     cgx::DevBuf hstage_dev;                 // device landing zone for host inputs
     cgx::DevBuf sched;                      // work-queue counters of persistent kernels
     cgx::DevBuf gen_tables;                 // synthetic-input generator tables
+    cudaStream_t aux = nullptr;             // side stream: G generation overlapping the sketch
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cgx::DevBuf gfull;                      // L2-sized G for the overlapped two-stage path
+    cgx::DevBuf gchunk;                     // G super-chunk of the chunked stage 2 (dgemm.cu)
     void* pinned = nullptr;                 // pinned staging for pageable host inputs
     size_t pinned_bytes = 0;
     cgx::Profile prof;
@@ -65,6 +69,8 @@ struct cgx_ctx {
     std::unordered_map<void*, size_t> pool_class;
     bool no_fuse = false;                  // option "fuse"=0: always run the two stages
     int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps fused, 2 warp-specialized
+    int64_t opt_rows_per_task = 1024;       // option "rows_per_task": dense stream-kernel task size
+    int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
 };
 
 struct cgx_xform {
@@ -115,9 +121,16 @@ void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr,
 void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d,
                        double* z, cudaStream_t s);
 void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStream_t s);
+// dgemm.cu: G columns [c0, c0+cols) of the transform -> out (m x cols, col-major)
+void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t cols, double* out, cudaStream_t s);
+// dgemm.cu: z = g . sx with g = all of G (m x B col-major) already in memory
+void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, const double* sx, int64_t d, double* z,
+                         cudaStream_t s);
 // dgemm.cu: G super-chunks + pipelined DMMA GEMM; false when Z is small (not used)
 bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
-                               int64_t d, double* z, cudaStream_t s);
+                               int64_t d, double* z, cudaStream_t s, bool force = false);
+// dgemm.cu: row-major fp32 (pitch ld) -> contiguous row-major fp64
+void launch_widen_f32(cgx_ctx* ctx, const float* src, int64_t ld, int64_t n, int64_t d, double* dst, cudaStream_t s);
 void launch_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int* bad,
                                cudaStream_t s);
 

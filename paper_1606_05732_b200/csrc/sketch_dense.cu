@@ -213,7 +213,7 @@ __device__ __forceinline__ void stream_buckets(const T* __restrict__ x, int64_t 
 }
 
 template <typename T, int V>
-__global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restrict__ x, int64_t ld, int64_t d,
+__global__ void __launch_bounds__(256, 3) sketch_dense_stream(const T* __restrict__ x, int64_t ld, int64_t d,
                                                               const uint32_t* __restrict__ perm,
                                                               const uint32_t* __restrict__ offsets, int64_t B,
                                                               int64_t nchunks, int G, double* __restrict__ sx,
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256, 4) sketch_dense_stream(const T* __restric
         const int64_t b0 = bg * G;
         const int nb = (int)min((int64_t)G, B - b0);
         double* out = sx + b0 * d + col0;
-        stream_buckets<T, V>(x, ld, col0, colok, perm, offsets, b0, nb, [&](int i, const double (&acc)[V]) {
+        stream_buckets<T, V, 4096>(x, ld, col0, colok, perm, offsets, b0, nb, [&](int i, const double (&acc)[V]) {
             if (colok) {
 #pragma unroll
                 for (int k = 0; k < V; ++k) out[(int64_t)i * d + k] = acc[k];
@@ -399,14 +399,14 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
     if (R == 1 && !accumulate && ld * (int64_t)sizeof(T) < ((int64_t)1 << 32)) {
         // ~1K rows per warp task, at most 31 buckets (one offsets load)
         const int64_t rows_per_bucket = xf->n / xf->B + 1;
-        int64_t G = 1024 / rows_per_bucket;
+        int64_t G = ctx->opt_rows_per_task / rows_per_bucket;
         G = G < 1 ? 1 : (G > 31 ? 31 : G);
         const int64_t nchunks = (d + CW - 1) / CW;
         const int64_t tasks = (xf->B + G - 1) / G * nchunks;
         auto kern = sketch_dense_stream<T, V>;
         int per_sm = 0;
         CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
-        int64_t blocks = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);
+        int64_t blocks = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm) * ctx->opt_grid_waves;
         if (blocks > (tasks + 7) / 8) blocks = (tasks + 7) / 8;
         unsigned* ctr = (unsigned*)ctx->sched.get(sizeof(unsigned));
         CGX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));

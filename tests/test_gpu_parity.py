@@ -295,6 +295,31 @@ def test_stage2_large_z(cg, restatement, m, d, B):
     assert rel_fro(z2, ref) <= 1e-14
 
 
+@pytest.mark.parametrize("n,d,m,dtype", [(5000, 24, 16, np.float64), (70000, 32, 64, np.float32),
+                                         (3000, 200, 40, np.float64)])
+def test_dense_gaussian_projection(cg, restatement, n, d, m, dtype):
+    """Dense-Gaussian baseline G~.X (gaussian_matrix(m, n, rng), matrix.cpp:199-207) vs the
+    oracle, and the rng advancing by exactly m*n draws."""
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, d)).astype(dtype)
+    r = cg.SeededRng(77)
+    state0 = r._state
+    z = cg.gaussian_project(x, m, r)
+    G = restatement.gaussian(state0, m, n)  # draws of the stream continuing from state0
+    ref = restatement.gemm(G, x.astype(np.float64))
+    assert rel_fro(z, ref) <= Z_TOL
+    assert r.next_u64() == oracle.draw(77, m * n)  # next draw after m*n normals
+
+
+def test_gp_nmf_vs_reference(cg, reference):
+    for trial in range(3):
+        x = reference.generate_separable(80, 50, 6, 300 + trial)
+        ref = reference.gp_nmf(reference.dense(x), 20, 400 + trial)
+        got = cg.gp_nmf(np.asfortranarray(x), 20, cg.SeededRng(400 + trial))
+        assert got.i_max == list(ref["i_max"]) and got.i_min == list(ref["i_min"])
+        assert got.tie_rows == ref["tie_rows"]
+
+
 # ------------------------------------------------------------------------- anchors
 def test_cg_nmf_golden(cg, golden):
     a = cg.cg_nmf(np.asfortranarray(golden["nmf_x"]), 12, 60, cg.SeededRng(7006))
@@ -353,10 +378,11 @@ def test_device_tensors_match_host(cg, restatement):
 @pytest.mark.parametrize("d,m,dtype", [(32, 64, np.float32), (24, 16, np.float32), (64, 32, np.float32),
                                        (128, 32, np.float32), (100, 8, np.float32), (32, 64, np.float64),
                                        (64, 64, np.float64), (40, 100, np.float32), (33, 5, np.float64)])
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_fused_matches_two_stage(cg, restatement, d, m, dtype, mode):
     """The one-pass kernels (sketch + G + contraction; mode 1 all-warps, mode 2
-    warp-specialized) vs the two-stage path and the oracle."""
+    warp-specialized) and mode 3 (G generated on a side stream under the sketch, then a
+    DMMA GEMM) vs the two-stage path and the oracle."""
     import torch
 
     rng = np.random.default_rng(d * 1000 + m)

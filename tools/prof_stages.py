@@ -21,6 +21,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--fuse", type=int, default=1)
     ap.add_argument("--fuse_mode", type=int, default=2)
+    ap.add_argument("--rows_per_task", type=int, default=1024)
+    ap.add_argument("--grid_waves", type=int, default=1)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--what", default="apply")
     ap.add_argument("--n", type=int, default=1 << 24)
@@ -31,6 +33,8 @@ def main():
     ctx = cg.context(0)
     ctx.set_option("fuse", a.fuse)
     ctx.set_option("fuse_mode", a.fuse_mode)
+    ctx.set_option("rows_per_task", a.rows_per_task)
+    ctx.set_option("grid_waves", a.grid_waves)
     t = cg.countgauss_new(a.m, a.B, a.n, cg.SeededRng(12345))
     x = bench_data.dense_normal(a.n, a.d, seed=7)
     z = torch.empty((a.d, a.m), dtype=torch.float64, device="cuda").t()
