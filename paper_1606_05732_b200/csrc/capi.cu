@@ -951,6 +951,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_rows_per_task = value;
         else if (k == "grid_waves" && value >= 1)
             ctx->opt_grid_waves = value;
+        else if (k == "ws_gw" && value >= 0 && value <= 8)
+            ctx->opt_ws_gw = value;
         else
             fail(CGX_EINVAL, "cgx_set_option: unknown key '" + k + "'");
     });

@@ -71,6 +71,7 @@ struct cgx_ctx {
     int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps fused, 2 warp-specialized
     int64_t opt_rows_per_task = 1024;       // option "rows_per_task": dense stream-kernel task size
     int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
+    int64_t opt_ws_gw = 0;                  // option "ws_gw": buckets per sketch warp per tile (0 = auto)
 };
 
 struct cgx_xform {

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--fuse_mode", type=int, default=2)
     ap.add_argument("--rows_per_task", type=int, default=1024)
     ap.add_argument("--grid_waves", type=int, default=1)
+    ap.add_argument("--ws_gw", type=int, default=0)
+    ap.add_argument("--explicit_g", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--what", default="apply")
     ap.add_argument("--n", type=int, default=1 << 24)
@@ -35,8 +37,13 @@ def main():
     ctx.set_option("fuse_mode", a.fuse_mode)
     ctx.set_option("rows_per_task", a.rows_per_task)
     ctx.set_option("grid_waves", a.grid_waves)
+    ctx.set_option("ws_gw", a.ws_gw)
     t = cg.countgauss_new(a.m, a.B, a.n, cg.SeededRng(12345))
     x = bench_data.dense_normal(a.n, a.d, seed=7)
+    if a.explicit_g:  # G read from memory instead of generated (isolates the generation cost)
+        gmat = torch.empty((a.B, a.m), dtype=torch.float64, device="cuda")
+        check(lib.cgx_fill_gaussian(ctx.h, t._xf.h, gmat.data_ptr(), CGX_MEM_DEVICE, C.c_void_p(1)))
+        check(lib.cgx_xform_set_gaussian_explicit(ctx.h, t._xf.h, a.m, gmat.data_ptr(), CGX_MEM_DEVICE))
     z = torch.empty((a.d, a.m), dtype=torch.float64, device="cuda").t()
     g = torch.empty((a.B, a.m), dtype=torch.float64, device="cuda")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
