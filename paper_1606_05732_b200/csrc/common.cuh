@@ -92,9 +92,53 @@ __device__ __forceinline__ double acklam(double p) {
     return upper ? -x : x;
 }
 
-// inverse_normal_cdf (rng.cpp:45-55) for p in (0,1): Acklam + one Halley step.
+// Out of line: taken by ~4e-6 of draws, and inlined it costs the warp-specialised kernels
+// registers on their hot path.
+static __device__ __noinline__ double acklam_far(double p) { return acklam(p); }
+
+// Starting point for the Halley step of inverse_normal_cdf: Acklam's rational, with the
+// central region in fp64 (FMA-contracted; its polynomial cancels near |p-0.5| = 0.475, so
+// fp32 would lose 1e-4 there) and the tails -- whose log/sqrt dominate the FP64 cost and
+// which diverge a warp 80% of the time -- in fp32 with MUFU log/sqrt (~4e-7 relative).
+// Halley's cubic convergence takes either start below fp64 resolution, so the refined
+// quantile is limited by erfc exactly as the reference's is (the reference starts from
+// Acklam's 1.15e-9).  The tail variable (p or 1-p) is formed in fp64 before narrowing.
+__device__ __forceinline__ double acklam_start(double p) {
+    const double a0 = -3.969683028665376e+01, a1 = 2.209460984245205e+02, a2 = -2.759285104469687e+02,
+                 a3 = 1.383577518672690e+02, a4 = -3.066479806614716e+01, a5 = 2.506628277459239e+00;
+    const double b0 = -5.447609879822406e+01, b1 = 1.615858368580409e+02, b2 = -1.556989798598866e+02,
+                 b3 = 6.680131188771972e+01, b4 = -1.328068155288572e+01;
+    const float c0 = -7.784894002430293e-03f, c1 = -3.223964580411365e-01f, c2 = -2.400758277161838e+00f,
+                c3 = -2.549732539343734e+00f, c4 = 4.374664141464968e+00f, c5 = 2.938163982698783e+00f;
+    const float d0 = 7.784695709041462e-03f, d1 = 3.224671290700398e-01f, d2 = 2.445134137142996e+00f,
+                d3 = 3.754408661907416e+00f;
+    const double p_low = 0.02425;
+    if (p >= p_low && p <= 1.0 - p_low) {
+        const double q = p - 0.5;
+        const double r = q * q;
+        const double num = (((((a0 * r + a1) * r + a2) * r + a3) * r + a4) * r + a5) * q;
+        const double den = ((((b0 * r + b1) * r + b2) * r + b3) * r + b4) * r + 1.0;
+        return num / den;
+    }
+    const bool upper = p > 1.0 - p_low;
+    const double t64 = upper ? 1.0 - p : p;
+    // Far tails (t < 2^-20, one draw in ~5e5 per tail): the reference's Halley residual is
+    // rounded at ulp(p), which near p = 1 resolves x only to ulp(p)/phi(x) -- there its
+    // output is its Acklam start plus noise, so the start must be the reference's own.
+    // (Also keeps fp32 away from t below FLT_MIN.)
+    if (t64 < 0x1.0p-20) return acklam_far(p);
+    const float t = (float)t64;
+    const float q = sqrtf(-2.0f * logf(t));
+    const float num = ((((c0 * q + c1) * q + c2) * q + c3) * q + c4) * q + c5;
+    const float den = (((d0 * q + d1) * q + d2) * q + d3) * q + 1.0f;
+    const double x = (double)(num / den);
+    return upper ? -x : x;
+}
+
+// inverse_normal_cdf (rng.cpp:45-55) for p in (0,1): one Halley step against erfc from an
+// Acklam start (fp32 in the near tails, see acklam_start).
 __device__ __forceinline__ double inverse_normal_cdf(double p) {
-    double x = acklam(p);
+    double x = acklam_start(p);
     const double sqrt2pi = 2.5066282746310005024;
     const double sqrt2 = 1.41421356237309504880;
     double e = __dadd_rn(CGX_M(0.5, erfc(__ddiv_rn(-x, sqrt2))), -p);

@@ -108,6 +108,30 @@ def test_inverse_normal_cdf_known_quantiles(cg, golden):
             cg.inverse_normal_cdf(bad)
 
 
+def test_inverse_normal_cdf_tails_and_region_edges(cg, restatement):
+    # The device starts Halley from an fp32 Acklam value; the refined quantile must agree
+    # with the reference's (fp64 Acklam start) to erfc resolution over the whole (0,1),
+    # including the extreme draws uniform53 can produce and both sides of p_low.
+    lo = 0.5 * 2.0 ** -53
+    p = np.concatenate([
+        np.array([lo, 3 * lo, 1e-15, 1e-12, 1e-9, 1e-6, 1e-3, 0.02425, np.nextafter(0.02425, 0),
+                  np.nextafter(0.02425, 1), 0.3, 0.5 - 2 ** -40, 0.5, 0.5 + 2 ** -40, 0.97575,
+                  np.nextafter(0.97575, 0), np.nextafter(0.97575, 1), 1 - 1e-6, 1 - 1e-9, 1 - 1e-12,
+                  1 - 2.0 ** -52, 1 - 2.0 ** -53]),
+        np.random.default_rng(3).random(4000),
+        np.exp(-np.random.default_rng(4).uniform(0, 36, 2000)),
+    ])
+    got = cg.inverse_normal_cdf_array(p)
+    ref = np.array([restatement.inverse_normal_cdf(float(v)) for v in p])
+    # The reference's Halley residual e = 0.5*erfc(-x/sqrt2) - p is rounded at ulp(p), so
+    # its own x is resolved only to ~ulp(p)/phi(x) (1e-10 near p = 1 - 1e-6): a different
+    # start value may land anywhere inside that band.
+    phi = np.exp(-0.5 * ref * ref) / np.sqrt(2 * np.pi)
+    tol = 4e-15 + 1e-13 * np.abs(ref) + 4 * np.spacing(p) / phi
+    excess = np.abs(got - ref) - tol
+    assert np.all(excess <= 0), (float(p[np.argmax(excess)]), float(excess.max()))
+
+
 def test_normal_moments(cg):
     # test_rng.cpp:23-37 on the GPU generator (1e6 draws)
     t = cg.countgauss_new(1000, 1000, 10, cg.SeededRng(2024))
