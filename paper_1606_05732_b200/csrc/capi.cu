@@ -953,6 +953,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_grid_waves = value;
         else if (k == "ws_gw" && value >= 0 && value <= 8)
             ctx->opt_ws_gw = value;
+        else if (k == "async_stages" && (value == 0 || (value >= 2 && value <= 4)))
+            ctx->opt_async = value;
         else
             fail(CGX_EINVAL, "cgx_set_option: unknown key '" + k + "'");
     });

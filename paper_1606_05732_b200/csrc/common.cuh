@@ -179,6 +179,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// ---- cp.async (LDGSTS): 16 B global -> shared, bypassing L1; completion by group ------
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Named barrier among `count` threads (id 1..15; 0 is __syncthreads).
 __device__ __forceinline__ void named_sync(unsigned id, unsigned count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

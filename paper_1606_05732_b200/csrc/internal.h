@@ -72,6 +72,7 @@ struct cgx_ctx {
     int64_t opt_rows_per_task = 1024;       // option "rows_per_task": dense stream-kernel task size
     int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
     int64_t opt_ws_gw = 0;                  // option "ws_gw": buckets per sketch warp per tile (0 = auto)
+    int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)
 };
 
 struct cgx_xform {

@@ -49,6 +49,15 @@ __device__ __forceinline__ void load_vec(const T* p, T (&out)[V]) {
     for (int k = 0; k < V; ++k) out[k] = e[k];
 }
 
+template <typename T, int V>
+__device__ __forceinline__ void load_smem_vec(const T* p, T (&out)[V]) {
+    using VT = typename Vec<T, V>::type;
+    VT v = *reinterpret_cast<const VT*>(p);
+    const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int k = 0; k < V; ++k) out[k] = e[k];
+}
+
 __device__ __forceinline__ float negate_if(float v, uint32_t neg) {
     return __int_as_float(__float_as_int(v) ^ (int)(neg & kNegBit));
 }
@@ -210,6 +219,148 @@ __device__ __forceinline__ void stream_buckets(const T* __restrict__ x, int64_t 
         }
     }
     while (cur < nb) flush();
+}
+
+// stream_buckets with the row gather moved off the register file: each 32-row chunk of
+// the warp's perm stretch is fetched by cp.async (16 B pieces, Q per row) into an
+// S-slot ring in shared memory, S-1 chunks ahead of the adds, so every warp keeps
+// (S-1) x 32 rows in flight continuously instead of a batch that drains before each
+// round of adds.  The perm entries of a chunk are loaded one chunk before its copies are
+// issued, the chunk's sign bits ride along in the ring (sneg), and the adds are the same
+// ascending-order adds as stream_buckets -- S.X stays bit-identical.
+// Requires: row pitch, column base and the warp's in-range columns in whole 16 B pieces
+// (host-checked); x 16 B aligned.  `qv` = valid 16 B pieces per row of this chunk.
+template <typename T, int V, int S, typename Sink>
+__device__ __forceinline__ void stream_buckets_async(const T* __restrict__ x, int64_t ld, int64_t cw0, int qv,
+                                                     const uint32_t* __restrict__ perm,
+                                                     const uint32_t* __restrict__ offsets, int64_t b0, int nb,
+                                                     T* ring, uint32_t* sneg, Sink&& sink) {
+    constexpr int CW = 32 * V;
+    constexpr int CB = CW * (int)sizeof(T);  // bytes per row chunk
+    constexpr int Q = CB / 16;               // 16 B pieces per row chunk (power of two)
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t offk = (int)lane <= nb ? __ldg(offsets + b0 + lane) : 0u;
+    const uint32_t P0 = __shfl_sync(0xffffffffu, offk, 0);
+    const uint32_t P1 = __shfl_sync(0xffffffffu, offk, nb);
+    int cur = 0;
+    uint32_t nextb = __shfl_sync(0xffffffffu, offk, 1);
+    double acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.0;
+    auto flush = [&]() {
+        sink(cur, acc);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = 0.0;
+        ++cur;
+        nextb = __shfl_sync(0xffffffffu, offk, min(cur + 1, 31));
+    };
+
+    const char* xc = reinterpret_cast<const char*>(x + cw0);
+    const uint32_t row_bytes = (uint32_t)(ld * (int64_t)sizeof(T));
+    const uint32_t nchunk = (P1 - P0 + 31) / 32;
+    auto perm_of = [&](uint32_t j) -> uint32_t {
+        const uint32_t pos = P0 + j * 32 + lane;
+        return (j < nchunk && pos < P1) ? __ldg(perm + pos) : kNegBit;  // kNegBit alone = padding
+    };
+    auto issue = [&](uint32_t j, uint32_t pe) {
+        if (j < nchunk) {
+            const int slot = (int)(j % S);
+            char* dst = reinterpret_cast<char*>(ring) + (size_t)slot * 32 * CB;
+            const uint32_t cnt = min(32u, P1 - (P0 + j * 32));
+            const uint32_t neg = __ballot_sync(0xffffffffu, pe & kNegBit);
+            if (lane == 0) sneg[slot] = neg;
+            const uint32_t prow = pe & kRowMask;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+                const int e = (int)lane + 32 * k;
+                const int t = e / Q, q = e % Q;
+                const uint32_t r = __shfl_sync(0xffffffffu, prow, t);
+                if ((uint32_t)t < cnt && q < qv) cpa16(dst + t * CB + q * 16, xc + (size_t)r * row_bytes + q * 16);
+            }
+        }
+        cpa_commit();  // one group per chunk slot, empty past the end: uniform group counting
+    };
+
+    uint32_t pe_next = perm_of(0);
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) {
+        const uint32_t pe = pe_next;
+        pe_next = perm_of(j + 1);
+        issue(j, pe);
+    }
+    for (uint32_t j = 0; j < nchunk; ++j) {
+        {   // keep S-1 chunks in flight: issue chunk j+S-1 into the slot freed at j-1
+            const uint32_t pe = pe_next;
+            pe_next = perm_of(j + S);
+            issue(j + S - 1, pe);
+        }
+        cpa_wait<S - 1>();
+        __syncwarp();
+        const int slot = (int)(j % S);
+        const T* src = ring + (size_t)slot * 32 * CW + lane * V;
+        const uint32_t nm = sneg[slot];
+        const uint32_t base = P0 + j * 32;
+        const int cnt = (int)min(32u, P1 - base);
+        if (cnt == 32 && nextb >= base + 32) {
+#pragma unroll 8
+            for (int t = 0; t < 32; ++t) {
+                T v[V];
+                load_smem_vec<T, V>(src + t * CW, v);
+#pragma unroll
+                for (int k = 0; k < V; ++k) acc[k] += (double)flip_sign(v[k], (nm >> t) & 1u);
+            }
+        } else {
+            for (int t = 0; t < cnt; ++t) {
+                while (base + t == nextb) flush();
+                T v[V];
+                load_smem_vec<T, V>(src + t * CW, v);
+#pragma unroll
+                for (int k = 0; k < V; ++k) acc[k] += (double)flip_sign(v[k], (nm >> t) & 1u);
+            }
+        }
+        __syncwarp();  // every lane is done with this slot before it is refilled
+    }
+    cpa_wait<0>();
+    while (cur < nb) flush();
+}
+
+// Persistent stream sketch over the cp.async ring (option async_stages = S): same tasks
+// and output as sketch_dense_stream.  Shared memory: per warp S x 32 x CB ring + S masks.
+template <typename T, int V, int S>
+__global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ x, int64_t ld, int64_t d,
+                                                          const uint32_t* __restrict__ perm,
+                                                          const uint32_t* __restrict__ offsets, int64_t B,
+                                                          int64_t nchunks, int G, double* __restrict__ sx,
+                                                          unsigned* __restrict__ next_task) {
+    constexpr int CW = 32 * V;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T* ring = reinterpret_cast<T*>(dsm) + (size_t)warp * S * 32 * CW;
+    uint32_t* sneg = reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(dsm) + (size_t)(blockDim.x >> 5) * S * 32 * CW) +
+                     warp * S;
+    const int64_t ngroups = (B + G - 1) / G;
+    const int64_t ntasks = ngroups * nchunks;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(next_task, 1u);
+        const int64_t task = __shfl_sync(0xffffffffu, t, 0);
+        if (task >= ntasks) break;
+        const int64_t bg = task / nchunks;
+        const int64_t cw0 = (task - bg * nchunks) * CW;
+        const int64_t col0 = cw0 + (int64_t)lane * V;
+        const bool colok = col0 < d;
+        const int qv = (int)min((int64_t)(CW * sizeof(T) / 16), (d - cw0) * (int64_t)sizeof(T) / 16);
+        const int64_t b0 = bg * G;
+        const int nb = (int)min((int64_t)G, B - b0);
+        double* out = sx + b0 * d + col0;
+        stream_buckets_async<T, V, S>(x, ld, cw0, qv, perm, offsets, b0, nb, ring, sneg,
+                                      [&](int i, const double (&acc)[V]) {
+                                          if (colok) {
+#pragma unroll
+                                              for (int k = 0; k < V; ++k) out[(int64_t)i * d + k] = acc[k];
+                                          }
+                                      });
+    }
 }
 
 template <typename T, int V>
@@ -403,6 +554,29 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
         G = G < 1 ? 1 : (G > 31 ? 31 : G);
         const int64_t nchunks = (d + CW - 1) / CW;
         const int64_t tasks = (xf->B + G - 1) / G * nchunks;
+        const int S = (int)ctx->opt_async;
+        const size_t CB = (size_t)CW * sizeof(T);
+        if (S >= 2 && (uintptr_t)x % 16 == 0 && (ld * sizeof(T)) % 16 == 0 && (d * sizeof(T)) % 16 == 0) {
+            // cp.async ring: W warps per CTA, each with S x 32 rows x CB of shared memory
+            const size_t per_warp = (size_t)S * 32 * CB + (size_t)S * 4;
+            int W = (int)((200 * 1024) / per_warp);
+            W = W > 8 ? 8 : (W < 1 ? 1 : W);
+            const size_t smem = per_warp * W;
+            auto kern = S == 2 ? sketch_dense_async<T, V, 2> : S == 3 ? sketch_dense_async<T, V, 3>
+                                                                       : sketch_dense_async<T, V, 4>;
+            CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int per_sm = 0;
+            CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem));
+            int64_t blocks = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);
+            if (blocks > (tasks + W - 1) / W) blocks = (tasks + W - 1) / W;
+            unsigned* ctr = (unsigned*)ctx->sched.get(sizeof(unsigned));
+            CGX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+            kern<<<(unsigned)blocks, 32 * W, smem, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks, (int)G, sx,
+                                                        ctr);
+            count_launch(ctx);
+            check_launch("sketch_dense_async");
+            return;
+        }
         auto kern = sketch_dense_stream<T, V>;
         int per_sm = 0;
         CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
@@ -454,7 +628,9 @@ void dispatch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t
 //    into registers (MR rows x V columns per thread), fixed order -> deterministic.
 // Hand-off: mbarrier `full[buf]` (256 sketch arrivals) and `freed[buf]` (128 math
 // arrivals) per slab; a named barrier orders the math warps' G slab reuse.
-template <typename T, int V, int MR>
+// S > 0: the sketch warps gather through an S-slot cp.async ring (stream_buckets_async)
+// placed after the two slabs in dynamic shared memory, instead of register batches.
+template <typename T, int V, int MR, int S>
 __global__ void __launch_bounds__(384, 2) countgauss_dense_ws(const T* __restrict__ x, int64_t ld, int64_t d,
                                                               const uint32_t* __restrict__ perm,
                                                               const uint32_t* __restrict__ offsets, int64_t B,
@@ -486,12 +662,20 @@ __global__ void __launch_bounds__(384, 2) countgauss_dense_ws(const T* __restric
             double* slab = fsm + buf * slab_sz + (int64_t)warp * Gw * CW + lane * V;
             const int64_t b0 = tile * TB + (int64_t)warp * Gw;
             const int nb = b0 < B ? (int)min((int64_t)Gw, B - b0) : 0;
-            if (nb > 0) {
-                stream_buckets<T, V, 4096>(x, ld, col0, colok, perm, offsets, b0, nb,
-                                           [&](int i, const double (&acc)[V]) {
+            auto sink = [&](int i, const double (&acc)[V]) {
 #pragma unroll
-                                               for (int q = 0; q < V; ++q) slab[i * CW + q] = colok ? acc[q] : 0.0;
-                                           });
+                for (int q = 0; q < V; ++q) slab[i * CW + q] = colok ? acc[q] : 0.0;
+            };
+            if (nb > 0) {
+                if constexpr (S > 0) {
+                    T* ring = reinterpret_cast<T*>(fsm + 2 * slab_sz) + (size_t)warp * S * 32 * CW;
+                    uint32_t* sneg = reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(fsm + 2 * slab_sz) +
+                                                                 (size_t)8 * S * 32 * CW) + warp * S;
+                    const int qv = (int)min((int64_t)(CW * sizeof(T) / 16), d * (int64_t)sizeof(T) / 16);
+                    stream_buckets_async<T, V, S>(x, ld, 0, qv, perm, offsets, b0, nb, ring, sneg, sink);
+                } else {
+                    stream_buckets<T, V, 4096>(x, ld, col0, colok, perm, offsets, b0, nb, sink);
+                }
             }
             for (int i = nb; i < Gw; ++i)
 #pragma unroll
@@ -675,13 +859,19 @@ template <typename T, int V, int MR>
 void launch_ws(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
     constexpr int CW = 32 * V;
     const int64_t B = xf->B, m = xf->m;
-    auto kern = countgauss_dense_ws<T, V, MR>;
+    int S = (int)ctx->opt_async;
+    if (S > 3 || (uintptr_t)x % 16 != 0 || (ld * sizeof(T)) % 16 != 0 || (d * sizeof(T)) % 16 != 0 ||
+        8 * (size_t)S * 32 * CW * sizeof(T) > 128 * 1024)
+        S = 0;
+    auto kern = S == 2 ? countgauss_dense_ws<T, V, MR, 2>
+                       : (S == 3 ? countgauss_dense_ws<T, V, MR, 3> : countgauss_dense_ws<T, V, MR, 0>);
     int64_t Gw = B / (8 * 32 * (int64_t)ctx->num_sms * 2);
     Gw = Gw < 1 ? 1 : (Gw > 8 ? 8 : Gw);
     if (ctx->opt_ws_gw > 0) Gw = ctx->opt_ws_gw;
     const int64_t TB = 8 * Gw;
     const int64_t ntiles = (B + TB - 1) / TB;
-    const size_t smem = sizeof(double) * (size_t)(2 * (TB * CW + m * TB));
+    const size_t ring = S > 0 ? 8 * ((size_t)S * 32 * CW * sizeof(T) + (size_t)S * 4) : 0;
+    const size_t smem = sizeof(double) * (size_t)(2 * (TB * CW + m * TB)) + ring;
     CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 384, smem));

@@ -433,6 +433,39 @@ def test_fused_matches_two_stage(cg, restatement, d, m, dtype, mode):
     assert rel_fro(z_fused, z_two) <= Z_TOL
 
 
+@pytest.mark.parametrize("d,dtype,offset", [(32, np.float32, 0), (40, np.float32, 0), (100, np.float32, 0),
+                                            (128, np.float32, 0), (256, np.float32, 0), (32, np.float64, 0),
+                                            (64, np.float64, 0), (36, np.float32, 0), (32, np.float32, 1),
+                                            (48, np.float64, 0)])
+@pytest.mark.parametrize("stages", [0, 2, 3, 4])
+def test_async_gather_ring(cg, restatement, d, dtype, offset, stages):
+    """Row gather through the cp.async shared-memory ring (option async_stages) vs register
+    batches (0): S.X bit-exact against the oracle for every ring depth and row width --
+    partial last column chunks, and a misaligned base (offset) that must fall back -- and
+    the one-pass Z deterministic and within tolerance."""
+    import torch
+
+    rng = np.random.default_rng(d * 10 + stages)
+    n, B, m = 30000, 501, 16
+    xfull = rng.standard_normal((n, d + offset)).astype(dtype)
+    x = np.ascontiguousarray(xfull[:, offset:]) if offset == 0 else xfull[:, offset:]
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(d + 7))
+    ctx = cg.context()
+    xt = torch.from_numpy(xfull).cuda()
+    xd = xt[:, offset:] if offset else xt
+    ctx.set_option("async_stages", stages)
+    try:
+        sx = cg.countsketch_apply(t, xd).cpu().numpy()
+        z1 = cg.countgauss_apply(t, xd).cpu().numpy()
+        z2 = cg.countgauss_apply(t, xd).cpu().numpy()
+    finally:
+        ctx.set_option("async_stages", 2)
+    z_ref, sx_ref = restatement.countgauss(d + 7, m, B, x=np.ascontiguousarray(x))
+    assert np.array_equal(sx, sx_ref)
+    assert np.array_equal(z1, z2)
+    assert rel_fro(z1, z_ref) <= Z_TOL
+
+
 def test_deterministic_across_runs(cg):
     rng = np.random.default_rng(12)
     x = rng.standard_normal((50000, 24))

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--grid_waves", type=int, default=1)
     ap.add_argument("--ws_gw", type=int, default=0)
     ap.add_argument("--explicit_g", type=int, default=0)
+    ap.add_argument("--async_stages", type=int, default=0)
+    ap.add_argument("--dtype", default="f32")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--what", default="apply")
     ap.add_argument("--n", type=int, default=1 << 24)
@@ -38,8 +40,11 @@ def main():
     ctx.set_option("rows_per_task", a.rows_per_task)
     ctx.set_option("grid_waves", a.grid_waves)
     ctx.set_option("ws_gw", a.ws_gw)
+    ctx.set_option("async_stages", a.async_stages)
     t = cg.countgauss_new(a.m, a.B, a.n, cg.SeededRng(12345))
     x = bench_data.dense_normal(a.n, a.d, seed=7)
+    if a.dtype == "f64":
+        x = x.double()
     if a.explicit_g:  # G read from memory instead of generated (isolates the generation cost)
         gmat = torch.empty((a.B, a.m), dtype=torch.float64, device="cuda")
         check(lib.cgx_fill_gaussian(ctx.h, t._xf.h, gmat.data_ptr(), CGX_MEM_DEVICE, C.c_void_p(1)))
@@ -47,6 +52,7 @@ def main():
     z = torch.empty((a.d, a.m), dtype=torch.float64, device="cuda").t()
     g = torch.empty((a.B, a.m), dtype=torch.float64, device="cuda")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ctx.profile(True)
     for rep in range(a.reps):
         ev[0].record()
         if a.what == "apply":
@@ -58,6 +64,10 @@ def main():
         ev[1].record()
         torch.cuda.synchronize()
         print(f"{a.what} fuse={a.fuse} rep {rep}: {ev[0].elapsed_time(ev[1]):.3f} ms")
+    for st in (0, 1):
+        ms, n = ctx.profile_read(st)
+        if n:
+            print(f"  stage {st}: {ms / n:.3f} ms/launch over {n} (includes warm-up)")
 
 
 if __name__ == "__main__":
