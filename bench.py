@@ -205,6 +205,9 @@ def run_ours(args):
 
     c = CONFIGS[args.config]
     ctx = cg.context(local)
+    for kv in args.opt:
+        k, v = kv.split("=", 1)
+        ctx.set_option(k, int(v))
     n, d, B, m = c["n"], c["d"], c["B"], c["m"]
     r0, r1 = shard_range(n, world, rank)
     rows = r1 - r0
@@ -389,6 +392,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ablation", action="store_true", help="skip the dense-Gaussian G~.X ablation")
+    ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
+                    help="cgx_set_option before timing (A/B of kernel variants)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3", file=sys.stderr)

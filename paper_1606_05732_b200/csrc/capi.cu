@@ -268,8 +268,11 @@ void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
         vp = base + off_v;
     }
     ctx->prof.begin(0, s);
-    launch_sketch_csr(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, sx_dev,
-                      csr_chunk_rows(n, xf->B, d), s);
+    const int64_t chunk_rows = csr_chunk_rows(n, xf->B, d);
+    if (chunk_rows == 0 && csr_partition_applies(ctx, n, xf->B, d, nnz))
+        launch_sketch_csr_partition(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, nnz, sx_dev, s);
+    else
+        launch_sketch_csr(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, sx_dev, chunk_rows, s);
     ctx->prof.end(0, s);
 }
 
@@ -404,6 +407,7 @@ int cgx_free(cgx_ctx* ctx) {
         cudaStreamDestroy(ctx->aux);
         ctx->gfull.release();
         ctx->gchunk.release();
+        for (DevBuf& b : ctx->part) b.release();
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -955,6 +959,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_ws_gw = value;
         else if (k == "async_stages" && (value == 0 || (value >= 2 && value <= 4)))
             ctx->opt_async = value;
+        else if (k == "csr_mode" && value >= 0 && value <= 2)
+            ctx->opt_csr_mode = value;
         else
             fail(CGX_EINVAL, "cgx_set_option: unknown key '" + k + "'");
     });

@@ -198,6 +198,23 @@ __device__ __forceinline__ void named_sync(unsigned id, unsigned count) {
 constexpr uint32_t kRowMask = 0x7FFFFFFFu;
 constexpr uint32_t kNegBit = 0x80000000u;
 
+// Mask of the lanes whose v equals this lane's (the result of __match_any_sync), for
+// v < 2^nbits, built from nbits ballots.  MATCH.ANY resolves one distinct value per pass,
+// so on 32 mostly-distinct digits -- the common case for the bucket and bin digits here
+// -- it costs tens of times more than these vote-unit instructions.  All lanes active;
+// nbits <= 12.
+__device__ __forceinline__ unsigned match_any_bits(uint32_t v, int nbits) {
+    unsigned m = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 12; ++b) {  // nbits <= 12, warp-uniform
+        if (b < nbits) {
+            const unsigned x = __ballot_sync(0xffffffffu, (v >> b) & 1u);
+            m &= x ^ (((v >> b) & 1u) - 1u);  // x where my bit is 1, ~x where it is 0
+        }
+    }
+    return m;
+}
+
 __device__ __forceinline__ int warp_incl_scan(int v, unsigned lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

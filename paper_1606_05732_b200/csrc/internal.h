@@ -73,6 +73,8 @@ struct cgx_ctx {
     int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
     int64_t opt_ws_gw = 0;                  // option "ws_gw": buckets per sketch warp per tile (0 = auto)
     int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)
+    int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 2 stable partition
+    cgx::DevBuf part[6];                    // csr_partition.cu scratch: counters, payload copies, row keys
 };
 
 struct cgx_xform {
@@ -117,6 +119,12 @@ void launch_transpose_sx(cgx_ctx* ctx, const double* src, int64_t B, int64_t d, 
 void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
                        const void* vals, int dtype, int64_t n, int64_t d, double* sx, int64_t chunk_rows,
                        cudaStream_t s);
+
+// csr_partition.cu: the same S.X by stable two-level partition of the nonzeros (short rows)
+bool csr_partition_applies(const cgx_ctx* ctx, int64_t n, int64_t B, int64_t d, int64_t nnz);
+void launch_sketch_csr_partition(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols,
+                                 int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
+                                 double* sx, cudaStream_t s);
 
 // gauss_gemm.cu: z (col-major m x d) = G . sx (row-major B x d)
 // Buckets [b0, b1) only: sx points at row b0 (split-K across ranks).

@@ -255,6 +255,52 @@ def test_csr_bit_exact_shapes(cg, restatement, n, d, B, density, idx, val):
     assert rel_fro(cg.countgauss_apply(t, x), z_ref) <= Z_TOL or np.abs(z_ref).max() == 0
 
 
+def _csr_with_dups(rng, n, d, mean_len):
+    """Rows of Poisson(mean_len) nonzeros with repeated and unsorted columns (legal CSR
+    the reference accumulates in stored order)."""
+    lens = rng.poisson(mean_len, n)
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    c = rng.integers(0, d, int(rp[-1]))
+    v = rng.standard_normal(int(rp[-1]))
+    return rp, c, v
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("n,d,B,mean_len,idx,val", [
+    (60000, 256, 262144, 2.5, np.int32, np.float32),   # c3-like: B >> n/B, short rows
+    (40000, 256, 4099, 2.5, np.int64, np.float64),
+    (50000, 512, 1 << 16, 10.0, np.int32, np.float32),  # c5-like widths
+    (30000, 1, 300, 1.0, np.int32, np.float64),
+    (30000, 3, 70000, 2.0, np.int64, np.float32),
+    (20000, 40, 5, 6.0, np.int32, np.float32),         # few buckets: long runs per bin
+    (25000, 1000, 33333, 3.0, np.int32, np.float64),   # d not a power of two, padded slices
+])
+def test_csr_partition_bit_exact(cg, restatement, mode, n, d, B, mean_len, idx, val):
+    """Stable two-level partition (csr_mode 2) and row gather (1): S.X bit-exact against the
+    oracle, including duplicate columns inside a row and empty rows."""
+    rng = np.random.default_rng(n + d + B)
+    rp, c, v = _csr_with_dups(rng, n, d, mean_len)
+    c, v = c.astype(idx), v.astype(val)
+    seed = 5 + d
+    ctx = cg.context()
+    ctx.set_option("csr_mode", mode)
+    try:
+        t = cg.countgauss_new(8, B, n, cg.SeededRng(seed))
+        x = cg.SparseMatrix(n, d, rp, c, v)
+        sx = cg.countsketch_apply(t, x)
+        z = cg.countgauss_apply(t, x)
+        # explicit map with the same hash/sign: the partition's per-row keys come from perm
+        mp = cg.CountSketchMap.from_arrays(B, t.cs.hash, t.cs.sign)
+        sx_explicit = cg.countsketch_apply(mp, x)
+    finally:
+        ctx.set_option("csr_mode", 0)
+    z_ref, sx_ref = restatement.countgauss(seed, 8, B, csr=(rp, c, v, d))
+    assert np.array_equal(sx, sx_ref)
+    assert np.array_equal(sx_explicit, sx_ref)
+    assert rel_fro(z, z_ref) <= Z_TOL
+
+
 def test_csr_long_rows(cg, restatement):
     # heavy-tailed rows (config 5 shape): rows up to 2000 nnz
     rng = np.random.default_rng(3)
