@@ -12,7 +12,7 @@
 // The sort is a stable LSD radix sort over the bucket bits (8 bits per pass).  Its
 // first pass computes (bucket, sign) straight from the SplitMix64 index map
 // (bucket = draw 2i mod B, sign = parity of draw 2i+1), so no hash array is ever
-// stored.  Stability comes from a per-tile rank built with __match_any_sync and
+// stored.  Stability comes from a per-tile rank built with warp lane matching and
 // per-warp digit counters, processed in index order.
 #include "common.cuh"
 #include "internal.h"
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads) radix_scatter(KeySrc src, int64_t n,
         uint32_t key = 0, val = 0;
         if (valid) load_item<MODE>(src, idx, key, val);
         const uint32_t digit = valid ? ((key >> shift) & 255u) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        const unsigned peers = match_any_bits(digit, 9);  // digit <= 256
         const unsigned rank = __popc(peers & lt_mask);
         if (valid && rank == 0) s_wcnt[warp][digit] = __popc(peers);
         __syncthreads();

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
                                                          const uint32_t* __restrict__ perm,
                                                          const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
                                                          double* __restrict__ sx, double* __restrict__ gpart,
-                                                         int64_t chunk_rows, int use_smem) {
+                                                         int64_t chunk_rows, int use_smem, int cbits) {
     extern __shared__ double smem[];
     __shared__ int s_incl[8][32];
     __shared__ int64_t s_beg[8][32];
@@ -143,9 +143,13 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
                             if (mine) todo = false;
                         }
                     } else {
-                        const unsigned peers = __match_any_sync(0xffffffffu, col);
+                        // same-column lanes: ballot matching for narrow column ranges
+                        // (MATCH.ANY is slow on 32 mostly-distinct values)
+                        const unsigned peers =
+                            cbits <= 12 ? match_any_bits(valid ? (uint32_t)col : 1u << (cbits - 1), cbits)
+                                        : __match_any_sync(0xffffffffu, col);
                         const unsigned rank = __popc(peers & lt_mask);
-                        const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
+                        const unsigned maxr = __reduce_max_sync(0xffffffffu, valid ? rank : 0u);
                         for (unsigned r = 0; r <= maxr; ++r) {
                             if (valid && rank == r) acc[col] += val;
                             __syncwarp();
@@ -188,8 +192,10 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
     int64_t blocks = (xf->B + warps - 1) / warps;
     const int64_t cap = (int64_t)ctx->num_sms * 32;
     if (blocks > cap) blocks = cap;
+    int cbits = 1;  // bits of a column index plus one sentinel value
+    while (((int64_t)1 << (cbits - 1)) < d) ++cbits;
     kern<<<(unsigned)blocks, warps * 32, smem, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, gpart,
-                                                   chunk_rows, use_smem);
+                                                   chunk_rows, use_smem, cbits);
     count_launch(ctx);
     check_launch("sketch_csr");
 }
