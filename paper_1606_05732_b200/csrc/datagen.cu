@@ -36,14 +36,16 @@ __global__ void gen_dense_kernel(uint64_t seed, int64_t row0, int64_t n, int64_t
 
 // Inclusion rule of entry (row, j).  Bernoulli: probability `density`.  Zipf (config 5):
 // the row draws a target length L from Zipf(s_len) on [1, cap] (inverse CDF table), and
-// column j is kept with probability min(1, L * w_j), w_j ~ (j+1)^-s_col normalized -- so
-// rows are heavy-tailed in length and columns skewed toward small indices, with sorted
-// distinct columns by construction.
+// column j is kept with probability min(1, c_L * w_j), w_j ~ (j+1)^-s_col normalized and
+// c_L solved on the host so that sum_j min(1, c_L * w_j) = L: a row's expected length is
+// exactly L (mean nnz/row = E[L], 17.36 at s_len = 1.5, cap 512), rows are heavy-tailed,
+// columns skewed toward small indices, sorted and distinct by construction.
 struct CsrRule {
     double density;          // Bernoulli mode when len_cdf == nullptr
     const double* len_cdf;   // cap entries, CDF of the target length
     int cap;
     const double* colw;      // d entries, normalized column weights
+    const double* scale;     // cap entries: c_L for L = 1..cap
     uint64_t lseed;
 };
 
@@ -55,13 +57,13 @@ __device__ __forceinline__ double row_scale(const CsrRule& rule, int64_t row) {
         const int mid = (lo + hi) >> 1;
         if (rule.len_cdf[mid] >= u) hi = mid; else lo = mid + 1;
     }
-    return (double)(lo + 1);
+    return rule.scale[lo];
 }
 
 __device__ __forceinline__ bool included(const CsrRule& rule, double L, uint64_t mseed, int64_t row, int64_t d,
                                          int64_t j) {
     const double u = uniform53(rng_draw(mseed, (uint64_t)(row * d + j)));
-    const double p = rule.len_cdf ? fmin(1.0, L * rule.colw[j]) : rule.density;
+    const double p = rule.len_cdf ? fmin(1.0, L * rule.colw[j]) : rule.density;  // L: the row's c_L
     return u < p;
 }
 
@@ -113,9 +115,9 @@ void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int6
 namespace {
 // Device copies of the Zipf tables (identical on every call for the same spec).
 CsrRule make_rule(cgx_ctx* ctx, uint64_t seed, int64_t d, const CsrGenSpec& spec, cudaStream_t s) {
-    CsrRule r{spec.density, nullptr, 0, nullptr, mix64(seed, 4)};
+    CsrRule r{spec.density, nullptr, 0, nullptr, nullptr, mix64(seed, 4)};
     if (!spec.zipf) return r;
-    std::vector<double> tab((size_t)(spec.cap + d));
+    std::vector<double> tab((size_t)(2 * spec.cap + d));
     double acc = 0.0;
     for (int k = 1; k <= spec.cap; ++k) acc += std::pow((double)k, -spec.s_len);
     double run = 0.0;
@@ -127,12 +129,35 @@ CsrRule make_rule(cgx_ctx* ctx, uint64_t seed, int64_t d, const CsrGenSpec& spec
     double wsum = 0.0;
     for (int64_t j = 0; j < d; ++j) wsum += std::pow((double)(j + 1), -spec.s_col);
     for (int64_t j = 0; j < d; ++j) tab[(size_t)(spec.cap + j)] = std::pow((double)(j + 1), -spec.s_col) / wsum;
+    // c_L: bisection on the monotone f(c) = sum_j min(1, c w_j) (f(c) -> d; L >= d keeps all)
+    const double* w = tab.data() + spec.cap;
+    for (int L = 1; L <= spec.cap; ++L) {
+        double c;
+        if (L >= d) {
+            c = 1e300;
+        } else {
+            double lo = 0.0, hi = 1.0;
+            auto f = [&](double cc) {
+                double t = 0.0;
+                for (int64_t j = 0; j < d; ++j) t += std::min(1.0, cc * w[j]);
+                return t;
+            };
+            while (f(hi) < L) hi *= 2.0;
+            for (int it = 0; it < 100; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                (f(mid) < L ? lo : hi) = mid;
+            }
+            c = hi;
+        }
+        tab[(size_t)(spec.cap + d + L - 1)] = c;
+    }
     double* dev = (double*)ctx->gen_tables.get(sizeof(double) * tab.size());
     CGX_CUDA(cudaMemcpyAsync(dev, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice, s));
     CGX_CUDA(cudaStreamSynchronize(s));  // tab is a host temporary
     r.len_cdf = dev;
     r.cap = spec.cap;
     r.colw = dev + spec.cap;
+    r.scale = dev + spec.cap + d;
     return r;
 }
 } // namespace

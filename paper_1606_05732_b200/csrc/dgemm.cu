@@ -34,6 +34,11 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
     const int sz = pred ? 8 : 0;  // src-size 0 zero-fills
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(pred ? gmem : nullptr), "r"(sz));
 }
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool pred) {
+    const unsigned dst = smem_addr(smem);
+    const int sz = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(pred ? gmem : nullptr), "r"(sz));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -42,7 +47,8 @@ __device__ __forceinline__ void cp_wait() {
 
 // C[split] (+)= A . Bm over k in [split*kps, min(K, (split+1)*kps)).
 // A: m x K column-major (element (r,k) at k*m + r); Bm: K x d row-major; C: col-major d x m.
-template <int WGM, int WGN>  // warp grid (WGM x WGN = 8); CTA tile = 32*WGM x 32*WGN
+// V2: m, d even and A, Bm 16 B aligned -> tiles move as 16 B cp.async pairs.
+template <int WGM, int WGN, bool V2>  // warp grid (WGM x WGN = 8); CTA tile = 32*WGM x 32*WGN
 __global__ void __launch_bounds__(256, 2) gemm_dmma(const double* __restrict__ A, int64_t m,
                                                     const double* __restrict__ Bm, int64_t d, int64_t K,
                                                     int64_t kps, double* __restrict__ C, int accumulate) {
@@ -62,17 +68,28 @@ __global__ void __launch_bounds__(256, 2) gemm_dmma(const double* __restrict__ A
         const int64_t k0 = kb + (int64_t)t * BK;
         double* as = As + stage * BK * LDA;
         double* bs = Bs + stage * BK * LDB;
-        for (int e = tid; e < BK * BM; e += 256) {
-            const int kk = e / BM, r = e - kk * BM;
-            const int64_t gk = k0 + kk, gr = m0 + r;
-            const bool ok = gk < ke && gr < m;
-            cp_async8(as + kk * LDA + r, A + gk * m + gr, ok);
-        }
-        for (int e = tid; e < BK * BN; e += 256) {
-            const int kk = e / BN, c = e - kk * BN;
-            const int64_t gk = k0 + kk, gc = n0 + c;
-            const bool ok = gk < ke && gc < d;
-            cp_async8(bs + kk * LDB + c, Bm + gk * d + gc, ok);
+        if constexpr (V2) {
+            for (int e = tid; e < BK * BM / 2; e += 256) {
+                const int kk = e / (BM / 2), r = 2 * (e - kk * (BM / 2));
+                const int64_t gk = k0 + kk, gr = m0 + r;
+                cp_async16(as + kk * LDA + r, A + gk * m + gr, gk < ke && gr < m);
+            }
+            for (int e = tid; e < BK * BN / 2; e += 256) {
+                const int kk = e / (BN / 2), c = 2 * (e - kk * (BN / 2));
+                const int64_t gk = k0 + kk, gc = n0 + c;
+                cp_async16(bs + kk * LDB + c, Bm + gk * d + gc, gk < ke && gc < d);
+            }
+        } else {
+            for (int e = tid; e < BK * BM; e += 256) {
+                const int kk = e / BM, r = e - kk * BM;
+                const int64_t gk = k0 + kk, gr = m0 + r;
+                cp_async8(as + kk * LDA + r, A + gk * m + gr, gk < ke && gr < m);
+            }
+            for (int e = tid; e < BK * BN; e += 256) {
+                const int kk = e / BN, c = e - kk * BN;
+                const int64_t gk = k0 + kk, gc = n0 + c;
+                cp_async8(bs + kk * LDB + c, Bm + gk * d + gc, gk < ke && gc < d);
+            }
         }
     };
 
@@ -141,7 +158,9 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
                 cudaStream_t s, const double* gready = nullptr) {
     constexpr int BM = 32 * WGM, BN = 32 * WGN;
     const int64_t m = xf->m, K = b1 - b0;
-    // super-chunk of S bucket-columns: m x S fp64 <= 48 MB (L2-resident), multiple of BK
+    // super-chunk of S bucket-columns: m x S fp64 <= 48 MB (L2-resident), multiple of BK.
+    // (Sizing it so the chunk's S.X rows fit L2 too measured slower: every chunk costs each
+    // split-K CTA a read-modify-write of its partial tile.)
     int64_t S = (48ll << 20) / (8 * m);
     S = S < BK ? BK : S / BK * BK;
     if (S > K) S = (K + BK - 1) / BK * BK;
@@ -154,7 +173,9 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     // own buffer: xstage may hold the (transposed) X this GEMM is about to read
     double* gbuf = gready ? nullptr : (double*)ctx->gchunk.get(sizeof(double) * (size_t)(m * S));
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
-    auto kern = gemm_dmma<WGM, WGN>;
+    const bool v2 = m % 2 == 0 && d % 2 == 0 && ((uintptr_t)sx % 16) == 0 &&
+                    (gready ? (uintptr_t)gready % 16 == 0 : !xf->g_explicit || (uintptr_t)xf->g_dev % 16 == 0);
+    auto kern = v2 ? gemm_dmma<WGM, WGN, true> : gemm_dmma<WGM, WGN, false>;
     const size_t smem = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
     CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool first = true;
