@@ -365,6 +365,10 @@ def run_ours(args):
                 "input_dtype": c.get("dtype", "f32"), "accumulate": "f64 (S.X and G.(S.X))",
                 "l2": f"inputs larger than L2 ({x_bytes / 1e9:.2f} GB X per rank), no flush",
                 "construct_ms": construct_ms,
+                "G": ("materialized once per transform (countgauss_new, like the reference's t.g), read by apply"
+                      if c["m"] * c["B"] * 8 <= (4 << 30) and not any(o.startswith("g_resident=0") for o in args.opt)
+                      else "generated inside the apply kernels"),
+                "options": args.opt,
                 "stage_ms": {"sketch": sk_avg_ms, "gemm_fused_G": gm_ms / max(gm_n, 1)},
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -167,6 +167,28 @@ cgx_xform* new_xform(cgx_ctx* ctx, int64_t B, int64_t n) {
     return xf;
 }
 
+void drop_g(cgx_xform* xf) {
+    if (!xf->g_dev) return;
+    if (xf->g_pool)
+        pool_free(xf->ctx, xf->g_dev);
+    else
+        cudaFree(xf->g_dev);
+    xf->g_dev = nullptr;
+    xf->g_pool = false;
+}
+
+// Seeded G, materialized once per transform the way the reference's countgauss_new fills
+// CountGaussTransform::g (sketch.cpp:115-130): every apply then reads G (m*B*8 bytes)
+// instead of regenerating ~170 FP64 instructions per entry.  Skipped above 4 GiB or
+// when option g_resident = 0 (the apply kernels then generate G where they use it).
+void make_g_resident(cgx_ctx* ctx, cgx_xform* xf, cudaStream_t s) {
+    const int64_t bytes = (int64_t)sizeof(double) * xf->m * xf->B;
+    if (!ctx->opt_g_resident || xf->g_explicit || bytes > ((int64_t)4 << 30)) return;
+    xf->g_dev = (double*)pool_alloc(ctx, (size_t)bytes);
+    xf->g_pool = true;
+    launch_gen_gauss(ctx, xf, 0, xf->B, xf->g_dev, s);
+}
+
 // Caller holds ctx->mu.  The device is drained first: kernels of this (or a failed)
 // call may still read xf's arrays, and pooled blocks are reused immediately.
 void free_xform(cgx_xform* xf) {
@@ -175,7 +197,7 @@ void free_xform(cgx_xform* xf) {
     cudaDeviceSynchronize();
     pool_free(xf->ctx, xf->perm);
     pool_free(xf->ctx, xf->offsets);
-    if (xf->g_dev) cudaFree(xf->g_dev);
+    drop_g(xf);
     delete xf;
 }
 
@@ -550,6 +572,7 @@ int cgx_countgauss_new_shard(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t b
             xf->m = m;
             xf->has_g = true;
             build_perm_seeded(ctx, xf, sc.st);  // stream-ordered: no host wait
+            make_g_resident(ctx, xf, sc.st);
         } catch (...) {
             free_xform(xf);
             throw;
@@ -563,15 +586,13 @@ int cgx_xform_set_gaussian_seeded(cgx_ctx* ctx, cgx_xform* xf, int64_t m, uint64
         need_ctx(ctx);
         need_xf(xf);
         if (m < 1) fail(CGX_EINVAL, "gaussian_matrix: dimensions must be positive");
-        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
-        if (xf->g_dev) {
-            cudaFree(xf->g_dev);
-            xf->g_dev = nullptr;
-        }
+        CallScope sc(ctx, nullptr);
+        drop_g(xf);
         xf->m = m;
         xf->g_seed = g_seed;
         xf->has_g = true;
         xf->g_explicit = false;
+        make_g_resident(ctx, xf, sc.st);
     });
 }
 
@@ -588,7 +609,7 @@ int cgx_xform_set_gaussian_explicit(cgx_ctx* ctx, cgx_xform* xf, int64_t m, cons
         CGX_CUDA(cudaMemcpyAsync(gd, g, bytes, mem == CGX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                                  sc.st));
         sc.sync();
-        if (xf->g_dev) cudaFree(xf->g_dev);
+        drop_g(xf);
         xf->g_dev = gd;
         xf->m = m;
         xf->has_g = true;
@@ -726,7 +747,7 @@ int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x,
         // FP64-bound generator and the HBM-bound gather share the SMs -- then one small
         // DMMA GEMM contracts the two.  The join is an event: no kernel waits on another.
         const bool wide = d >= 17 && (dtype == CGX_F32 ? d % 4 == 0 || d <= 64 : d <= 64 || d % 2 == 0);
-        if (!ctx->no_fuse && ctx->fuse_mode == 3 && !xf->g_explicit && wide &&
+        if (!ctx->no_fuse && ctx->fuse_mode == 3 && !xf->g_dev && wide &&
             xf->m * xf->B * 8 <= (int64_t(64) << 20)) {
             const size_t zb = sizeof(double) * (size_t)(xf->m * d);
             double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
@@ -961,6 +982,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_async = value;
         else if (k == "csr_mode" && value >= 0 && value <= 2)
             ctx->opt_csr_mode = value;
+        else if (k == "g_resident" && (value == 0 || value == 1))
+            ctx->opt_g_resident = value;
         else
             fail(CGX_EINVAL, "cgx_set_option: unknown key '" + k + "'");
     });

@@ -174,7 +174,7 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     double* gbuf = gready ? nullptr : (double*)ctx->gchunk.get(sizeof(double) * (size_t)(m * S));
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
     const bool v2 = m % 2 == 0 && d % 2 == 0 && ((uintptr_t)sx % 16) == 0 &&
-                    (gready ? (uintptr_t)gready % 16 == 0 : !xf->g_explicit || (uintptr_t)xf->g_dev % 16 == 0);
+                    (gready ? (uintptr_t)gready % 16 == 0 : !xf->g_dev || (uintptr_t)xf->g_dev % 16 == 0);
     auto kern = v2 ? gemm_dmma<WGM, WGN, true> : gemm_dmma<WGM, WGN, false>;
     const size_t smem = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
     CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -184,8 +184,8 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
         const double* Ach;
         if (gready) {
             Ach = gready + c0 * m;
-        } else if (xf->g_explicit) {
-            Ach = xf->g_dev + (b0 + c0) * m;  // explicit G is already m x B column-major
+        } else if (xf->g_dev) {
+            Ach = xf->g_dev + (b0 + c0) * m;  // G in memory is already m x B column-major
         } else {
             int64_t blocks = (m * cols + 255) / 256;
             if (blocks > ctx->num_sms * 32) blocks = ctx->num_sms * 32;

@@ -235,7 +235,7 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
         const int64_t splits = (B + k_per_split - 1) / k_per_split;
         const size_t smem = sizeof(double) * (size_t)(WM * (KW + 1) + KW * (dp + 1));
         double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
-        const double* gex = xf->g_explicit ? xf->g_dev : nullptr;
+        const double* gex = xf->g_dev;
         const dim3 grid((unsigned)tm, (unsigned)splits);
 #define CGX_WIDE(WM_, KW_)                                                                                       \
     do {                                                                                                         \
@@ -264,7 +264,7 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
     const int64_t splits = (B + k_per_split - 1) / k_per_split;
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
     gauss_gemm_kernel<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)splits), 256, 0, s>>>(
-        sx, B, d, m, xf->g_seed, xf->g_explicit ? xf->g_dev : nullptr, b0, k_per_split, zpart);
+        sx, B, d, m, xf->g_seed, xf->g_dev, b0, k_per_split, zpart);
     count_launch(ctx);
     check_launch("gauss_gemm");
     launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
@@ -279,7 +279,7 @@ void launch_reduce_splits(cgx_ctx* ctx, const double* zpart, int64_t splits, int
 
 void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStream_t s) {
     const int64_t total = xf->m * xf->B;
-    if (xf->g_explicit) {
+    if (xf->g_dev) {
         CGX_CUDA(cudaMemcpyAsync(g, xf->g_dev, sizeof(double) * (size_t)total, cudaMemcpyDeviceToDevice, s));
         return;
     }

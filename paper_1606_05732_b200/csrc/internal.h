@@ -74,6 +74,7 @@ struct cgx_ctx {
     int64_t opt_ws_gw = 0;                  // option "ws_gw": buckets per sketch warp per tile (0 = auto)
     int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)
     int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 2 stable partition
+    int64_t opt_g_resident = 1;             // option "g_resident": materialize seeded G at construction (<= 4 GiB)
     cgx::DevBuf part[6];                    // csr_partition.cu scratch: counters, payload copies, row keys
 };
 
@@ -85,7 +86,8 @@ struct cgx_xform {
     bool seeded_map = true;        // hash/sign are the index functions of map_seed
     bool has_g = false;
     bool g_explicit = false;
-    double* g_dev = nullptr;       // explicit G only (m x B col-major)
+    double* g_dev = nullptr;       // G in memory (m x B col-major): explicit, or resident seeded G
+    bool g_pool = false;           // g_dev is a resident copy from the pool (else cudaMalloc'd explicit G)
     uint32_t* perm = nullptr;      // n entries: row | neg<<31, sorted by (bucket, row)
     uint32_t* offsets = nullptr;   // B+1 bucket boundaries into perm
 };

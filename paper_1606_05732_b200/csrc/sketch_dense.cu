@@ -849,7 +849,7 @@ void launch_ws2(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64
     const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(grid * m * d));
     kern<<<(unsigned)grid, 256, smem, s>>>(x, ld, d, xf->perm, xf->offsets, B, m, xf->g_seed,
-                                           xf->g_explicit ? xf->g_dev : nullptr, (int)Gw, zpart);
+                                           xf->g_dev, (int)Gw, zpart);
     count_launch(ctx);
     check_launch("countgauss_dense_ws2");
     launch_reduce_splits(ctx, zpart, grid, m * d, z, s);
@@ -880,7 +880,7 @@ void launch_ws(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_
     const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(grid * m * d));
     kern<<<(unsigned)grid, 384, smem, s>>>(x, ld, d, xf->perm, xf->offsets, B, m, xf->g_seed,
-                                           xf->g_explicit ? xf->g_dev : nullptr, (int)Gw, zpart);
+                                           xf->g_dev, (int)Gw, zpart);
     count_launch(ctx);
     check_launch("countgauss_dense_ws");
     launch_reduce_splits(ctx, zpart, grid, m * d, z, s);
@@ -905,7 +905,7 @@ void launch_fused(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int
     const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(grid * m * d));
     kern<<<(unsigned)grid, 256, smem, s>>>(x, ld, d, xf->perm, xf->offsets, B, m, xf->g_seed,
-                                           xf->g_explicit ? xf->g_dev : nullptr, (int)Gw, zpart);
+                                           xf->g_dev, (int)Gw, zpart);
     count_launch(ctx);
     check_launch("countgauss_dense_fused");
     launch_reduce_splits(ctx, zpart, grid, m * d, z, s);

@@ -19,6 +19,16 @@ pytestmark = pytest.mark.gpu
 Z_TOL = 1e-12
 
 
+@pytest.fixture(params=[1, 0], ids=["G-resident", "G-generated"])
+def g_mode(request, cg):
+    """Transforms built with G materialized at construction (the default, like the
+    reference's CountGaussTransform::g) and with G generated inside the apply kernels."""
+    ctx = cg.context()
+    ctx.set_option("g_resident", request.param)
+    yield request.param
+    ctx.set_option("g_resident", 1)
+
+
 def rel_fro(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
@@ -85,7 +95,7 @@ def test_injective_map(cg, reference):
 
 # ------------------------------------------------------------------------------ G
 @pytest.mark.parametrize("m,B,seed", [(16, 2048, 12345), (64, 65536, 12345), (7, 33, 5)])
-def test_gaussian_within_tolerance(cg, restatement, m, B, seed):
+def test_gaussian_within_tolerance(cg, restatement, m, B, seed, g_mode):
     t = cg.countgauss_new(m, B, 10, cg.SeededRng(seed))
     _, _, gs = restatement.countgauss_seeds(seed)
     ref = restatement.gaussian(gs, m, B)
@@ -155,7 +165,7 @@ def test_definition_case(cg):
         cg.CountSketchMap.from_arrays(2, [0, 1, 0], [1.0, -0.5, 1.0])
 
 
-def test_dense_golden(cg, golden):
+def test_dense_golden(cg, golden, g_mode):
     n, d, B, m, seed = (int(v) for v in golden["dense_params"])
     t = cg.countgauss_new(m, B, n, cg.SeededRng(seed))
     x = golden["dense_x"]
@@ -244,7 +254,7 @@ def _random_csr(rng, n, d, density, idx, val):
                                            (1000, 600, 50, 0.2), (777, 40, 1, 0.1), (9000, 3, 2, 0.0)])
 @pytest.mark.parametrize("idx", [np.int32, np.int64])
 @pytest.mark.parametrize("val", [np.float32, np.float64])
-def test_csr_bit_exact_shapes(cg, restatement, n, d, B, density, idx, val):
+def test_csr_bit_exact_shapes(cg, restatement, n, d, B, density, idx, val, g_mode):
     rng = np.random.default_rng(n + d + B)
     rp, c, v = _random_csr(rng, n, d, density, idx, val)
     seed = 17 + n
@@ -339,7 +349,7 @@ def test_csr_zipf_config5_shape(cg, restatement):
 
 
 @pytest.mark.parametrize("m,d,B", [(96, 300, 20011), (256, 512, 40000), (130, 70, 9000), (64, 129, 33333)])
-def test_stage2_large_z(cg, restatement, m, d, B):
+def test_stage2_large_z(cg, restatement, m, d, B, g_mode):
     """Stage 2 on its own (gemm(t.g, SX), matrix.cpp:111-129) for Z shapes that take the
     G-super-chunk + pipelined DMMA path, with G seeded (generated) and explicit."""
     import ctypes as C
@@ -449,7 +459,7 @@ def test_device_tensors_match_host(cg, restatement):
                                        (128, 32, np.float32), (100, 8, np.float32), (32, 64, np.float64),
                                        (64, 64, np.float64), (40, 100, np.float32), (33, 5, np.float64)])
 @pytest.mark.parametrize("mode", [1, 2, 3])
-def test_fused_matches_two_stage(cg, restatement, d, m, dtype, mode):
+def test_fused_matches_two_stage(cg, restatement, d, m, dtype, mode, g_mode):
     """The one-pass kernels (sketch + G + contraction; mode 1 all-warps, mode 2
     warp-specialized) and mode 3 (G generated on a side stream under the sketch, then a
     DMMA GEMM) vs the two-stage path and the oracle."""
