@@ -48,11 +48,11 @@ __device__ __forceinline__ void cp_wait() {
 // C[split] (+)= A . Bm over k in [split*kps, min(K, (split+1)*kps)).
 // A: m x K column-major (element (r,k) at k*m + r); Bm: K x d row-major; C: col-major d x m.
 // V2: m, d even and A, Bm 16 B aligned -> tiles move as 16 B cp.async pairs.
-template <int WGM, int WGN, bool V2>  // warp grid (WGM x WGN = 8); CTA tile = 32*WGM x 32*WGN
-__global__ void __launch_bounds__(256, 2) gemm_dmma(const double* __restrict__ A, int64_t m,
+template <int WGM, int WGN, bool V2>  // warp grid WGM x WGN (<= 8 warps); CTA tile = 32*WGM x 32*WGN
+__global__ void __launch_bounds__(32 * WGM * WGN, 16 / (WGM * WGN)) gemm_dmma(const double* __restrict__ A, int64_t m,
                                                     const double* __restrict__ Bm, int64_t d, int64_t K,
                                                     int64_t kps, double* __restrict__ C, int accumulate) {
-    constexpr int BM = 32 * WGM, BN = 32 * WGN;
+    constexpr int BM = 32 * WGM, BN = 32 * WGN, NT = 32 * WGM * WGN;
     constexpr int LDA = BM + 4, LDB = BN + 4;  // padding: 2-wavefront fragment loads
     extern __shared__ double dsm[];
     double* As = dsm;                          // [STAGES][BK][LDA]
@@ -69,23 +69,23 @@ __global__ void __launch_bounds__(256, 2) gemm_dmma(const double* __restrict__ A
         double* as = As + stage * BK * LDA;
         double* bs = Bs + stage * BK * LDB;
         if constexpr (V2) {
-            for (int e = tid; e < BK * BM / 2; e += 256) {
+            for (int e = tid; e < BK * BM / 2; e += NT) {
                 const int kk = e / (BM / 2), r = 2 * (e - kk * (BM / 2));
                 const int64_t gk = k0 + kk, gr = m0 + r;
                 cp_async16(as + kk * LDA + r, A + gk * m + gr, gk < ke && gr < m);
             }
-            for (int e = tid; e < BK * BN / 2; e += 256) {
+            for (int e = tid; e < BK * BN / 2; e += NT) {
                 const int kk = e / (BN / 2), c = 2 * (e - kk * (BN / 2));
                 const int64_t gk = k0 + kk, gc = n0 + c;
                 cp_async16(bs + kk * LDB + c, Bm + gk * d + gc, gk < ke && gc < d);
             }
         } else {
-            for (int e = tid; e < BK * BM; e += 256) {
+            for (int e = tid; e < BK * BM; e += NT) {
                 const int kk = e / BM, r = e - kk * BM;
                 const int64_t gk = k0 + kk, gr = m0 + r;
                 cp_async8(as + kk * LDA + r, A + gk * m + gr, gk < ke && gr < m);
             }
-            for (int e = tid; e < BK * BN; e += 256) {
+            for (int e = tid; e < BK * BN; e += NT) {
                 const int kk = e / BN, c = e - kk * BN;
                 const int64_t gk = k0 + kk, gc = n0 + c;
                 cp_async8(bs + kk * LDB + c, Bm + gk * d + gc, gk < ke && gc < d);
@@ -165,7 +165,8 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     S = S < BK ? BK : S / BK * BK;
     if (S > K) S = (K + BK - 1) / BK * BK;
     const int64_t tm = (m + BM - 1) / BM, tn = (d + BN - 1) / BN;
-    int64_t splits = (2 * (int64_t)ctx->num_sms + tm * tn - 1) / (tm * tn);
+    const int64_t resident = (int64_t)ctx->num_sms * (16 / (WGM * WGN));  // CTAs per wave
+    int64_t splits = (resident + tm * tn - 1) / (tm * tn);
     const int64_t max_splits = (S + 4 * BK - 1) / (4 * BK);  // >= 4 K-tiles per split per chunk
     splits = splits < 1 ? 1 : (splits > max_splits ? max_splits : splits);
     const int64_t kps = ((S + splits - 1) / splits + BK - 1) / BK * BK;
@@ -195,8 +196,8 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
             Ach = gbuf;
         }
         const int64_t sp = (cols + kps - 1) / kps;  // splits that have work in this chunk
-        kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), 256, smem, s>>>(Ach, m, sx + c0 * d, d, cols, kps,
-                                                                                zpart, first ? 0 : 1);
+        kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), 32 * WGM * WGN, smem, s>>>(Ach, m, sx + c0 * d, d, cols,
+                                                                                          kps, zpart, first ? 0 : 1);
         count_launch(ctx);
         check_launch("gemm_dmma");
         if (first && sp < splits)  // splits without work in the first chunk start at zero
@@ -242,6 +243,28 @@ void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t col
     gen_gauss_cols<<<(unsigned)blocks, 256, 0, s>>>(xf->g_seed, xf->m, c0, cols, out);
     count_launch(ctx);
     check_launch("gen_gauss_cols");
+}
+
+bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
+                               int64_t d, double* z, cudaStream_t s) {
+    // Z covered by one CTA tile of <= 8 warps (32 x 32 each) with G in memory: CTAs of
+    // exactly the Z tile, many split-K CTAs per SM -- the contraction is a bandwidth-bound
+    // stream of G and S.X.
+    const int64_t m = xf->m;
+    if (!xf->g_dev) return false;
+    auto p2 = [](int64_t v) { int64_t p = 1; while (p < v) p <<= 1; return p; };
+    const int64_t wm = p2((m + 31) / 32), wn = p2((d + 31) / 32);
+    if (wm * wn > 8) return false;
+    const double* g = xf->g_dev + b0 * m;
+#define CGX_SMALL(A, B_)                                                \
+    if (wm == A && wn == B_) {                                          \
+        run_chunks<A, B_>(ctx, xf, sx, b0, b1, d, z, s, g);             \
+        return true;                                                    \
+    }
+    CGX_SMALL(1, 1) CGX_SMALL(1, 2) CGX_SMALL(1, 4) CGX_SMALL(1, 8) CGX_SMALL(2, 1)
+    CGX_SMALL(2, 2) CGX_SMALL(2, 4) CGX_SMALL(4, 1) CGX_SMALL(4, 2) CGX_SMALL(8, 1)
+#undef CGX_SMALL
+    return false;
 }
 
 void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, const double* sx, int64_t d, double* z,

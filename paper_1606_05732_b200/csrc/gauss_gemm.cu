@@ -220,6 +220,7 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
         CGX_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)(m * d), s));
         return;
     }
+    if (launch_gemm_small_g_ready(ctx, xf, sx, b0, b1, d, z, s)) return;  // small Z, G in memory
     if (launch_gauss_gemm_chunked(ctx, xf, sx, b0, b1, d, z, s)) return;  // large Z (dgemm.cu)
     if (d <= 1024) {
         // wide tile: WM rows x all columns, WM * dp <= 8192 (<= 16 fragments per warp)

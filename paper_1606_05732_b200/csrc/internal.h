@@ -68,6 +68,7 @@ struct cgx_ctx {
     std::map<size_t, std::vector<void*>> pool_free;
     std::unordered_map<void*, size_t> pool_class;
     bool no_fuse = false;                  // option "fuse"=0: always run the two stages
+    bool force_fuse = false;               // option "fuse"=2: one-pass kernel even when G is in memory
     int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps fused, 2 warp-specialized
     int64_t opt_rows_per_task = 1024;       // option "rows_per_task": dense stream-kernel task size
     int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
@@ -135,6 +136,10 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
 void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStream_t s);
 // dgemm.cu: G columns [c0, c0+cols) of the transform -> out (m x cols, col-major)
 void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t cols, double* out, cudaStream_t s);
+// dgemm.cu: Z within one CTA tile (ceil(m/32) x ceil(d/32) <= 8 warps) with G in memory
+// (xf->g_dev); false when not applicable
+bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
+                               int64_t d, double* z, cudaStream_t s);
 // dgemm.cu: z = g . sx with g = all of G (m x B col-major) already in memory
 void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, const double* sx, int64_t d, double* z,
                          cudaStream_t s);

@@ -472,11 +472,13 @@ def test_fused_matches_two_stage(cg, restatement, d, m, dtype, mode, g_mode):
     ctx = cg.context()
     xd = torch.from_numpy(x).cuda()
     ctx.set_option("fuse_mode", mode)
+    ctx.set_option("fuse", 2)  # one-pass kernel even when G is resident
     try:
         z_fused = cg.countgauss_apply(t, xd).cpu().numpy()
         z_again = cg.countgauss_apply(t, xd).cpu().numpy()
     finally:
         ctx.set_option("fuse_mode", 2)
+        ctx.set_option("fuse", 1)
     ctx.set_option("fuse", 0)
     try:
         z_two = cg.countgauss_apply(t, xd).cpu().numpy()
