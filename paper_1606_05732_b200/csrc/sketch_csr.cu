@@ -170,6 +170,119 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
     }
 }
 
+// Lean form of the serial-order gather for the common case (reference serial branch,
+// accumulator in shared memory): the same bucket-ordered, row-ascending walk with far
+// fewer instructions per nonzero, since at ~0.5 us of DRAM latency per row group the
+// kernel was issue-bound (c5: 205 warp instructions per 32 nonzeros).
+//  * item -> row: the rows starting inside each 32-item wave come from one OR-reduction
+//    of start bits, and a per-group table maps (nonzero-row rank) -> lane; no search;
+//  * same-column lanes: each lane stamps its lane id into a byte tag per column; if every
+//    lane reads its own stamp back the wave's columns are distinct (the usual case) and
+//    all adds go at once, otherwise the ballot matcher orders them by lane;
+//  * the next row group's perm entries and row offsets are loaded while the current group
+//    is processed, and a group's item loads are issued kW waves at a time.
+// Adds happen in exactly the serial kernel's order, so S.X is bit-identical to it.
+template <typename TV, typename TI>
+__global__ void __launch_bounds__(256) sketch_csr_lean(const int64_t* __restrict__ rowptr, const TI* __restrict__ cols,
+                                                       const TV* __restrict__ vals, const uint32_t* __restrict__ perm,
+                                                       const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
+                                                       double* __restrict__ sx, int cbits) {
+    constexpr int kW = 4;
+    extern __shared__ double smem[];
+    __shared__ uint8_t s_tbl[8][32];
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+    const int warps_per_cta = blockDim.x >> 5;
+    double* acc = smem + (size_t)wid * d;
+    uint8_t* tag = reinterpret_cast<uint8_t*>(smem + (size_t)warps_per_cta * d) + (size_t)wid * d;
+    uint8_t* tbl = s_tbl[wid];
+
+    for (int64_t b = (int64_t)blockIdx.x * warps_per_cta + wid; b < B; b += (int64_t)gridDim.x * warps_per_cta) {
+        for (int64_t j = lane; j < d; j += 32) acc[j] = 0.0;
+        __syncwarp();
+        const uint32_t beg = offsets[b], end = offsets[b + 1];
+        // row group g = perm[base .. base+32): lane k holds row k's (sign, begin, length)
+        uint32_t npe = 0;
+        int64_t nrb = 0, nre = 0;
+        auto fetch = [&](uint32_t base) {
+            npe = 0;
+            nrb = nre = 0;
+            if (base + lane < end) {
+                npe = __ldg(perm + base + lane);
+                const int64_t row = npe & kRowMask;
+                nrb = ld_na(rowptr + row);
+                nre = ld_na(rowptr + row + 1);
+            }
+        };
+        fetch(beg);
+        for (uint32_t base = beg; base < end; base += 32) {
+            const uint32_t pe = npe;
+            const int64_t rb = nrb;
+            const int len = (int)(nre - nrb);
+            fetch(base + 32);  // next group, in flight while this one is processed
+            const int incl = warp_incl_scan(len, lane);
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            const int excl = incl - len;
+            const unsigned nz = __ballot_sync(0xffffffffu, len > 0);
+            if (len > 0) tbl[__popc(nz & lt)] = (uint8_t)lane;
+            __syncwarp();
+            int kbase = 0;  // nonzero rows started in earlier waves
+            for (int q0 = 0; q0 < total; q0 += 32 * kW) {
+                TI c[kW];
+                TV v[kW];
+                uint32_t neg[kW];
+#pragma unroll
+                for (int u = 0; u < kW; ++u) {
+                    const int w0 = q0 + u * 32;
+                    const bool starts_here = len > 0 && excl >= w0 && excl < w0 + 32;
+                    const unsigned st = __reduce_or_sync(0xffffffffu, starts_here ? 1u << (excl - w0) : 0u);
+                    const int r = kbase + __popc(st & le) - 1;
+                    kbase += __popc(st);
+                    const int j = tbl[r & 31];
+                    const int64_t rbj = __shfl_sync(0xffffffffu, rb, j);
+                    const int exj = __shfl_sync(0xffffffffu, excl, j);
+                    neg[u] = __shfl_sync(0xffffffffu, pe, j) & kNegBit;
+                    const int q = w0 + (int)lane;
+                    c[u] = 0;
+                    v[u] = TV(0);
+                    if (q < total) {
+                        const int64_t pos = rbj + (q - exj);
+                        c[u] = ld_na(cols + pos);
+                        v[u] = ld_na(vals + pos);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kW; ++u) {
+                    const int w0 = q0 + u * 32;
+                    if (w0 >= total) break;
+                    const bool ok = w0 + (int)lane < total;
+                    const uint32_t col = ok ? (uint32_t)c[u] : 0u;
+                    double x = (double)v[u];
+                    if (neg[u]) x = -x;
+                    if (ok) tag[col] = (uint8_t)lane;
+                    __syncwarp();
+                    const bool mine = !ok || tag[col] == (uint8_t)lane;
+                    if (__all_sync(0xffffffffu, mine)) {
+                        if (ok) acc[col] += x;
+                    } else {  // a column twice in the wave: lane (= row) order per column
+                        const unsigned peers = cbits <= 12 ? match_any_bits(ok ? col : 1u << (cbits - 1), cbits)
+                                                           : __match_any_sync(0xffffffffu, ok ? col : 0xffffffffu);
+                        const unsigned rank = __popc(peers & lt);
+                        for (unsigned rr = 0; __any_sync(0xffffffffu, ok && rank >= rr); ++rr) {
+                            if (ok && rank == rr) acc[col] += x;
+                            __syncwarp();
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncwarp();
+        for (int64_t j = lane; j < d; j += 32) sx[b * d + j] = acc[j];
+        __syncwarp();
+    }
+}
+
 template <typename TV, typename TI, bool CHUNKED>
 void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* cols, const TV* vals, int64_t d,
             double* sx, int64_t chunk_rows, cudaStream_t s) {
@@ -186,6 +299,25 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
         warps = 8;
         CGX_CUDA(cudaMemsetAsync(sx, 0, sizeof(double) * (size_t)(xf->B * d), s));
         if (CHUNKED) gpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(xf->B * d));
+    }
+    if (!CHUNKED && d <= 8192) {  // lean kernel: fp64 accumulator + byte tags per warp
+        const size_t per_warp_l = (sizeof(double) + 1) * (size_t)d;
+        int wl = (int)((96 * 1024) / per_warp_l);
+        wl = wl > 8 ? 8 : wl;
+        if (wl >= 1) {
+            const size_t sm = per_warp_l * wl + 8;
+            auto lk = sketch_csr_lean<TV, TI>;
+            CGX_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            int64_t nb = (xf->B + wl - 1) / wl;
+            const int64_t cap = (int64_t)ctx->num_sms * 32;
+            if (nb > cap) nb = cap;
+            int cb = 1;
+            while (((int64_t)1 << (cb - 1)) < d) ++cb;
+            lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, cb);
+            count_launch(ctx);
+            check_launch("sketch_csr_lean");
+            return;
+        }
     }
     auto kern = sketch_csr_kernel<TV, TI, CHUNKED>;
     if (smem > 40 * 1024) CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
