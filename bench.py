@@ -173,7 +173,7 @@ def run_reference_arm(args):
     line = {
         "metric": METRIC, "impl": "reference", "value": r["value"], "unit": "nnz/s", "n_gpus": args.gpus,
         "steps": len(r["ms"]), "warmup": args.warmup, "ms_per_step": r["median_ms"], "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config, c), "layout": "fp64 column-major (reference DenseMatrix)"},
         "cpu_baseline": {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "reference",
                          "sample": r["sample"]},
@@ -209,6 +209,10 @@ def run_ours(args):
         k, v = kv.split("=", 1)
         ctx.set_option(k, int(v))
     n, d, B, m = c["n"], c["d"], c["B"], c["m"]
+    if args.scaling == "weak":
+        # X grows with N: N shards of the config's n rows each (rows are independent units;
+        # the only exchange is the all-reduce of the m x d partial Z)
+        n = n * world
     r0, r1 = shard_range(n, world, rank)
     rows = r1 - r0
     t_seed = cg.SeededRng(SEED).next_u64()
@@ -360,11 +364,13 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": workload_name(args.config, c), "n": n, "d": d, "B": B, "m": m,
-                "rows_per_rank": rows, "nnz_per_rank": int(nnz_local), "mean_row_nnz": nnz_local / rows, "parallelism": f"rows sharded x{world}" + (", NCCL all-reduce of Z" if world > 1 else ""),
+                "rows_per_rank": rows, "nnz_per_rank": int(nnz_local), "mean_row_nnz": nnz_local / rows, "parallelism": f"rows sharded x{world} ({args.scaling} scaling: "
+                + ("the config's n rows per rank" if args.scaling == "weak" else "the config's n rows split across ranks")
+                + ")" + (", NCCL all-reduce of Z" if world > 1 else ""),
                 "input_dtype": c.get("dtype", "f32"), "accumulate": "f64 (S.X and G.(S.X))",
                 "l2": f"inputs larger than L2 ({x_bytes / 1e9:.2f} GB X per rank), no flush",
                 "construct_ms": construct_ms,
@@ -399,6 +405,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ablation", action="store_true", help="skip the dense-Gaussian G~.X ablation")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank sketches the config's n rows (X has N*n rows); strong: n split N ways")
     ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
                     help="cgx_set_option before timing (A/B of kernel variants)")
     args = ap.parse_args()

@@ -48,17 +48,22 @@ __device__ __forceinline__ void cp_wait() {
 // C[split] (+)= A . Bm over k in [split*kps, min(K, (split+1)*kps)).
 // A: m x K column-major (element (r,k) at k*m + r); Bm: K x d row-major; C: col-major d x m.
 // V2: m, d even and A, Bm 16 B aligned -> tiles move as 16 B cp.async pairs.
-template <int WGM, int WGN, bool V2>  // warp grid WGM x WGN (<= 8 warps); CTA tile = 32*WGM x 32*WGN
-__global__ void __launch_bounds__(32 * WGM * WGN, 16 / (WGM * WGN)) gemm_dmma(const double* __restrict__ A, int64_t m,
-                                                    const double* __restrict__ Bm, int64_t d, int64_t K,
-                                                    int64_t kps, double* __restrict__ C, int accumulate) {
-    constexpr int BM = 32 * WGM, BN = 32 * WGN, NT = 32 * WGM * WGN;
+// KG k-groups: KG sets of WGM x WGN warps share the CTA tile and split each BK slice
+// (group g takes k4-steps g, g+KG, ...); their accumulators are summed in group order at
+// the end, so a small Z tile still gets 8 warps per CTA without more split-K partials.
+template <int WGM, int WGN, int KG, bool V2>  // CTA tile = 32*WGM x 32*WGN, 32*WGM*WGN*KG threads
+__global__ void __launch_bounds__(32 * WGM * WGN * KG, (32 * WGM * WGN * KG) <= 256 ? 512 / (32 * WGM * WGN * KG) : 1)
+    gemm_dmma(const double* __restrict__ A, int64_t m, const double* __restrict__ Bm, int64_t d, int64_t K, int64_t kps,
+              double* __restrict__ C, int accumulate) {
+    constexpr int BM = 32 * WGM, BN = 32 * WGN, NT = 32 * WGM * WGN * KG;
     constexpr int LDA = BM + 4, LDB = BN + 4;  // padding: 2-wavefront fragment loads
+    static_assert(KG == 1 || KG == 2 || KG == 4, "BK = 16 has 4 k4-steps");
     extern __shared__ double dsm[];
     double* As = dsm;                          // [STAGES][BK][LDA]
     double* Bs = dsm + STAGES * BK * LDA;      // [STAGES][BK][LDB]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp % WGM, wn = warp / WGM;
+    const int wg = warp % (WGM * WGN), grp = warp / (WGM * WGN);
+    const int wm = wg % WGM, wn = wg / WGM;
     const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
     const int64_t split = blockIdx.z;
     const int64_t kb = split * kps, ke = min(K, kb + kps);
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(32 * WGM * WGN, 16 / (WGM * WGN)) gemm_dmma(co
         const double* as = As + stage * BK * LDA + wm * 32 + (lane >> 2);
         const double* bs = Bs + stage * BK * LDB + wn * 32 + (lane >> 2);
 #pragma unroll
-        for (int k4 = 0; k4 < BK; k4 += 4) {
+        for (int k4 = 4 * grp; k4 < BK; k4 += 4 * KG) {
             double a[4], b[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) a[i] = as[(k4 + (lane & 3)) * LDA + i * 8];
@@ -127,6 +132,33 @@ __global__ void __launch_bounds__(32 * WGM * WGN, 16 / (WGM * WGN)) gemm_dmma(co
         cp_commit();
     }
     cp_wait<0>();
+    if constexpr (KG > 1) {  // fold groups 1..KG-1 into group 0, in group order
+        __syncthreads();     // pipeline buffers are free now
+        constexpr int G0 = 32 * WGM * WGN;
+        if (grp > 0) {
+            double* dst = dsm + ((size_t)(grp - 1) * G0 + wg * 32 + lane) * 32;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    dst[(i * 4 + j) * 2] = acc[i][j][0];
+                    dst[(i * 4 + j) * 2 + 1] = acc[i][j][1];
+                }
+        }
+        __syncthreads();
+        if (grp > 0) return;
+#pragma unroll
+        for (int g = 1; g < KG; ++g) {
+            const double* src = dsm + ((size_t)(g - 1) * G0 + wg * 32 + lane) * 32;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[i][j][0] += src[(i * 4 + j) * 2];
+                    acc[i][j][1] += src[(i * 4 + j) * 2 + 1];
+                }
+        }
+    }
     double* cp = C + split * m * d;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -153,10 +185,10 @@ __global__ void gen_gauss_cols(uint64_t g_seed, int64_t m, int64_t c0, int64_t c
 }
 
 // gready: all of G[:, b0:b1) already materialized (m x K column-major), or nullptr.
-template <int WGM, int WGN>
+template <int WGM, int WGN, int KG = 1>
 void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d, double* z,
                 cudaStream_t s, const double* gready = nullptr) {
-    constexpr int BM = 32 * WGM, BN = 32 * WGN;
+    constexpr int BM = 32 * WGM, BN = 32 * WGN, NT = 32 * WGM * WGN * KG;
     const int64_t m = xf->m, K = b1 - b0;
     // super-chunk of S bucket-columns: m x S fp64 <= 48 MB (L2-resident), multiple of BK.
     // (Sizing it so the chunk's S.X rows fit L2 too measured slower: every chunk costs each
@@ -165,7 +197,7 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     S = S < BK ? BK : S / BK * BK;
     if (S > K) S = (K + BK - 1) / BK * BK;
     const int64_t tm = (m + BM - 1) / BM, tn = (d + BN - 1) / BN;
-    const int64_t resident = (int64_t)ctx->num_sms * (16 / (WGM * WGN));  // CTAs per wave
+    const int64_t resident = (int64_t)ctx->num_sms * (NT <= 256 ? 512 / NT : 1);  // CTAs per wave
     int64_t splits = (resident + tm * tn - 1) / (tm * tn);
     const int64_t max_splits = (S + 4 * BK - 1) / (4 * BK);  // >= 4 K-tiles per split per chunk
     splits = splits < 1 ? 1 : (splits > max_splits ? max_splits : splits);
@@ -176,8 +208,10 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
     const bool v2 = m % 2 == 0 && d % 2 == 0 && ((uintptr_t)sx % 16) == 0 &&
                     (gready ? (uintptr_t)gready % 16 == 0 : !xf->g_dev || (uintptr_t)xf->g_dev % 16 == 0);
-    auto kern = v2 ? gemm_dmma<WGM, WGN, true> : gemm_dmma<WGM, WGN, false>;
-    const size_t smem = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
+    auto kern = v2 ? gemm_dmma<WGM, WGN, KG, true> : gemm_dmma<WGM, WGN, KG, false>;
+    const size_t pipe = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
+    const size_t fold = sizeof(double) * (size_t)((KG - 1) * BM * BN);
+    const size_t smem = pipe > fold ? pipe : fold;
     CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool first = true;
     for (int64_t c0 = 0; c0 < K; c0 += S) {
@@ -196,8 +230,8 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
             Ach = gbuf;
         }
         const int64_t sp = (cols + kps - 1) / kps;  // splits that have work in this chunk
-        kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), 32 * WGM * WGN, smem, s>>>(Ach, m, sx + c0 * d, d, cols,
-                                                                                          kps, zpart, first ? 0 : 1);
+        kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), NT, smem, s>>>(Ach, m, sx + c0 * d, d, cols, kps, zpart,
+                                                                               first ? 0 : 1);
         count_launch(ctx);
         check_launch("gemm_dmma");
         if (first && sp < splits)  // splits without work in the first chunk start at zero
@@ -256,13 +290,13 @@ bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* 
     const int64_t wm = p2((m + 31) / 32), wn = p2((d + 31) / 32);
     if (wm * wn > 8) return false;
     const double* g = xf->g_dev + b0 * m;
-#define CGX_SMALL(A, B_)                                                \
+#define CGX_SMALL(A, B_, KG_)                                           \
     if (wm == A && wn == B_) {                                          \
-        run_chunks<A, B_>(ctx, xf, sx, b0, b1, d, z, s, g);             \
+        run_chunks<A, B_, KG_>(ctx, xf, sx, b0, b1, d, z, s, g);        \
         return true;                                                    \
     }
-    CGX_SMALL(1, 1) CGX_SMALL(1, 2) CGX_SMALL(1, 4) CGX_SMALL(1, 8) CGX_SMALL(2, 1)
-    CGX_SMALL(2, 2) CGX_SMALL(2, 4) CGX_SMALL(4, 1) CGX_SMALL(4, 2) CGX_SMALL(8, 1)
+    CGX_SMALL(1, 1, 4) CGX_SMALL(1, 2, 4) CGX_SMALL(1, 4, 2) CGX_SMALL(1, 8, 1) CGX_SMALL(2, 1, 4)
+    CGX_SMALL(2, 2, 2) CGX_SMALL(2, 4, 1) CGX_SMALL(4, 1, 2) CGX_SMALL(4, 2, 1) CGX_SMALL(8, 1, 1)
 #undef CGX_SMALL
     return false;
 }
