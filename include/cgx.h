@@ -141,6 +141,16 @@ int cgx_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int sx_l
 int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_rows, int64_t b0, int64_t b1,
                          int64_t d, int sx_mem, double* z, int z_mem, void* stream);
 
+/* Batched tiny sketches -- distcheck's Monte-Carlo loop (distcheck.cpp:107-113): for each
+ * trial t in [t0, t0+trials): map = countsketch_new(buckets, n, SeededRng(mix64(master, t)))
+ * (sketch.cpp:12-28), su = countsketch_apply(map, U) (sketch.cpp:52-66), gram(su)
+ * (matrix.cpp:149-165).  U: n x d fp64 column-major (leading dimension ld).  Outputs, each
+ * optional (null to skip): su, trials blocks of buckets x d column-major; gram, trials
+ * blocks of d x d column-major.  Both bit-identical to the reference.  One launch. */
+int cgx_countsketch_batch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_t trials, int64_t buckets,
+                               const double* u, int64_t ld, int64_t n, int64_t d, int u_mem, double* su,
+                               double* gram, int out_mem, void* stream);
+
 /* Dense-Gaussian baseline (SURVEY 8f, config-5 ablation): z = G~ . X with G~ the m x n
  * i.i.d. N(0,1) matrix gaussian_matrix(m, n, rng) would draw (matrix.cpp:199-207) from a
  * SeededRng whose current state is `rng_state` -- the product gp_nmf computes

@@ -213,6 +213,7 @@ class Reference:
         L.cgref_random_sparse.argtypes = [_I64, _I64, _I64, _U64, _P, _P, _P]
         L.cgref_gp_nmf.argtypes = [_P, _I64, _U64] + [_P] * 7
         L.cgref_generate_separable.argtypes = [_I64, _I64, _I64, _U64, _P]
+        L.cgref_sketch_gram_trials.argtypes = [_U64, _I64, _I64, _I64, _P, _I64, _I64, _P, _P]
 
     def _check(self, rc):
         if rc == 1:
@@ -311,6 +312,16 @@ class Reference:
                                           C.byref(cnt[3])))
         return dict(i_max=bufs[0][:cnt[0].value].copy(), i_min=bufs[1][:cnt[1].value].copy(),
                     unioned=bufs[2][:cnt[2].value].copy(), tie_rows=cnt[3].value)
+
+    def sketch_gram_trials(self, master, t0, trials, B, u):
+        """distcheck.cpp:107-113 for trials [t0, t0+trials): (su, gram), trial-major."""
+        u = np.asfortranarray(u, dtype=np.float64)
+        n, d = u.shape
+        su = np.empty((trials, d, B), np.float64)
+        gm = np.empty((trials, d, d), np.float64)
+        self._check(self.lib.cgref_sketch_gram_trials(master, t0, trials, B, _ptr(u), n, d, _ptr(su),
+                                                      _ptr(gm)))
+        return su.transpose(0, 2, 1), gm.transpose(0, 2, 1)
 
     def gp_nmf(self, xm, m, caller_seed):
         cap = max(2 * m, 1)

@@ -251,6 +251,25 @@ int cgref_apply(void* xf, void* xh, int sparse, int kind, double* out) {
     });
 }
 
+// distcheck's trial loop body (distcheck.cpp:107-113) for trials [t0, t0+trials):
+// SeededRng(mix64(master, t)) -> countsketch_new -> countsketch_apply(map, U) -> gram.
+// su (trials x B x d) and gram (trials x d x d), each column-major; either may be null.
+int cgref_sketch_gram_trials(uint64_t master, int64_t t0, int64_t trials, int64_t B, const double* u_colmajor,
+                             int64_t n, int64_t d, double* su, double* gm) {
+    return guard([&] {
+        DenseMatrix u(n, d);
+        std::memcpy(u.data(), u_colmajor, sizeof(double) * (size_t)(n * d));
+#pragma omp parallel for schedule(static)  // as the reference's trial loop
+        for (int64_t t = 0; t < trials; ++t) {
+            SeededRng trial_rng(mix64(master, static_cast<std::uint64_t>(t0 + t)));
+            CountSketchMap s = countsketch_new(B, n, trial_rng);
+            DenseMatrix r = countsketch_apply(s, u);
+            if (su) to_colmajor(r, su + t * B * d);
+            if (gm) to_colmajor(gram(r), gm + t * d * d);
+        }
+    });
+}
+
 // Times `reps` calls of cgref_apply after one warm-up, like timed_median_ms
 // (countgauss_main.cpp:96-108); writes every sample (ms).
 int cgref_time_apply(void* xf, void* xh, int sparse, int kind, int reps, double* ms_out, double* out) {

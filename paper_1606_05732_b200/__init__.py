@@ -6,13 +6,14 @@ Gaussian-fused G.(S.X) contraction, anchor selection) is hand-written sm_100a CU
 host-side mirror of the reference library's API (see :mod:`.api`).
 """
 from .api import (AnchorSet, Context, CountGaussTransform, CountSketchMap, SeededRng, SparseMatrix, cg_nmf,
-                  context, countgauss_apply, countgauss_new, countsketch_apply, countsketch_injective,
+                  context, countgauss_apply, countgauss_new, countsketch_apply, countsketch_batch_gram,
+                  countsketch_injective,
                   countsketch_new, gaussian_project, gp_nmf, inverse_normal_cdf, inverse_normal_cdf_array, mix64,
                   select_extremes)
 
 __all__ = [
     "AnchorSet", "Context", "CountGaussTransform", "CountSketchMap", "SeededRng", "SparseMatrix", "cg_nmf",
-    "context", "countgauss_apply", "countgauss_new", "countsketch_apply", "countsketch_injective",
+    "context", "countgauss_apply", "countgauss_new", "countsketch_apply", "countsketch_batch_gram", "countsketch_injective",
     "countsketch_new", "gaussian_project", "gp_nmf", "inverse_normal_cdf", "inverse_normal_cdf_array", "mix64",
     "select_extremes",
 ]

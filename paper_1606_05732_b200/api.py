@@ -546,6 +546,41 @@ def gaussian_project(x, m: int, rng: SeededRng, ctx: Optional[Context] = None):
     return out
 
 
+def countsketch_batch_gram(u, buckets: int, trials: int, master: int, t0: int = 0, want_su: bool = False,
+                           ctx: Optional[Context] = None):
+    """distcheck's trial loop in one launch (distcheck.cpp:107-113): for t in [t0, t0+trials),
+    map = countsketch_new(buckets, n, SeededRng(mix64(master, t))), su = S_t.U, gram(su).
+    u: n x d float64 (host array or CUDA tensor).  Returns gram (trials x d x d) and, with
+    want_su, su (trials x buckets x d) -- each trial's matrices in the reference layout,
+    bit-identical to the reference."""
+    import numpy as np
+
+    ctx = ctx or context()
+    if _is_torch(u) and u.is_cuda:
+        import torch
+
+        if u.dtype != torch.float64:
+            raise ValueError("countsketch_batch_gram: U must be float64")
+        ut = u.t().contiguous().t() if not (u.stride(0) == 1) else u  # column-major
+        n, d = ut.shape
+        ld = ut.stride(1) if d > 1 else n
+        gram = torch.empty((trials, d, d), dtype=torch.float64, device=u.device)
+        su = torch.empty((trials, d, buckets), dtype=torch.float64, device=u.device) if want_su else None
+        check(lib.cgx_countsketch_batch_gram(ctx.h, master, t0, trials, buckets, ut.data_ptr(), ld, n, d, CGX_MEM_DEVICE,
+                                             su.data_ptr() if want_su else None, gram.data_ptr(), CGX_MEM_DEVICE,
+                                             _stream_of(ut)))
+        gram = gram.transpose(1, 2)
+        return (gram, su.transpose(1, 2)) if want_su else gram
+    ua = np.asfortranarray(np.asarray(u, dtype=np.float64))
+    n, d = ua.shape
+    gram = np.empty((trials, d, d), dtype=np.float64)
+    su = np.empty((trials, d, buckets), dtype=np.float64) if want_su else None
+    check(lib.cgx_countsketch_batch_gram(ctx.h, master, t0, trials, buckets, ua.ctypes.data, n, n, d, CGX_MEM_HOST,
+                                         su.ctypes.data if want_su else None, gram.ctypes.data, CGX_MEM_HOST, None))
+    gram = gram.transpose(0, 2, 1)
+    return (gram, su.transpose(0, 2, 1)) if want_su else gram
+
+
 def gp_nmf(x, m: int, rng: SeededRng, ctx: Optional[Context] = None) -> AnchorSet:
     """Gaussian-projection anchor extraction (nmf.cpp:155-159): extremes of G~.X."""
     n, d = x.shape

@@ -923,6 +923,39 @@ int cgx_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d, int
     });
 }
 
+int cgx_countsketch_batch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_t trials, int64_t buckets,
+                               const double* u, int64_t ld, int64_t n, int64_t d, int u_mem, double* su,
+                               double* gram, int out_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_mem(u_mem);
+        need_mem(out_mem);
+        if (buckets < 1 || n < 1) fail(CGX_EINVAL, "countsketch_new: buckets and input_dim must be >= 1");
+        if (trials < 0 || d < 1 || t0 < 0) fail(CGX_EINVAL, "cgx_countsketch_batch_gram: need trials >= 0, d >= 1");
+        if (ld < n) fail(CGX_EINVAL, "cgx_countsketch_batch_gram: ld < n");
+        if (trials == 0) return;
+        CallScope sc(ctx, stream);
+        const double* ud = (const double*)to_device(ctx, ctx->hstage_dev, u, sizeof(double) * (size_t)(ld * d), u_mem,
+                                                    sc.st);
+        const size_t su_b = sizeof(double) * (size_t)(trials * buckets * d), g_b = sizeof(double) * (size_t)(trials * d * d);
+        double* sud = su;
+        double* gd = gram;
+        if (out_mem == CGX_MEM_HOST) {
+            char* base = (char*)ctx->tmp.get((su ? su_b : 0) + (gram ? g_b : 0));
+            sud = su ? (double*)base : nullptr;
+            gd = gram ? (double*)(base + (su ? su_b : 0)) : nullptr;
+        }
+        launch_batch_sketch_gram(ctx, master, t0, trials, buckets, ud, ld, n, d, sud, gd, sc.st);
+        if (out_mem == CGX_MEM_HOST) {
+            if (su) CGX_CUDA(cudaMemcpyAsync(su, sud, su_b, cudaMemcpyDeviceToHost, sc.st));
+            if (gram) CGX_CUDA(cudaMemcpyAsync(gram, gd, g_b, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        } else if (u_mem == CGX_MEM_HOST) {
+            sc.sync();  // the staged U must outlive the kernel
+        }
+    });
+}
+
 int cgx_gen_dense_normal(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype, int layout,
                          void* x_dev, void* stream) {
     return guard([&] {

@@ -169,6 +169,10 @@ void launch_gen_csr_counts(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, co
 void launch_gen_csr_fill(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, const CsrGenSpec& spec,
                          const int64_t* rowptr, int32_t* cols, float* vals, cudaStream_t s);
 
+// batch.cu: distcheck's trial loop -- su = S_t.U and gram(su) for trials [t0, t0+trials)
+void launch_batch_sketch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_t trials, int64_t B, const double* u,
+                              int64_t ld, int64_t n, int64_t d, double* su_out, double* gram_out, cudaStream_t s);
+
 // scan.cu: exclusive scans (in place allowed), total written to out[count] when requested
 void exclusive_scan_u32(cgx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t count, cudaStream_t s);
 void exclusive_scan_i64(cgx_ctx* ctx, const int64_t* in, int64_t* out, int64_t count, cudaStream_t s);

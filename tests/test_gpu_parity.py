@@ -553,3 +553,26 @@ def test_config2_full_size_bit_exact(cg, restatement):
     z_ref, sx_ref = restatement.countgauss(12345, m, B, x=xh)
     assert np.array_equal(sx, sx_ref)
     assert rel_fro(z, z_ref) <= Z_TOL
+
+
+# ------------------------------------------------------------- batched tiny sketches
+@pytest.mark.parametrize("n,d,B,trials,t0", [(200, 5, 40, 64, 0), (1000, 20, 7, 33, 5), (77, 1, 1, 9, 0),
+                                              (3000, 33, 300, 12, 100), (64, 3, 1000, 40, 7)])
+def test_batch_sketch_gram_bit_exact(cg, reference, n, d, B, trials, t0):
+    """distcheck's trial loop (distcheck.cpp:107-113) in one launch: every trial's S.U and
+    gram(S.U) bit-identical to the reference's countsketch_new/countsketch_apply/gram,
+    including the global-memory path (B*d > 1536) and a t0 offset."""
+    import torch
+
+    rng = np.random.default_rng(n + d + B)
+    u = np.linalg.qr(rng.standard_normal((n, d)))[0] if n >= d else rng.standard_normal((n, d))
+    master = 0xC0FFEE + n
+    su_ref, g_ref = reference.sketch_gram_trials(master, t0, trials, B, u)
+    g, su = cg.countsketch_batch_gram(u, B, trials, master, t0=t0, want_su=True)
+    assert np.array_equal(su, su_ref)
+    assert np.array_equal(g, g_ref)
+    gd = cg.countsketch_batch_gram(torch.from_numpy(np.asfortranarray(u)).cuda(), B, trials, master, t0=t0)
+    assert np.array_equal(gd.cpu().numpy(), g_ref)
+    # chunking the trial range gives the same trials (seeds are mix64(master, t))
+    g2 = cg.countsketch_batch_gram(u, B, trials - trials // 2, master, t0=t0 + trials // 2)
+    assert np.array_equal(g2, g_ref[trials // 2:])
