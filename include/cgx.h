@@ -141,6 +141,15 @@ int cgx_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int sx_l
 int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_rows, int64_t b0, int64_t b1,
                          int64_t d, int sx_mem, double* z, int z_mem, void* stream);
 
+/* Dense-Gaussian baseline for CSR X (the config-5 ablation): z = G~ . X with
+ * G~ = gaussian_matrix(m, n, rng) at the rng state `rng_state` -- the reference bench's
+ * naive O(nnz * m) loop (tools/countgauss_main.cpp:535-547, acceptance.cpp:365-377).
+ * G~ is generated where it is used and never stored.  Z matches to rounding (fp64
+ * atomics), not bitwise; the caller's rng advances by m*n draws. */
+int cgx_gaussian_project_csr(cgx_ctx* ctx, uint64_t rng_state, int64_t m, const int64_t* rowptr, const void* cols,
+                             int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem,
+                             double* z, int z_mem, void* stream);
+
 /* Batched tiny sketches -- distcheck's Monte-Carlo loop (distcheck.cpp:107-113): for each
  * trial t in [t0, t0+trials): map = countsketch_new(buckets, n, SeededRng(mix64(master, t)))
  * (sketch.cpp:12-28), su = countsketch_apply(map, U) (sketch.cpp:52-66), gram(su)

@@ -532,10 +532,18 @@ def select_extremes(z, ctx: Optional[Context] = None) -> AnchorSet:
 def gaussian_project(x, m: int, rng: SeededRng, ctx: Optional[Context] = None):
     """Dense-Gaussian baseline Z = G~.X with G~ = gaussian_matrix(m, n, rng) (matrix.cpp:199-207,
     the product gp_nmf forms, nmf.cpp:155-159).  G~ is generated on the GPU in L2-sized
-    chunks (never stored whole); rng advances by m*n draws exactly as in the reference."""
+    chunks (never stored whole); rng advances by m*n draws exactly as in the reference.
+    A SparseMatrix X takes the CSR kernel (the bench's naive loop; Z to rounding)."""
     if m < 1:
         raise ValueError("anchor extraction: m must be >= 1")
     ctx = ctx or context()
+    if isinstance(x, SparseMatrix):  # the reference bench's O(nnz*m) loop (countgauss_main.cpp:535-547)
+        rp, ci, it, v, dt, mem, keep, dev = _csr_args(x)
+        out, optr = _out(m, x.cols, dev, x.values)
+        check(lib.cgx_gaussian_project_csr(ctx.h, rng._state, int(m), rp, ci, it, v, dt, x.rows, x.cols, x.nnz(), mem,
+                                           optr, mem, _stream_of(x.values) if dev else None))
+        rng._state = (rng._state + m * x.rows * GAMMA) & _MASK
+        return out
     ptr, dt, layout, ld, n, d, mem, keep, dev = _dense_args(x)
     if d < 1:
         raise ValueError("anchor extraction: X must have at least one column")

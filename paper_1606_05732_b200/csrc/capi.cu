@@ -260,6 +260,23 @@ void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtyp
     ctx->prof.end(0, s);
 }
 
+// Host CSR inputs -> one device staging allocation with three regions (device inputs pass).
+void stage_csr(cgx_ctx* ctx, const void** rp, const void** cp, int idx_type, const void** vp, size_t es, int64_t n,
+               int64_t nnz, int x_mem, cudaStream_t s) {
+    if (x_mem != CGX_MEM_HOST) return;
+    const size_t is = idx_type == CGX_I32 ? 4 : 8;
+    const size_t r_b = sizeof(int64_t) * (size_t)(n + 1), c_b = is * (size_t)nnz, v_b = es * (size_t)nnz;
+    const size_t a = 256;
+    const size_t off_c = (r_b + a - 1) / a * a, off_v = off_c + (c_b + a - 1) / a * a;
+    char* base = (char*)ctx->hstage_dev.get(off_v + v_b);
+    CGX_CUDA(cudaMemcpyAsync(base, *rp, r_b, cudaMemcpyHostToDevice, s));
+    if (c_b) CGX_CUDA(cudaMemcpyAsync(base + off_c, *cp, c_b, cudaMemcpyHostToDevice, s));
+    if (v_b) CGX_CUDA(cudaMemcpyAsync(base + off_v, *vp, v_b, cudaMemcpyHostToDevice, s));
+    *rp = base;
+    *cp = base + off_c;
+    *vp = base + off_v;
+}
+
 void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
                     const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem, double* sx_dev,
                     cudaStream_t s) {
@@ -271,24 +288,10 @@ void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
     if (d < 0 || nnz < 0) fail(CGX_EINVAL, "cgx: negative size");
     if (d >= ((int64_t)1 << 26)) fail(CGX_EINVAL, "cgx: CSR column count must be < 2^26 on the GPU path");
     if (d == 0) return;
-    const size_t is = idx_type == CGX_I32 ? 4 : 8;
-    DevBuf& b0 = ctx->hstage_dev;
-    // host inputs: one staging allocation, three regions
     const void* rp = rowptr;
     const void* cp = cols;
     const void* vp = vals;
-    if (x_mem == CGX_MEM_HOST) {
-        const size_t r_b = sizeof(int64_t) * (size_t)(n + 1), c_b = is * (size_t)nnz, v_b = es * (size_t)nnz;
-        const size_t a = 256;
-        const size_t off_c = (r_b + a - 1) / a * a, off_v = off_c + (c_b + a - 1) / a * a;
-        char* base = (char*)b0.get(off_v + v_b);
-        CGX_CUDA(cudaMemcpyAsync(base, rowptr, r_b, cudaMemcpyHostToDevice, s));
-        if (c_b) CGX_CUDA(cudaMemcpyAsync(base + off_c, cols, c_b, cudaMemcpyHostToDevice, s));
-        if (v_b) CGX_CUDA(cudaMemcpyAsync(base + off_v, vals, v_b, cudaMemcpyHostToDevice, s));
-        rp = base;
-        cp = base + off_c;
-        vp = base + off_v;
-    }
+    stage_csr(ctx, &rp, &cp, idx_type, &vp, es, n, nnz, x_mem, s);
     ctx->prof.begin(0, s);
     const int64_t chunk_rows = csr_chunk_rows(n, xf->B, d);
     if (chunk_rows == 0 && csr_partition_applies(ctx, n, xf->B, d, nnz))
@@ -890,6 +893,38 @@ int cgx_gaussian_project_dense(cgx_ctx* ctx, uint64_t rng_state, int64_t m, cons
         ctx->prof.end(1, sc.st);
         if (z_mem == CGX_MEM_HOST) {
             CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        }
+    });
+}
+
+int cgx_gaussian_project_csr(cgx_ctx* ctx, uint64_t rng_state, int64_t m, const int64_t* rowptr, const void* cols,
+                             int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem,
+                             double* z, int z_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_mem(x_mem);
+        need_mem(z_mem);
+        const size_t es = dsize(dtype);
+        if (idx_type != CGX_I32 && idx_type != CGX_I64) fail(CGX_EINVAL, "cgx: idx_type must be CGX_I32 or CGX_I64");
+        if (m < 1) fail(CGX_EINVAL, "anchor extraction: m must be >= 1");
+        if (n < 1) fail(CGX_EINVAL, "gaussian_matrix: dimensions must be positive");
+        if (d < 1) fail(CGX_EINVAL, "anchor extraction: X must have at least one column");
+        if (nnz < 0) fail(CGX_EINVAL, "cgx: negative size");
+        CallScope sc(ctx, stream);
+        const void* rp = rowptr;
+        const void* cp = cols;
+        const void* vp = vals;
+        stage_csr(ctx, &rp, &cp, idx_type, &vp, es, n, nnz, x_mem, sc.st);
+        const size_t zb = sizeof(double) * (size_t)(m * d);
+        double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
+        ctx->prof.begin(1, sc.st);
+        launch_gproject_csr(ctx, rng_state, m, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, zd, sc.st);
+        ctx->prof.end(1, sc.st);
+        if (z_mem == CGX_MEM_HOST) {
+            CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        } else if (x_mem == CGX_MEM_HOST) {
             sc.sync();
         }
     });

@@ -169,6 +169,10 @@ void launch_gen_csr_counts(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, co
 void launch_gen_csr_fill(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, const CsrGenSpec& spec,
                          const int64_t* rowptr, int32_t* cols, float* vals, cudaStream_t s);
 
+// gproject.cu: dense-Gaussian baseline Z = G~.X for CSR X, G~(r, i) = draw i*m + r of g_seed
+void launch_gproject_csr(cgx_ctx* ctx, uint64_t g_seed, int64_t m, const int64_t* rowptr, const void* cols,
+                         int idx_type, const void* vals, int dtype, int64_t n, int64_t d, double* z, cudaStream_t s);
+
 // batch.cu: distcheck's trial loop -- su = S_t.U and gram(su) for trials [t0, t0+trials)
 void launch_batch_sketch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_t trials, int64_t B, const double* u,
                               int64_t ld, int64_t n, int64_t d, double* su_out, double* gram_out, cudaStream_t s);

@@ -576,3 +576,27 @@ def test_batch_sketch_gram_bit_exact(cg, reference, n, d, B, trials, t0):
     # chunking the trial range gives the same trials (seeds are mix64(master, t))
     g2 = cg.countsketch_batch_gram(u, B, trials - trials // 2, master, t0=t0 + trials // 2)
     assert np.array_equal(g2, g_ref[trials // 2:])
+
+
+@pytest.mark.parametrize("n,d,m,density,idx,val", [(3000, 40, 16, 0.05, np.int32, np.float32),
+                                                   (2000, 300, 70, 0.02, np.int64, np.float64),
+                                                   (5000, 7, 33, 0.5, np.int32, np.float64)])
+def test_gaussian_project_csr(cg, restatement, n, d, m, density, idx, val):
+    """The config-5 ablation: dense-Gaussian G~.X for CSR X, against
+    G~ = gaussian_matrix(m, n, rng) from the restatement times the densified X, and against
+    the dense-input path on the same rng state; rng advances by m*n draws."""
+    rng = np.random.default_rng(n + d + m)
+    rp, c, v = _random_csr(rng, n, d, density, idx, val)
+    x = cg.SparseMatrix(n, d, rp, c, v)
+    r1 = cg.SeededRng(99)
+    state0 = r1._state
+    z = cg.gaussian_project(x, m, r1)
+    G = restatement.gaussian(state0, m, n)
+    xd = np.zeros((n, d))
+    for i in range(n):
+        xd[i, c[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+    assert rel_fro(z, G @ xd) <= Z_TOL
+    r2 = cg.SeededRng(99)
+    zd = cg.gaussian_project(xd, m, r2)
+    assert rel_fro(z, zd) <= Z_TOL
+    assert r1._state == r2._state
