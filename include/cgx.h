@@ -141,6 +141,11 @@ int cgx_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int sx_l
 int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_rows, int64_t b0, int64_t b1,
                          int64_t d, int sx_mem, double* z, int z_mem, void* stream);
 
+/* T = G . S  (m x n, column-major): the CountGauss projection matrix that svm-check builds as
+ * gemm(t.g, reference::materialize(t.cs)) (tools/countgauss_main.cpp:660-668, svm.cpp:128-150).
+ * Column i is sign_i * G(:, hash_i), bit-identical to that gemm (which skips S's zeros). */
+int cgx_countgauss_materialize(cgx_ctx* ctx, const cgx_xform* xf, double* t, int mem, void* stream);
+
 /* Dense-Gaussian baseline for CSR X (the config-5 ablation): z = G~ . X with
  * G~ = gaussian_matrix(m, n, rng) at the rng state `rng_state` -- the reference bench's
  * naive O(nnz * m) loop (tools/countgauss_main.cpp:535-547, acceptance.cpp:365-377).

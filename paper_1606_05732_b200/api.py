@@ -226,8 +226,8 @@ class CountSketchMap:
 
 
 class CountGaussTransform:
-    """T = G.S with G m x buckets (sketch.hpp:42-47).  ``g`` is materialized on demand;
-    countgauss_apply regenerates G inside its GEMM instead."""
+    """T = G.S with G m x buckets (sketch.hpp:42-47).  G lives on the device (materialized by
+    countgauss_new, like the reference's t.g); ``g`` copies it to the host on demand."""
 
     def __init__(self, xf: _Xform):
         self._xf = xf
@@ -244,6 +244,13 @@ class CountGaussTransform:
             check(lib.cgx_fill_gaussian(self._xf.ctx.h, self._xf.h, g.ctypes.data, CGX_MEM_HOST, None))
             self._g = g.T
         return self._g
+
+    def materialize(self) -> np.ndarray:
+        """T = G.S (m x n): the projection svm-check forms as gemm(t.g, materialize(t.cs))
+        (tools/countgauss_main.cpp:660-668); column i is sign_i * G(:, hash_i)."""
+        t = np.empty((self.cs.input_dim, self.m), np.float64)  # col-major m x n
+        check(lib.cgx_countgauss_materialize(self._xf.ctx.h, self._xf.h, t.ctypes.data, CGX_MEM_HOST, None))
+        return t.T
 
 
 def countsketch_new(buckets: int, input_dim: int, rng: SeededRng, ctx: Optional[Context] = None) -> CountSketchMap:

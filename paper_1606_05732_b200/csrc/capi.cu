@@ -958,6 +958,23 @@ int cgx_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d, int
     });
 }
 
+int cgx_countgauss_materialize(cgx_ctx* ctx, const cgx_xform* xf, double* t, int mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(mem);
+        need_g(xf);
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)(xf->m * xf->n);
+        double* td = mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(bytes) : t;
+        launch_materialize_t(ctx, xf, td, sc.st);
+        if (mem == CGX_MEM_HOST) {
+            CGX_CUDA(cudaMemcpyAsync(t, td, bytes, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        }
+    });
+}
+
 int cgx_countsketch_batch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_t trials, int64_t buckets,
                                const double* u, int64_t ld, int64_t n, int64_t d, int u_mem, double* su,
                                double* gram, int out_mem, void* stream) {

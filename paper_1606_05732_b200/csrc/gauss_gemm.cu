@@ -192,6 +192,29 @@ __global__ void __launch_bounds__(256, 2) gauss_gemm_wide(const double* __restri
     }
 }
 
+// T = G . S (m x n, column-major): the projection svm-check materializes as
+// gemm(t.g, reference::materialize(t.cs)) (tools/countgauss_main.cpp:660-668).  gemm skips
+// the zero entries of S, so column i is exactly sign_i * G(:, hash_i).  Warp per bucket:
+// G(:, b) is read (or generated) once and written, sign-flipped, to each of b's columns.
+__global__ void materialize_t_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ offsets, int64_t B,
+                                     int64_t m, uint64_t g_seed, const double* __restrict__ g_dev,
+                                     double* __restrict__ t) {
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = threadIdx.x & 31;
+    if (b >= B) return;
+    const uint32_t p0 = offsets[b], p1 = offsets[b + 1];
+    if (p0 == p1) return;
+    for (int64_t r0 = 0; r0 < m; r0 += 32) {
+        const int64_t r = r0 + lane;
+        double g = 0.0;
+        if (r < m) g = g_dev ? g_dev[b * m + r] : gauss_entry(g_seed, (uint64_t)m, (uint64_t)r, (uint64_t)b);
+        for (uint32_t p = p0; p < p1; ++p) {
+            const uint32_t e = __ldg(perm + p);
+            if (r < m) t[(int64_t)(e & kRowMask) * m + r] = (e & kNegBit) ? -g : g;
+        }
+    }
+}
+
 __global__ void fill_gaussian_kernel(uint64_t g_seed, int64_t m, int64_t total, double* g) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = e / m, r = e - c * m;
@@ -269,6 +292,14 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
     count_launch(ctx);
     check_launch("gauss_gemm");
     launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
+}
+
+void launch_materialize_t(cgx_ctx* ctx, const cgx_xform* xf, double* t, cudaStream_t s) {
+    const int64_t threads = xf->B * 32;
+    materialize_t_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(xf->perm, xf->offsets, xf->B, xf->m,
+                                                                           xf->g_seed, xf->g_dev, t);
+    count_launch(ctx);
+    check_launch("materialize_t");
 }
 
 void launch_reduce_splits(cgx_ctx* ctx, const double* zpart, int64_t splits, int64_t md, double* z, cudaStream_t s) {

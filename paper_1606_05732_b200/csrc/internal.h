@@ -134,6 +134,8 @@ void launch_sketch_csr_partition(cgx_ctx* ctx, const cgx_xform* xf, const int64_
 void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d,
                        double* z, cudaStream_t s);
 void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStream_t s);
+// gauss_gemm.cu: T = G . S, m x n column-major
+void launch_materialize_t(cgx_ctx* ctx, const cgx_xform* xf, double* t, cudaStream_t s);
 // dgemm.cu: G columns [c0, c0+cols) of the transform -> out (m x cols, col-major)
 void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t cols, double* out, cudaStream_t s);
 // dgemm.cu: Z within one CTA tile (ceil(m/32) x ceil(d/32) <= 8 warps) with G in memory

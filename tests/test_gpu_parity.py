@@ -600,3 +600,16 @@ def test_gaussian_project_csr(cg, restatement, n, d, m, density, idx, val):
     zd = cg.gaussian_project(xd, m, r2)
     assert rel_fro(z, zd) <= Z_TOL
     assert r1._state == r2._state
+
+
+@pytest.mark.parametrize("m,B,n,seed", [(8, 40, 300, 3), (16, 2048, 1000, 12345), (5, 1, 77, 9)])
+def test_materialize_projection(cg, reference, m, B, n, seed, g_mode):
+    """T = G.S as svm-check builds it, gemm(t.g, materialize(t.cs))
+    (tools/countgauss_main.cpp:660-668), with the reference's own gemm and materialize over
+    this transform's G: bit-identical."""
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(seed))
+    T = t.materialize()
+    ref = reference.xform_explicit(B, t.cs.hash, t.cs.sign, np.asfortranarray(t.g))
+    s_mat = ref.materialized_sketch(np.eye(n))  # B x n
+    assert np.array_equal(T, reference.gemm(t.g, s_mat))
+    assert T.shape == (m, n)
