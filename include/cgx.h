@@ -141,6 +141,19 @@ int cgx_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int sx_l
 int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_rows, int64_t b0, int64_t b1,
                          int64_t d, int sx_mem, double* z, int z_mem, void* stream);
 
+/* Large CSR ingestion, replacing the text Matrix Market / CSV readers
+ * (io.cpp:72-136, 159-214): a binary container "CGXCSR1" -- 64-byte header, then row
+ * offsets int64[n+1], column indices (CGX_I32/CGX_I64) [nnz], values (CGX_F32/CGX_F64)
+ * [nnz] -- holding the arrays exactly as the apply entry points take them.
+ * cgx_csr_load with mem = CGX_MEM_DEVICE streams the file through two pinned 32 MiB
+ * buffers, overlapping the disk read of chunk k+1 with the H2D copy of chunk k; the
+ * caller provides arrays sized from cgx_csr_info.  With mem = CGX_MEM_HOST it is a plain
+ * read and ctx may be null. */
+int cgx_csr_save(const char* path, const int64_t* rowptr, const void* cols, int idx_type, const void* vals, int dtype,
+                 int64_t n, int64_t d, int64_t nnz);
+int cgx_csr_info(const char* path, int64_t* n, int64_t* d, int64_t* nnz, int* idx_type, int* dtype);
+int cgx_csr_load(cgx_ctx* ctx, const char* path, int64_t* rowptr, void* cols, void* vals, int mem, void* stream);
+
 /* T = G . S  (m x n, column-major): the CountGauss projection matrix that svm-check builds as
  * gemm(t.g, reference::materialize(t.cs)) (tools/countgauss_main.cpp:660-668, svm.cpp:128-150).
  * Column i is sign_i * G(:, hash_i), bit-identical to that gemm (which skips S's zeros). */

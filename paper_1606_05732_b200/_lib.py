@@ -53,6 +53,9 @@ SIGNATURES = {
     "cgx_gauss_gemm": (_I, [_P, _P, _P, _I, _I64, _I, _P, _I, _P]),
     "cgx_select_extremes": (_I, [_P, _P, _I64, _I64, _I, _P, _P, _P, _P]),
     "cgx_gaussian_project_dense": (_I, [_P, _U64, _I64, _P, _I, _I, _I64, _I64, _I64, _I, _P, _I, _P]),
+    "cgx_csr_save": (_I, [C.c_char_p, _P, _P, _I, _P, _I, _I64, _I64, _I64]),
+    "cgx_csr_info": (_I, [C.c_char_p, _P, _P, _P, _P, _P]),
+    "cgx_csr_load": (_I, [_P, C.c_char_p, _P, _P, _P, _I, _P]),
     "cgx_countgauss_materialize": (_I, [_P, _P, _P, _I, _P]),
     "cgx_gaussian_project_csr": (_I, [_P, _U64, _I64, _P, _P, _I, _P, _I, _I64, _I64, _I64, _I, _P, _I, _P]),
     "cgx_countsketch_batch_gram": (_I, [_P, _U64, _I64, _I64, _I64, _P, _I64, _I64, _I64, _I, _P, _P, _I, _P]),

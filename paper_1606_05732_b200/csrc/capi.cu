@@ -958,6 +958,35 @@ int cgx_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d, int
     });
 }
 
+int cgx_csr_save(const char* path, const int64_t* rowptr, const void* cols, int idx_type, const void* vals, int dtype,
+                 int64_t n, int64_t d, int64_t nnz) {
+    return guard([&] {
+        if (!path) fail(CGX_EINVAL, "cgx_csr_save: null path");
+        csr_save(path, rowptr, cols, idx_type, vals, dtype, n, d, nnz);
+    });
+}
+
+int cgx_csr_info(const char* path, int64_t* n, int64_t* d, int64_t* nnz, int* idx_type, int* dtype) {
+    return guard([&] {
+        if (!path) fail(CGX_EINVAL, "cgx_csr_info: null path");
+        csr_info(path, n, d, nnz, idx_type, dtype);
+    });
+}
+
+int cgx_csr_load(cgx_ctx* ctx, const char* path, int64_t* rowptr, void* cols, void* vals, int mem, void* stream) {
+    return guard([&] {
+        need_mem(mem);
+        if (!path) fail(CGX_EINVAL, "cgx_csr_load: null path");
+        if (mem == CGX_MEM_HOST) {  // plain file read, no device involved (ctx may be null)
+            csr_load(nullptr, path, rowptr, cols, vals, mem, nullptr);
+            return;
+        }
+        need_ctx(ctx);
+        CallScope sc(ctx, stream);
+        csr_load(ctx, path, rowptr, cols, vals, mem, sc.st);
+    });
+}
+
 int cgx_countgauss_materialize(cgx_ctx* ctx, const cgx_xform* xf, double* t, int mem, void* stream) {
     return guard([&] {
         need_ctx(ctx);

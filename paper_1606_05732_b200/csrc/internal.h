@@ -175,6 +175,12 @@ void launch_gen_csr_fill(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, cons
 void launch_gproject_csr(cgx_ctx* ctx, uint64_t g_seed, int64_t m, const int64_t* rowptr, const void* cols,
                          int idx_type, const void* vals, int dtype, int64_t n, int64_t d, double* z, cudaStream_t s);
 
+// csr_io.cu: binary CSR container (CGXCSR1) and the streamed file -> pinned -> HBM loader
+void csr_save(const char* path, const int64_t* rowptr, const void* cols, int idx_type, const void* vals, int dtype,
+              int64_t n, int64_t d, int64_t nnz);
+void csr_info(const char* path, int64_t* n, int64_t* d, int64_t* nnz, int* idx_type, int* dtype);
+void csr_load(cgx_ctx* ctx, const char* path, int64_t* rowptr, void* cols, void* vals, int mem, cudaStream_t s);
+
 // batch.cu: distcheck's trial loop -- su = S_t.U and gram(su) for trials [t0, t0+trials)
 void launch_batch_sketch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_t trials, int64_t B, const double* u,
                               int64_t ld, int64_t n, int64_t d, double* su_out, double* gram_out, cudaStream_t s);

@@ -613,3 +613,29 @@ def test_materialize_projection(cg, reference, m, B, n, seed, g_mode):
     s_mat = ref.materialized_sketch(np.eye(n))  # B x n
     assert np.array_equal(T, reference.gemm(t.g, s_mat))
     assert T.shape == (m, n)
+
+
+def test_csr_streamed_device_load(cg, tmp_path):
+    """cgx_csr_load into HBM through the pinned double buffer (files of several 32 MiB
+    chunks): arrays identical to the saved ones, and S.X of the loaded matrix equals S.X of
+    the in-memory one."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    n, d = 400000, 256
+    lens = rng.poisson(20, n)
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    c = rng.integers(0, d, int(rp[-1])).astype(np.int32)
+    v = rng.standard_normal(int(rp[-1])).astype(np.float32)
+    x = cg.SparseMatrix(n, d, rp, c, v)
+    p = str(tmp_path / "big.cgxcsr")
+    x.save(p)
+    y = cg.SparseMatrix.load(p, device=0)
+    torch.cuda.synchronize()
+    assert y.values.is_cuda and y.col_indices.dtype == torch.int32
+    assert np.array_equal(y.row_offsets.cpu().numpy(), rp)
+    assert np.array_equal(y.col_indices.cpu().numpy(), c)
+    assert np.array_equal(y.values.cpu().numpy(), v)
+    t = cg.countgauss_new(16, 4096, n, cg.SeededRng(3))
+    assert np.array_equal(cg.countsketch_apply(t, y).cpu().numpy(), cg.countsketch_apply(t, x))
