@@ -639,3 +639,24 @@ def test_csr_streamed_device_load(cg, tmp_path):
     assert np.array_equal(y.values.cpu().numpy(), v)
     t = cg.countgauss_new(16, 4096, n, cg.SeededRng(3))
     assert np.array_equal(cg.countsketch_apply(t, y).cpu().numpy(), cg.countsketch_apply(t, x))
+
+
+def test_concurrent_calls_from_threads(cg, restatement):
+    """The boundary is called from inside OpenMP regions (distcheck.cpp:107-111,
+    acceptance.cpp:181-188): many host threads building transforms and applying them on
+    one device at once must each get the serial result."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(77)
+    xs = [rng.standard_normal((3000, 7)) for _ in range(16)]
+
+    def job(k):
+        t = cg.countgauss_new(6, 97, 3000, cg.SeededRng(1000 + k))
+        return cg.countsketch_apply(t, xs[k]), cg.countgauss_apply(t, xs[k])
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        par = list(ex.map(job, range(16)))
+    for k in range(16):
+        z_ref, sx_ref = restatement.countgauss(1000 + k, 6, 97, x=xs[k])
+        assert np.array_equal(par[k][0], sx_ref)
+        assert rel_fro(par[k][1], z_ref) <= Z_TOL
