@@ -51,11 +51,14 @@ __device__ __forceinline__ void cp_wait() {
 // KG k-groups: KG sets of WGM x WGN warps share the CTA tile and split each BK slice
 // (group g takes k4-steps g, g+KG, ...); their accumulators are summed in group order at
 // the end, so a small Z tile still gets 8 warps per CTA without more split-K partials.
-template <int WGM, int WGN, int KG, bool V2>  // CTA tile = 32*WGM x 32*WGN, 32*WGM*WGN*KG threads
-__global__ void __launch_bounds__(32 * WGM * WGN * KG, (32 * WGM * WGN * KG) <= 256 ? 512 / (32 * WGM * WGN * KG) : 1)
+// FM x FN m8n8 fragments per warp (warp tile 8FM x 8FN): 4 x 4 by default; 8 x 4 halves the
+// fragment loads per DMMA for large Z at one CTA per SM.
+template <int WGM, int WGN, int KG, bool V2, int FM = 4, int FN = 4>  // CTA tile 8FM*WGM x 8FN*WGN
+__global__ void __launch_bounds__(32 * WGM * WGN * KG,
+                                  FM * FN > 16 ? 1 : ((32 * WGM * WGN * KG) <= 256 ? 512 / (32 * WGM * WGN * KG) : 1))
     gemm_dmma(const double* __restrict__ A, int64_t m, const double* __restrict__ Bm, int64_t d, int64_t K, int64_t kps,
               double* __restrict__ C, int accumulate) {
-    constexpr int BM = 32 * WGM, BN = 32 * WGN, NT = 32 * WGM * WGN * KG;
+    constexpr int BM = 8 * FM * WGM, BN = 8 * FN * WGN, NT = 32 * WGM * WGN * KG;
     constexpr int LDA = BM + 4, LDB = BN + 4;  // padding: 2-wavefront fragment loads
     static_assert(KG == 1 || KG == 2 || KG == 4, "BK = 16 has 4 k4-steps");
     extern __shared__ double dsm[];
@@ -98,11 +101,11 @@ __global__ void __launch_bounds__(32 * WGM * WGN * KG, (32 * WGM * WGN * KG) <= 
         }
     };
 
-    double acc[4][4][2];
+    double acc[FM][FN][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -113,19 +116,19 @@ __global__ void __launch_bounds__(32 * WGM * WGN * KG, (32 * WGM * WGN * KG) <= 
         cp_wait<STAGES - 2>();
         __syncthreads();
         const int stage = t % STAGES;
-        const double* as = As + stage * BK * LDA + wm * 32 + (lane >> 2);
-        const double* bs = Bs + stage * BK * LDB + wn * 32 + (lane >> 2);
+        const double* as = As + stage * BK * LDA + wm * 8 * FM + (lane >> 2);
+        const double* bs = Bs + stage * BK * LDB + wn * 8 * FN + (lane >> 2);
 #pragma unroll
         for (int k4 = 4 * grp; k4 < BK; k4 += 4 * KG) {
-            double a[4], b[4];
+            double a[FM], b[FN];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = as[(k4 + (lane & 3)) * LDA + i * 8];
+            for (int i = 0; i < FM; ++i) a[i] = as[(k4 + (lane & 3)) * LDA + i * 8];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = bs[(k4 + (lane & 3)) * LDB + j * 8];
+            for (int j = 0; j < FN; ++j) b[j] = bs[(k4 + (lane & 3)) * LDB + j * 8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < FM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+                for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
         const int nt = t + STAGES - 1;
         if (nt < ntiles) load_tile(nt % STAGES, nt);
@@ -136,38 +139,38 @@ __global__ void __launch_bounds__(32 * WGM * WGN * KG, (32 * WGM * WGN * KG) <= 
         __syncthreads();     // pipeline buffers are free now
         constexpr int G0 = 32 * WGM * WGN;
         if (grp > 0) {
-            double* dst = dsm + ((size_t)(grp - 1) * G0 + wg * 32 + lane) * 32;
+            double* dst = dsm + ((size_t)(grp - 1) * G0 + wg * 32 + lane) * (2 * FM * FN);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < FM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    dst[(i * 4 + j) * 2] = acc[i][j][0];
-                    dst[(i * 4 + j) * 2 + 1] = acc[i][j][1];
+                for (int j = 0; j < FN; ++j) {
+                    dst[(i * FN + j) * 2] = acc[i][j][0];
+                    dst[(i * FN + j) * 2 + 1] = acc[i][j][1];
                 }
         }
         __syncthreads();
         if (grp > 0) return;
 #pragma unroll
         for (int g = 1; g < KG; ++g) {
-            const double* src = dsm + ((size_t)(g - 1) * G0 + wg * 32 + lane) * 32;
+            const double* src = dsm + ((size_t)(g - 1) * G0 + wg * 32 + lane) * (2 * FM * FN);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < FM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    acc[i][j][0] += src[(i * 4 + j) * 2];
-                    acc[i][j][1] += src[(i * 4 + j) * 2 + 1];
+                for (int j = 0; j < FN; ++j) {
+                    acc[i][j][0] += src[(i * FN + j) * 2];
+                    acc[i][j][1] += src[(i * FN + j) * 2 + 1];
                 }
         }
     }
     double* cp = C + split * m * d;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < FN; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t r = m0 + wm * 32 + i * 8 + (lane >> 2);
-                const int64_t c = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + h;
+                const int64_t r = m0 + wm * 8 * FM + i * 8 + (lane >> 2);
+                const int64_t c = n0 + wn * 8 * FN + j * 8 + (lane & 3) * 2 + h;
                 if (r < m && c < d) {
                     double* p = cp + c * m + r;
                     *p = accumulate ? *p + acc[i][j][h] : acc[i][j][h];
@@ -185,10 +188,10 @@ __global__ void gen_gauss_cols(uint64_t g_seed, int64_t m, int64_t c0, int64_t c
 }
 
 // gready: all of G[:, b0:b1) already materialized (m x K column-major), or nullptr.
-template <int WGM, int WGN, int KG = 1>
+template <int WGM, int WGN, int KG = 1, int FM = 4, int FN = 4>
 void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d, double* z,
                 cudaStream_t s, const double* gready = nullptr) {
-    constexpr int BM = 32 * WGM, BN = 32 * WGN, NT = 32 * WGM * WGN * KG;
+    constexpr int BM = 8 * FM * WGM, BN = 8 * FN * WGN, NT = 32 * WGM * WGN * KG;
     const int64_t m = xf->m, K = b1 - b0;
     // super-chunk of S bucket-columns: m x S fp64 <= 48 MB (L2-resident), multiple of BK.
     // (Sizing it so the chunk's S.X rows fit L2 too measured slower: every chunk costs each
@@ -197,7 +200,7 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     S = S < BK ? BK : S / BK * BK;
     if (S > K) S = (K + BK - 1) / BK * BK;
     const int64_t tm = (m + BM - 1) / BM, tn = (d + BN - 1) / BN;
-    const int64_t resident = (int64_t)ctx->num_sms * (NT <= 256 ? 512 / NT : 1);  // CTAs per wave
+    const int64_t resident = (int64_t)ctx->num_sms * (FM * FN > 16 ? 1 : (NT <= 256 ? 512 / NT : 1));  // CTAs per wave
     int64_t splits = (resident + tm * tn - 1) / (tm * tn);
     const int64_t max_splits = (S + 4 * BK - 1) / (4 * BK);  // >= 4 K-tiles per split per chunk
     splits = splits < 1 ? 1 : (splits > max_splits ? max_splits : splits);
@@ -208,9 +211,9 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
     const bool v2 = m % 2 == 0 && d % 2 == 0 && ((uintptr_t)sx % 16) == 0 &&
                     (gready ? (uintptr_t)gready % 16 == 0 : !xf->g_dev || (uintptr_t)xf->g_dev % 16 == 0);
-    auto kern = v2 ? gemm_dmma<WGM, WGN, KG, true> : gemm_dmma<WGM, WGN, KG, false>;
+    auto kern = v2 ? gemm_dmma<WGM, WGN, KG, true, FM, FN> : gemm_dmma<WGM, WGN, KG, false, FM, FN>;
     const size_t pipe = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
-    const size_t fold = sizeof(double) * (size_t)((KG - 1) * BM * BN);
+    const size_t fold = sizeof(double) * (size_t)((KG - 1) * BM * BN);  // KG > 1 only with FM = FN = 4
     const size_t smem = pipe > fold ? pipe : fold;
     CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool first = true;
@@ -247,6 +250,7 @@ bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* 
                                int64_t d, double* z, cudaStream_t s, bool force) {
     const int64_t m = xf->m;
     if (!force && m * d <= 64 * 128) return false;  // small Z: the wide in-kernel-generation GEMM is better
+    // (64 x 32 warp tiles at one CTA per SM measured slower: c5 19.2 vs 13.7 ms, c3 0.82 vs 0.70)
     if (m >= 2 * d)
         run_chunks<4, 2>(ctx, xf, sx, b0, b1, d, z, s);  // 128 x 64 tiles
     else

@@ -23,9 +23,13 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--explicit", type=int, default=0)
+    ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE")
     a = ap.parse_args()
     B, m, d = SHAPES[a.config]
     ctx = cg.context(0)
+    for kv in a.opt:
+        k, v = kv.split("=", 1)
+        ctx.set_option(k, int(v))
     t = cg.countgauss_new(m, B, 10, cg.SeededRng(12345))
     if a.explicit:
         g = torch.empty((B, m), dtype=torch.float64, device="cuda")
