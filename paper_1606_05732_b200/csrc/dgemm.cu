@@ -72,20 +72,46 @@ __global__ void __launch_bounds__(32 * WGM * WGN * KG,
     const int64_t kb = split * kps, ke = min(K, kb + kps);
     const int ntiles = (int)((ke - kb + BK - 1) / BK);
 
+    // V2: this thread's 16 B pieces of every tile sit at fixed (k, row/col) offsets, so their
+    // global pointers are set up once and advance by BK rows per issued tile (tiles are
+    // issued in order) -- no per-tile index arithmetic next to the DMMAs.
+    constexpr int PA = (BK * BM / 2 + NT - 1) / NT, PB = (BK * BN / 2 + NT - 1) / NT;
+    const double* ga[PA];
+    const double* gb[PB];
+    int sa_off[PA], sb_off[PB], ka[PA], kb_[PB];
+    bool oka[PA], okb[PB];
+    if constexpr (V2) {
+#pragma unroll
+        for (int q = 0; q < PA; ++q) {
+            const int e = tid + q * NT, kk = e / (BM / 2), r = 2 * (e - kk * (BM / 2));
+            ka[q] = kk;
+            oka[q] = e < BK * BM / 2 && m0 + r < m;
+            sa_off[q] = kk * LDA + r;
+            ga[q] = A + (kb + kk) * m + m0 + r;
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            const int e = tid + q * NT, kk = e / (BN / 2), c = 2 * (e - kk * (BN / 2));
+            kb_[q] = kk;
+            okb[q] = e < BK * BN / 2 && n0 + c < d;
+            sb_off[q] = kk * LDB + c;
+            gb[q] = Bm + (kb + kk) * d + n0 + c;
+        }
+    }
     auto load_tile = [&](int stage, int t) {
         const int64_t k0 = kb + (int64_t)t * BK;
         double* as = As + stage * BK * LDA;
         double* bs = Bs + stage * BK * LDB;
         if constexpr (V2) {
-            for (int e = tid; e < BK * BM / 2; e += NT) {
-                const int kk = e / (BM / 2), r = 2 * (e - kk * (BM / 2));
-                const int64_t gk = k0 + kk, gr = m0 + r;
-                cp_async16(as + kk * LDA + r, A + gk * m + gr, gk < ke && gr < m);
+#pragma unroll
+            for (int q = 0; q < PA; ++q) {
+                if (tid + q * NT < BK * BM / 2) cp_async16(as + sa_off[q], ga[q], oka[q] && k0 + ka[q] < ke);
+                ga[q] += BK * m;
             }
-            for (int e = tid; e < BK * BN / 2; e += NT) {
-                const int kk = e / (BN / 2), c = 2 * (e - kk * (BN / 2));
-                const int64_t gk = k0 + kk, gc = n0 + c;
-                cp_async16(bs + kk * LDB + c, Bm + gk * d + gc, gk < ke && gc < d);
+#pragma unroll
+            for (int q = 0; q < PB; ++q) {
+                if (tid + q * NT < BK * BN / 2) cp_async16(bs + sb_off[q], gb[q], okb[q] && k0 + kb_[q] < ke);
+                gb[q] += BK * d;
             }
         } else {
             for (int e = tid; e < BK * BM; e += NT) {
