@@ -179,6 +179,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// ---- bulk copies (TMA engine, 1-D): global -> shared, completion counted on an mbarrier --
+// The arriving thread announces the transaction bytes, then issues copies that complete_tx
+// on the same barrier; waiters see the phase flip once every byte has landed.
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                     smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// size and both addresses multiples of 16 bytes
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(smem)),
+                 "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
 // ---- cp.async (LDGSTS): 16 B global -> shared, bypassing L1; completion by group ------
 __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");

@@ -348,8 +348,17 @@ def test_csr_zipf_config5_shape(cg, restatement):
     assert rel_fro(cg.countgauss_apply(t, x).cpu().numpy(), z_ref) <= Z_TOL
 
 
-@pytest.mark.parametrize("m,d,B", [(96, 300, 20011), (256, 512, 40000), (130, 70, 9000), (64, 129, 33333)])
-def test_stage2_large_z(cg, restatement, m, d, B, g_mode):
+@pytest.fixture(params=[0, 1], ids=["gemm-pipelined", "gemm-warp-specialized"])
+def gemm_ws(request, cg):
+    ctx = cg.context()
+    ctx.set_option("gemm_ws", request.param)
+    yield request.param
+    ctx.set_option("gemm_ws", 0)
+
+
+@pytest.mark.parametrize("m,d,B", [(96, 300, 20011), (256, 512, 40000), (130, 70, 9000), (64, 129, 33333),
+                                   (128, 256, 30000)])
+def test_stage2_large_z(cg, restatement, m, d, B, g_mode, gemm_ws):
     """Stage 2 on its own (gemm(t.g, SX), matrix.cpp:111-129) for Z shapes that take the
     G-super-chunk + pipelined DMMA path, with G seeded (generated) and explicit."""
     import ctypes as C
