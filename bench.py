@@ -298,7 +298,7 @@ def run_ours(args):
         kernel_name = ("countgauss_dense_ws (one pass: sketch + G + G.(S.X))" if fused
                        else "sketch_dense_async (stage 1: cp.async row gather -> S.X)")
     else:
-        kernel_name = "sketch_csr_kernel (stage 1: bucket-ordered row gather -> S.X)"
+        kernel_name = "sketch_csr_lean (stage 1: bucket-ordered row gather -> S.X)"
     sk_avg_ms = sk_ms / max(sk_n, 1)
     achieved = bytes_alg / (sk_avg_ms / 1e3) / 1e9
     traffic = None  # DRAM bytes per launch of this kernel, from the committed ncu capture
