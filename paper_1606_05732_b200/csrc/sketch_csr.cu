@@ -25,20 +25,28 @@ namespace cgx {
 namespace {
 
 constexpr int kWaves = 4;  // item waves loaded before they are applied
+#ifndef CGX_CSR_MINB
+#define CGX_CSR_MINB 4  // 4 CTAs/SM: c5 sketch 17.9 -> 15.3 ms (tools/sweep_csr.sh)
+#endif
+#ifndef CGX_CSR_KW
+#define CGX_CSR_KW 4
+#endif
 
-// Random short reads: a plain global load that does not allocate in L1 (the gathered
-// rows are never re-read by this SM), so only the touched 32 B sectors move.
+// Random short reads: a global load that does not allocate in L1 (the gathered rows are
+// never re-read by this SM) and asks L2 for a 64 B fetch.  Without the L2::64B hint every
+// L1 miss is promoted to a 128 B L2/DRAM fetch: a random 4 B load then costs 128 B of DRAM
+// traffic, with it 64 B (tools/microbench/sector_fetch.cu; 64 B is the smallest hint).
 template <typename T>
 __device__ __forceinline__ T ld_na(const T* p) {
     if constexpr (sizeof(T) == 8) {
         unsigned long long v;
-        asm volatile("ld.global.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+        asm volatile("ld.global.L1::no_allocate.L2::64B.b64 %0, [%1];" : "=l"(v) : "l"(p));
         T out;
         memcpy(&out, &v, 8);
         return out;
     } else {
         unsigned v;
-        asm volatile("ld.global.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+        asm volatile("ld.global.L1::no_allocate.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
         T out;
         memcpy(&out, &v, 4);
         return out;
@@ -183,11 +191,11 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
 //    is processed, and a group's item loads are issued kW waves at a time.
 // Adds happen in exactly the serial kernel's order, so S.X is bit-identical to it.
 template <typename TV, typename TI>
-__global__ void __launch_bounds__(256) sketch_csr_lean(const int64_t* __restrict__ rowptr, const TI* __restrict__ cols,
+__global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64_t* __restrict__ rowptr, const TI* __restrict__ cols,
                                                        const TV* __restrict__ vals, const uint32_t* __restrict__ perm,
                                                        const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
                                                        double* __restrict__ sx, int cbits) {
-    constexpr int kW = 4;
+    constexpr int kW = CGX_CSR_KW;
     extern __shared__ double smem[];
     __shared__ uint8_t s_tbl[8][32];
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
