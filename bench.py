@@ -147,11 +147,11 @@ def cpu_reference_run(cfg_name, c, steps, warmup):
     R.set_threads(threads)
     cores = R.max_threads()
     t_seed_rng = SEED
+    if c["kind"] != "dense":
+        return _cpu_reference_csr(cfg_name, c, R, steps, cores)
     t0 = time.time()
     xf = R.countgauss_new(c["m"], c["B"], c["n"], t_seed_rng)
     construct_s = time.time() - t0
-    if c["kind"] != "dense":
-        raise SystemExit("cpu reference arm implemented for dense configs")
     xm = R.dense_generated(c["n"], c["d"], mix64(SEED, 2), O)
     ms, _ = xf.time_apply(xm, 1, max(1, steps + warmup - 1))
     ms = list(ms)[warmup - 1:] if warmup > 1 else list(ms)
@@ -160,6 +160,47 @@ def cpu_reference_run(cfg_name, c, steps, warmup):
     return dict(value=units / (med / 1e3), ms=ms, median_ms=med, cores=cores, construct_s=construct_s,
                 sample=(f"full {cfg_name}: countgauss_apply on fp64 column-major X (the reference layout), "
                         f"{len(ms)} timed calls after warm-up, median; reference CSR/dense code as-is"))
+
+
+def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000):
+    """CSR configs: the reference's countgauss_apply on a bounded row sample of the config's
+    X (its first rows, same generator), timed as the whole apply (kind 1) and as the sketch
+    alone (kind 0).  The full-size time is extrapolated as sketch_ms * nnz/nnz_sample +
+    (apply_ms - sketch_ms): the serial CSR sketch is linear in nnz, and the GEMM stage
+    (m x B by B x d) does not depend on n."""
+    import numpy as np
+    import torch
+
+    from paper_1606_05732_b200 import bench_data
+
+    mean = c.get("mean_row_nnz") or (c["d"] * c.get("density", 0.0) or 17.36)
+    rows = int(min(c["n"], max(1024, sample_nnz / mean)))
+    if "zipf" in c:
+        s_len, cap, s_col = c["zipf"]
+        x = bench_data.csr_zipf(rows, c["d"], seed=mix64(SEED, 5), s_len=s_len, cap=cap, s_col=s_col)
+    else:
+        x = bench_data.csr_bernoulli(rows, c["d"], c["density"], seed=mix64(SEED, 3))
+    rp = x.row_offsets.cpu().numpy()
+    ci = x.col_indices.cpu().numpy().astype(np.int64)
+    vv = x.values.cpu().numpy().astype(np.float64)
+    nnz_s = int(rp[-1])
+    del x
+    torch.cuda.empty_cache()
+    xm = R.csr(rp, ci, vv, rows, c["d"])
+    t0 = time.time()
+    xf = R.countgauss_new(c["m"], c["B"], rows, SEED)
+    construct_s = time.time() - t0
+    reps = max(1, min(steps, 5))
+    ms_all, _ = xf.time_apply(xm, 1, reps)
+    ms_sk, _ = xf.time_apply(xm, 0, reps)
+    t_all, t_sk = statistics.median(ms_all), statistics.median(ms_sk)
+    nnz_full = c.get("nnz_full") or nnz_s * (c["n"] / rows)
+    est_ms = t_sk * nnz_full / nnz_s + max(0.0, t_all - t_sk)
+    return dict(value=nnz_full / (est_ms / 1e3), ms=[est_ms] * reps, median_ms=est_ms, cores=cores,
+                construct_s=construct_s,
+                sample=(f"{cfg_name} rows 0..{rows} ({nnz_s} nnz) through the reference's countgauss_apply "
+                        f"(serial CSR branch + OpenMP gemm): apply {t_all:.0f} ms, sketch {t_sk:.0f} ms, median of "
+                        f"{reps}; full size extrapolated as sketch x nnz ratio + gemm"))
 
 
 def run_reference_arm(args):
@@ -363,7 +404,7 @@ def run_ours(args):
                              "bench's O(nnz*m) loop (countgauss_main.cpp:535-547), the config-5 ablation")}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and c["kind"] == "dense":
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
             r = cpu_reference_run(args.config, c, 1, 1)
             cpu = {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "reference",
