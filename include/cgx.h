@@ -204,15 +204,26 @@ int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, dou
                           void* stream);
 
 /* Config-5 style heavy-tailed CSR: row i draws a target length L from Zipf(s_len) on
- * [1, cap]; column j is kept with probability min(1, L * w_j), w_j ~ (j+1)^-s_col
- * normalized (Zipf-skewed columns, sorted and distinct).  Same two-phase protocol. */
+ * [1, cap]; column j is kept with probability min(1, c_L * w_j), w_j ~ (j+1)^-s_col
+ * normalized and c_L solved so that a row's expected length is L (Zipf-skewed columns,
+ * sorted and distinct).  Same two-phase protocol. */
 int cgx_gen_csr_zipf(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double s_len, int64_t cap, double s_col,
                      int64_t* rowptr_dev, int32_t* cols_dev, float* vals_dev, int64_t* nnz_out, void* stream);
 
 /* ---- instrumentation ---------------------------------------------------------------- */
-/* Context options.  "fuse" (default 1): countgauss_apply on dense wide-row X runs the
- * one-pass sketch+G+contraction kernel; 0 forces the two-stage path (S.X to HBM, then
- * the Gaussian GEMM).  Both give the same S.X bits; Z agrees to rounding. */
+/* Context options (kernel variants for A/B runs; every variant gives the same S.X bits and
+ * Z to rounding):
+ *   "g_resident"   1 (default): countgauss_new materializes G (<= 4 GiB) and applies read
+ *                  it; 0: G is generated inside the apply kernels.  Set before construction.
+ *   "fuse"         1 (default): the one-pass dense kernel (sketch + G + contraction) when G
+ *                  is not resident; 2: also when it is; 0: always the two stages.
+ *   "fuse_mode"    one-pass variant: 2 (default) warp-specialized, 1 all-warps, 3 G on a
+ *                  side stream, 4 6+2 warps with Z in shared memory.
+ *   "async_stages" dense row-gather ring depth: 2 (default), 3, 4; 0 = register batches.
+ *   "csr_mode"     0/1 (default): bucket-ordered row gather; 2: stable two-level partition.
+ *   "gemm_ws"      0 (default): cp.async-pipelined DMMA stage 2; 1: warp-specialized
+ *                  bulk-copy producer (large Z whose tiles divide it).
+ *   "rows_per_task", "grid_waves", "ws_gw": scheduling knobs of the dense kernels. */
 int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched so far. */
 uint64_t cgx_launch_count(const cgx_ctx* ctx);
