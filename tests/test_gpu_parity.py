@@ -669,3 +669,43 @@ def test_concurrent_calls_from_threads(cg, restatement):
         z_ref, sx_ref = restatement.countgauss(1000 + k, 6, 97, x=xs[k])
         assert np.array_equal(par[k][0], sx_ref)
         assert rel_fro(par[k][1], z_ref) <= Z_TOL
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_shards_recompose(cg, restatement, world, g_mode):
+    """The GPU side of the multi-GPU path, ranks emulated one after another on
+    one device: each shard transform (cgx_countgauss_new_shard, global row indices from the
+    shared seed) carries exactly the full transform's rows' hash/sign and G; the shards'
+    S.X partials sum to S.X, their Z partials to Z ("z" combine); and stage 2 over bucket
+    slices of the summed S.X (cgx_gauss_gemm_range, the "sx" combine) sums to Z as well."""
+    import ctypes as C
+
+    from paper_1606_05732_b200._lib import CGX_MEM_HOST, check, lib
+    from paper_1606_05732_b200.distributed import bucket_range, shard_range
+
+    n, d, B, m, seed = 20011, 24, 997, 12, 31337
+    x = np.random.default_rng(world).standard_normal((n, d))
+    full = cg.countgauss_new(m, B, n, cg.SeededRng(seed))
+    t_seed = full.seed
+    z_ref, sx_ref = restatement.countgauss(seed, m, B, x=x)
+    sx_sum = np.zeros((B, d))
+    z_sum = np.zeros((m, d))
+    for rank in range(world):
+        r0, r1 = shard_range(n, world, rank)
+        t = cg.api.countgauss_new_shard(m, B, n, r0, r1 - r0, t_seed)
+        assert np.array_equal(t.cs.hash, full.cs.hash[r0:r1]) and np.array_equal(t.cs.sign, full.cs.sign[r0:r1])
+        assert np.array_equal(t.g, full.g)
+        sx_sum += cg.countsketch_apply(t, x[r0:r1])
+        z_sum += cg.countgauss_apply(t, x[r0:r1])
+    assert rel_fro(sx_sum, sx_ref) <= 1e-14
+    assert rel_fro(z_sum, z_ref) <= Z_TOL
+    z_sx = np.zeros((m, d))
+    ctx = cg.context()
+    for rank in range(world):
+        b0, b1 = bucket_range(B, world, rank)
+        sl = np.ascontiguousarray(sx_sum[b0:b1])  # row-major (b1-b0) x d slice
+        zp = np.empty((m, d), order="F")
+        check(lib.cgx_gauss_gemm_range(ctx.h, full._xf.h, sl.ctypes.data, b0, b1, d, CGX_MEM_HOST, zp.ctypes.data,
+                                       CGX_MEM_HOST, None))
+        z_sx += zp
+    assert rel_fro(z_sx, z_ref) <= Z_TOL
