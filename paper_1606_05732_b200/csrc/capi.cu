@@ -774,10 +774,11 @@ int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x,
             return;
         }
         // One-pass kernel (sketch + G generation + contraction) when G must be generated and
-        // the shape allows.  With G in memory the two stages win: the cp.async stream sketch
-        // leaves S.X in L2 and the split-K DMMA contraction streams G (c2 0.418 vs 0.427 ms,
-        // c4 2.57 vs 3.59 ms measured).
-        if (!ctx->no_fuse && (!xf->g_dev || ctx->force_fuse)) {
+        // rows are narrow (d <= 64).  With G in memory, or wide rows, the two stages win: the
+        // cp.async stream sketch leaves S.X in L2 and the split-K DMMA contraction streams G
+        // (measured: resident G c2 0.418 vs 0.427 ms, c4 2.57 vs 3.59 ms; generated G c2
+        // one-pass 0.439 ms, c4 two-stage beats one-pass 3.62 ms).
+        if (!ctx->no_fuse && ((!xf->g_dev && d <= 64) || ctx->force_fuse)) {
             const size_t zb = sizeof(double) * (size_t)(xf->m * d);
             double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
             ctx->prof.begin(0, sc.st);

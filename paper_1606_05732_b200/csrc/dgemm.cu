@@ -417,15 +417,15 @@ void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t col
 
 bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
                                int64_t d, double* z, cudaStream_t s) {
-    // Z covered by one CTA tile of <= 8 warps (32 x 32 each) with G in memory: CTAs of
-    // exactly the Z tile, many split-K CTAs per SM -- the contraction is a bandwidth-bound
-    // stream of G and S.X.
+    // Z covered by one CTA tile of <= 8 warps (32 x 32 each): CTAs of exactly the Z tile,
+    // many split-K CTAs per SM -- the contraction is a bandwidth-bound stream of G (in
+    // memory, or generated into L2-resident chunks) and S.X.
     const int64_t m = xf->m;
-    if (!xf->g_dev) return false;
     auto p2 = [](int64_t v) { int64_t p = 1; while (p < v) p <<= 1; return p; };
     const int64_t wm = p2((m + 31) / 32), wn = p2((d + 31) / 32);
     if (wm * wn > 8) return false;
-    const double* g = xf->g_dev + b0 * m;
+    // G in memory: read it; otherwise run_chunks generates L2-resident column chunks first
+    const double* g = xf->g_dev ? xf->g_dev + b0 * m : nullptr;
 #define CGX_SMALL(A, B_, KG_)                                           \
     if (wm == A && wn == B_) {                                          \
         run_chunks<A, B_, KG_>(ctx, xf, sx, b0, b1, d, z, s, g);        \

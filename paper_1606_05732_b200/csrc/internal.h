@@ -139,8 +139,8 @@ void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStre
 void launch_materialize_t(cgx_ctx* ctx, const cgx_xform* xf, double* t, cudaStream_t s);
 // dgemm.cu: G columns [c0, c0+cols) of the transform -> out (m x cols, col-major)
 void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t cols, double* out, cudaStream_t s);
-// dgemm.cu: Z within one CTA tile (ceil(m/32) x ceil(d/32) <= 8 warps) with G in memory
-// (xf->g_dev); false when not applicable
+// dgemm.cu: Z within one CTA tile (ceil(m/32) x ceil(d/32) <= 8 warps), G in memory or
+// generated in L2-resident chunks; false when not applicable
 bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
                                int64_t d, double* z, cudaStream_t s);
 // dgemm.cu: z = g . sx with g = all of G (m x B col-major) already in memory
