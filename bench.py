@@ -286,11 +286,22 @@ def run_ours(args):
     zbuf = torch.empty((d, m), dtype=torch.float64, device=dev)  # contiguous storage of Z^T
     z = zbuf.t()  # column-major m x d view (the reference layout)
 
+    from paper_1606_05732_b200.distributed import combine
+
+    sxbuf = torch.empty((B, d), dtype=torch.float64, device=dev) if world > 1 and args.combine != "z" else None
+
     def step():
-        cg.api.countgauss_apply_into(t, x, z)
-        if world > 1:
-            dist.all_reduce(zbuf)  # partial Z of every row shard -> full Z on every rank
-        return z
+        if world == 1 or args.combine == "z":
+            cg.api.countgauss_apply_into(t, x, z)
+            if world > 1:
+                dist.all_reduce(zbuf)  # partial Z of every row shard -> full Z on every rank
+            return z
+        cg.api.countsketch_apply_into(t, x, sxbuf)  # partial S.X (row-major B x d)
+        if args.combine == "sx":
+            return combine("sx", world=world, rank=rank, B=B, d=d, partial_sx=sxbuf,
+                           stage2=lambda sl, b0, b1: cg.api.gauss_gemm_range(t, sl, b0, b1))
+        return combine("g", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
+                       stage2=lambda sx, r0, r1: cg.api.gauss_gemm_rows(t, sx, r0, r1))
 
     for _ in range(args.warmup):
         step()
@@ -422,7 +433,9 @@ def run_ours(args):
                 "workload": workload_name(args.config, c), "n": n, "d": d, "B": B, "m": m,
                 "rows_per_rank": rows, "nnz_per_rank": int(nnz_local), "mean_row_nnz": nnz_local / rows, "parallelism": f"rows sharded x{world} ({args.scaling} scaling: "
                 + ("the config's n rows per rank" if args.scaling == "weak" else "the config's n rows split across ranks")
-                + ")" + (", NCCL all-reduce of Z" if world > 1 else ""),
+                + ")" + ({"z": ", NCCL all-reduce of Z", "sx": ", NCCL reduce-scatter of S.X + split-K stage 2 + all-reduce of Z",
+                       "g": ", NCCL all-reduce of S.X + G's m rows split over ranks + all-gather of Z"}[args.combine]
+                      if world > 1 else ""),
                 "input_dtype": c.get("dtype", "f32"), "accumulate": "f64 (S.X and G.(S.X))",
                 "l2": f"inputs larger than L2 ({x_bytes / 1e9:.2f} GB X per rank), no flush",
                 "construct_ms": construct_ms,
@@ -461,6 +474,9 @@ def main():
                     help="weak: each rank sketches the config's n rows (X has N*n rows); strong: n split N ways")
     ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
                     help="cgx_set_option before timing (A/B of kernel variants)")
+    ap.add_argument("--combine", default="z", choices=["z", "sx", "g"],
+                    help="N>1 combine: z = all-reduce of Z; sx = reduce-scatter of S.X + split-K stage 2 + "
+                         "all-reduce; g = all-reduce of S.X + G's m rows split over ranks + all-gather")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3", file=sys.stderr)

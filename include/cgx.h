@@ -178,6 +178,12 @@ int cgx_countsketch_batch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_
                                const double* u, int64_t ld, int64_t n, int64_t d, int u_mem, double* su,
                                double* gram, int out_mem, void* stream);
 
+/* Split of G's m rows across ranks (north star's multi-GPU final product):
+ * z = G[r0:r1, :] . sx -- (r1-r0) x d column-major -- with sx the full row-major B x d S.X
+ * (e.g. after an all-reduce of the partial sketches). */
+int cgx_gauss_gemm_rows(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t d, int64_t r0, int64_t r1,
+                        int sx_mem, double* z, int z_mem, void* stream);
+
 /* Dense-Gaussian baseline (SURVEY 8f, config-5 ablation): z = G~ . X with G~ the m x n
  * i.i.d. N(0,1) matrix gaussian_matrix(m, n, rng) would draw (matrix.cpp:199-207) from a
  * SeededRng whose current state is `rng_state` -- the product gp_nmf computes

@@ -538,6 +538,78 @@ def countgauss_apply_into(t: CountGaussTransform, x, z):
     return z
 
 
+def countsketch_apply_into(cs, x, sx):
+    """Device-resident countsketch_apply writing into a preallocated CUDA tensor `sx`
+    (buckets x d, row-major -- ``torch.empty((B, d))`` -- or column-major): the partial
+    sketch a multi-GPU combine reduces."""
+    if isinstance(cs, CountGaussTransform):
+        cs = cs.cs
+    xf = cs._xf
+    if sx.stride(1) == 1 and sx.is_contiguous():
+        out_layout = CGX_ROW_MAJOR
+    elif sx.stride(0) == 1:
+        out_layout = CGX_COL_MAJOR
+    else:
+        raise ValueError("countsketch_apply_into: sx must be row- or column-major")
+    if isinstance(x, SparseMatrix):
+        rp, ci, it, v, dt, mem, keep, dev = _csr_args(x)
+        if not dev:
+            raise ValueError("countsketch_apply_into: device inputs only")
+        check(lib.cgx_countsketch_apply_csr(xf.ctx.h, xf.h, rp, ci, it, v, dt, x.rows, x.cols, x.nnz(), mem,
+                                            sx.data_ptr(), out_layout, CGX_MEM_DEVICE, _stream_of(x.values)))
+        return sx
+    ptr, dt, layout, ld, n, d, mem, keep, dev = _dense_args(x)
+    if not dev:
+        raise ValueError("countsketch_apply_into: device inputs only")
+    check(lib.cgx_countsketch_apply_dense(xf.ctx.h, xf.h, ptr, dt, layout, ld, n, d, mem, sx.data_ptr(), out_layout,
+                                          CGX_MEM_DEVICE, _stream_of(keep)))
+    return sx
+
+
+def _sx_rows_args(sx):
+    """Row-major float64 S.X (numpy or CUDA torch): (ptr, d, mem, keepalive, is_torch)."""
+    if _is_torch(sx):
+        import torch
+
+        if not sx.is_cuda:
+            return _sx_rows_args(sx.numpy())
+        sx = sx.to(torch.float64).contiguous()
+        return sx.data_ptr(), sx.shape[1], CGX_MEM_DEVICE, sx, True
+    sx = np.ascontiguousarray(sx, dtype=np.float64)
+    return sx.ctypes.data, sx.shape[1], CGX_MEM_HOST, sx, False
+
+
+def gauss_gemm_range(t: CountGaussTransform, sx_rows, b0: int, b1: int, z=None):
+    """Split-K piece of stage 2 (the "sx" combine): G[:, b0:b1) . sx_rows for the row-major
+    (b1-b0) x d slice of S.X; m x d column-major (into `z` when given)."""
+    xf = t._xf
+    ptr, d, mem, keep, dev = _sx_rows_args(sx_rows)
+    if keep.shape[0] != b1 - b0:
+        raise ValueError("gauss_gemm_range: sx_rows must have b1-b0 rows")
+    if z is None:
+        z, zptr = _out(t.m, d, dev, keep)
+    else:
+        zptr = z.data_ptr()
+    check(lib.cgx_gauss_gemm_range(xf.ctx.h, xf.h, ptr, b0, b1, d, mem, zptr, mem,
+                                   _stream_of(keep) if dev else None))
+    return z
+
+
+def gauss_gemm_rows(t: CountGaussTransform, sx, r0: int, r1: int, z=None):
+    """Rows [r0, r1) of Z = G.(S.X) from the full row-major buckets x d S.X (the "g" combine:
+    G's m rows split across ranks); (r1-r0) x d column-major (into `z` when given)."""
+    xf = t._xf
+    ptr, d, mem, keep, dev = _sx_rows_args(sx)
+    if keep.shape[0] != t.cs.buckets:
+        raise ValueError("gauss_gemm_rows: sx must be buckets x d")
+    if z is None:
+        z, zptr = _out(r1 - r0, d, dev, keep)
+    else:
+        zptr = z.data_ptr()
+    check(lib.cgx_gauss_gemm_rows(xf.ctx.h, xf.h, ptr, d, r0, r1, mem, zptr, mem, _stream_of(keep) if dev else None))
+    return z
+
+
 # --------------------------------------------------------------------------- NMF
 @dataclass
 class AnchorSet:

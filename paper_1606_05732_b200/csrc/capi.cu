@@ -856,6 +856,32 @@ int cgx_gauss_gemm_range(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_row
     });
 }
 
+int cgx_gauss_gemm_rows(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t d, int64_t r0, int64_t r1,
+                        int sx_mem, double* z, int z_mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(sx_mem);
+        need_mem(z_mem);
+        need_g(xf);
+        if (d < 1 || r0 < 0 || r1 <= r0 || r1 > xf->m) fail(CGX_EINVAL, "gemm: bad row range of G");
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(double) * (size_t)(xf->B * d);
+        const double* sd = (const double*)to_device(ctx, ctx->hstage_dev, sx, bytes, sx_mem, sc.st);
+        const size_t zb = sizeof(double) * (size_t)((r1 - r0) * d);
+        double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
+        ctx->prof.begin(1, sc.st);
+        launch_gauss_gemm_rows(ctx, xf, sd, d, r0, r1, zd, sc.st);
+        ctx->prof.end(1, sc.st);
+        if (z_mem == CGX_MEM_HOST) {
+            CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        } else if (sx_mem == CGX_MEM_HOST) {
+            sc.sync();
+        }
+    });
+}
+
 int cgx_gaussian_project_dense(cgx_ctx* ctx, uint64_t rng_state, int64_t m, const void* x, int dtype, int layout,
                                int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem, void* stream) {
     return guard([&] {

@@ -309,6 +309,16 @@ __global__ void gen_gauss_cols(uint64_t g_seed, int64_t m, int64_t c0, int64_t c
     }
 }
 
+// Rows [r0, r0+rows) of G over all B columns -> out (rows x B, column-major).
+__global__ void gen_gauss_rows(uint64_t g_seed, int64_t m, int64_t r0, int64_t rows, int64_t B,
+                               double* __restrict__ out) {
+    const int64_t total = rows * B;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / rows, r = e - c * rows;
+        out[e] = gauss_entry(g_seed, (uint64_t)m, (uint64_t)(r0 + r), (uint64_t)c);
+    }
+}
+
 // gready: all of G[:, b0:b1) already materialized (m x K column-major), or nullptr.
 template <int WGM, int WGN, int KG = 1, int FM = 4, int FN = 4>
 void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1, int64_t d, double* z,
@@ -435,6 +445,29 @@ bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* 
     CGX_SMALL(2, 2, 2) CGX_SMALL(2, 4, 1) CGX_SMALL(4, 1, 2) CGX_SMALL(4, 2, 1) CGX_SMALL(8, 1, 1)
 #undef CGX_SMALL
     return false;
+}
+
+void launch_gauss_gemm_rows(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t d, int64_t r0, int64_t r1,
+                            double* z, cudaStream_t s) {
+    // G rows [r0, r1) as their own (r1-r0) x B column-major matrix, then the ordinary stage 2
+    const int64_t rows = r1 - r0, B = xf->B;
+    double* gsub = (double*)ctx->gfull.get(sizeof(double) * (size_t)(rows * B));
+    if (xf->g_dev) {
+        CGX_CUDA(cudaMemcpy2DAsync(gsub, sizeof(double) * (size_t)rows, xf->g_dev + r0, sizeof(double) * (size_t)xf->m,
+                                   sizeof(double) * (size_t)rows, (size_t)B, cudaMemcpyDeviceToDevice, s));
+    } else {
+        int64_t blocks = (rows * B + 255) / 256;
+        if (blocks > ctx->num_sms * 32) blocks = ctx->num_sms * 32;
+        gen_gauss_rows<<<(unsigned)blocks, 256, 0, s>>>(xf->g_seed, xf->m, r0, rows, B, gsub);
+        count_launch(ctx);
+        check_launch("gen_gauss_rows");
+    }
+    cgx_xform gx = *xf;  // a view: rows of G, explicit; nothing owned
+    gx.m = rows;
+    gx.g_dev = gsub;
+    gx.g_pool = false;
+    gx.g_explicit = true;
+    launch_gauss_gemm(ctx, &gx, sx, 0, B, d, z, s);
 }
 
 void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, const double* sx, int64_t d, double* z,

@@ -139,6 +139,9 @@ void launch_fill_gaussian(cgx_ctx* ctx, const cgx_xform* xf, double* g, cudaStre
 void launch_materialize_t(cgx_ctx* ctx, const cgx_xform* xf, double* t, cudaStream_t s);
 // dgemm.cu: G columns [c0, c0+cols) of the transform -> out (m x cols, col-major)
 void launch_gen_gauss(cgx_ctx* ctx, const cgx_xform* xf, int64_t c0, int64_t cols, double* out, cudaStream_t s);
+// dgemm.cu: rows [r0, r1) of Z = G[r0:r1, :] . sx (the multi-GPU split of G's m rows)
+void launch_gauss_gemm_rows(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t d, int64_t r0, int64_t r1,
+                            double* z, cudaStream_t s);
 // dgemm.cu: Z within one CTA tile (ceil(m/32) x ceil(d/32) <= 8 warps), G in memory or
 // generated in L2-resident chunks; false when not applicable
 bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,

@@ -12,6 +12,11 @@ T.X is linear, so the partials combine after either stage:
   reduce-scattered; rank p owns buckets [b_p, b_{p+1}) of the summed S.X and computes
   Z_p = G[:, b_p:b_{p+1}) . S.X[b_p:b_{p+1}) (split-K: stage 2 and G generation divided
   by P), then Z = sum_p Z_p by all-reduce.  Communication is (P-1)/P * B*d*8 per rank.
+* ``"g"``: the partial sketches are all-reduced (every rank holds the summed S.X), rank p
+  computes rows [r_p, r_{p+1}) of Z = G[r_p:r_{p+1}, :] . S.X (cgx_gauss_gemm_rows: the
+  m rows of G split across ranks, stage 2 divided by P with no further reduction), and the
+  row blocks are all-gathered.  Z's rows are exact per rank (no cross-rank fp sum in
+  stage 2); communication is ~2 B*d*8 + m*d*8 per rank.
 
 The collectives go through ``torch.distributed`` (NCCL on the GPUs; gloo in the CPU
 tests).  Results equal the single-GPU T.X up to fp reassociation across ranks.
@@ -36,14 +41,27 @@ def bucket_range(B: int, world: int, rank: int) -> tuple[int, int]:
     return shard_range(B, world, rank)
 
 
+def g_row_range(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows of G (and of Z) computed by `rank` in the "g" combine: equal blocks of
+    ceil(m / world) (the all-gather needs equal chunks); trailing ranks may get fewer or none."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("g_row_range: need 0 <= rank < world")
+    per = (m + world - 1) // world
+    r0 = min(m, rank * per)
+    return r0, min(m, r0 + per)
+
+
 def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None, partial_z=None,
-            stage2: Optional[Callable] = None, group=None):
+            stage2: Optional[Callable] = None, m: Optional[int] = None, group=None):
     """Combine one rank's partial results into the full Z (every rank returns Z).
 
     mode "z":  partial_z (m x d) is all-reduced.
     mode "sx": partial_sx (B x d, row-major) is reduce-scattered by bucket range; the
                owned slice goes through stage2(sx_slice, b0, b1) -> Z_p (m x d), which is
                then all-reduced.
+    mode "g":  partial_sx (B x d, row-major) is all-reduced; stage2(sx, r0, r1) returns
+               rows [r0, r1) of Z ((r1-r0) x d) for g_row_range(m, world, rank), and the
+               row blocks are all-gathered into Z (m x d, row-major tensor).
     """
     import torch
     import torch.distributed as dist
@@ -51,8 +69,20 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
     if mode == "z":
         dist.all_reduce(partial_z, group=group)
         return partial_z
+    if mode == "g":
+        if m is None:
+            raise ValueError("combine: mode 'g' needs m")
+        dist.all_reduce(partial_sx, group=group)
+        r0, r1 = g_row_range(m, world, rank)
+        per = (m + world - 1) // world
+        blk = torch.zeros((per, d), dtype=partial_sx.dtype, device=partial_sx.device)
+        if r1 > r0:
+            blk[: r1 - r0] = stage2(partial_sx, r0, r1)
+        out = torch.empty((per * world, d), dtype=blk.dtype, device=blk.device)
+        dist.all_gather_into_tensor(out, blk, group=group)
+        return out[:m]
     if mode != "sx":
-        raise ValueError("combine: mode must be 'z' or 'sx'")
+        raise ValueError("combine: mode must be 'z', 'sx' or 'g'")
     # reduce_scatter_tensor needs equal chunks: pad B up to a multiple of world.
     per = (B + world - 1) // world
     flat = partial_sx.reshape(B, d)

@@ -1,7 +1,8 @@
 """CPU, world_size 2 over gloo: the multi-GPU host logic (paper_1606_05732_b200/distributed.py)
 -- contiguous row shards, per-rank transforms from the shared seed over *global* row
-indices, and both combine modes ("z": all-reduce of Z; "sx": bucket-range
-reduce-scatter of S.X, split-K stage 2, all-reduce) -- reproduces the single-device T.X.
+indices, and the three combine modes ("z": all-reduce of Z; "sx": bucket-range
+reduce-scatter of S.X, split-K stage 2, all-reduce; "g": all-reduce of S.X, G's m rows
+split over ranks, all-gather of Z's row blocks) -- reproduces the single-device T.X.
 The per-rank compute is the oracle here (no GPU); on the box it is libcgx."""
 import os
 import socket
@@ -13,7 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_1606_05732_b200.distributed import bucket_range, combine, shard_range
+from paper_1606_05732_b200.distributed import bucket_range, combine, g_row_range, shard_range
 
 N, D, B, M, SEED = 5003, 7, 67, 5, 424242
 
@@ -44,6 +45,12 @@ def _worker(rank, world, port, mode, out_path):
         G = O.gaussian(g_seed, M, B)
         z = torch.from_numpy(np.ascontiguousarray(O.gemm(G, sx_p)))
         z = combine("z", world=world, rank=rank, B=B, d=D, partial_z=z)
+    elif mode == "g":
+        def stage2_rows(sx, g0, g1):
+            G = O.gaussian(g_seed, M, B)  # rows [g0, g1) of G . S.X
+            return torch.from_numpy(np.ascontiguousarray(O.gemm(G[g0:g1], sx.numpy())))
+        z = combine("g", world=world, rank=rank, B=B, d=D, m=M,
+                    partial_sx=torch.from_numpy(np.ascontiguousarray(sx_p)), stage2=stage2_rows)
     else:
         def stage2(sx_slice, b0, b1):
             if b1 <= b0:
@@ -57,10 +64,11 @@ def _worker(rank, world, port, mode, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["z", "sx"])
-def test_two_rank_combine_matches_single_device(tmp_path, mode):
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", ["z", "sx", "g"])
+def test_multi_rank_combine_matches_single_device(tmp_path, mode, world):
     out = str(tmp_path / f"z_{mode}.npy")
-    mp.spawn(_worker, args=(2, _free_port(), mode, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), mode, out), nprocs=world, join=True)
     z = np.load(out)
     z_ref, _ = oracle.Restatement().countgauss(SEED, M, B, x=_problem())
     assert np.linalg.norm(z - z_ref) / np.linalg.norm(z_ref) <= 1e-13
@@ -74,5 +82,10 @@ def test_shard_ranges_cover_rows():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
     assert bucket_range(65536, 8, 7) == (57344, 65536)
+    for m in (1, 5, 64, 256):
+        for w in (1, 2, 3, 8):
+            spans = [g_row_range(m, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)

@@ -709,3 +709,24 @@ def test_row_shards_recompose(cg, restatement, world, g_mode):
                                        CGX_MEM_HOST, None))
         z_sx += zp
     assert rel_fro(z_sx, z_ref) <= Z_TOL
+    # "g" combine: G's m rows split over ranks, each block from the summed S.X
+    from paper_1606_05732_b200.distributed import g_row_range
+
+    z_g = np.zeros((m, d))
+    for rank in range(world):
+        g0, g1 = g_row_range(m, world, rank)
+        if g1 > g0:
+            z_g[g0:g1] = cg.api.gauss_gemm_rows(full, sx_sum, g0, g1)
+    assert rel_fro(z_g, z_ref) <= Z_TOL
+    # and the device-resident path with a row-major torch S.X
+    import torch
+
+    sx_dev = torch.from_numpy(np.ascontiguousarray(sx_sum)).cuda()
+    g0, g1 = g_row_range(m, world, 1)  # non-empty for every world here (m=12)
+    zr = cg.api.gauss_gemm_rows(full, sx_dev, g0, g1)
+    torch.cuda.synchronize()
+    assert rel_fro(zr.cpu().numpy(), z_g[g0:g1]) <= 1e-15
+    with pytest.raises(Exception):
+        cg.api.gauss_gemm_rows(full, sx_sum, 3, 3)
+    with pytest.raises(Exception):
+        cg.api.gauss_gemm_rows(full, sx_sum, 0, m + 1)
