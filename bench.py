@@ -257,9 +257,29 @@ def run_ours(args):
     r0, r1 = shard_range(n, world, rank)
     rows = r1 - r0
     t_seed = cg.SeededRng(SEED).next_u64()
+    hash_place = args.placement == "hash"
+    if hash_place and (c["kind"] != "dense" or args.combine != "z"):
+        raise SystemExit("--placement hash: dense configs and --combine z only")
 
     # inputs in HBM
-    if c["kind"] == "dense":
+    t_hash = None
+    if hash_place:
+        from paper_1606_05732_b200.distributed import bucket_range
+
+        b0, b1 = bucket_range(B, world, rank)
+        t0 = time.perf_counter()
+        t_hash = cg.api.countgauss_bucket_shard(m, B, n, b0, b1, t_seed, ctx=ctx)
+        torch.cuda.synchronize()
+        construct_hash_ms = (time.perf_counter() - t0) * 1e3
+        grows = cg.api.xform_rows(t_hash, device=dev)
+        rows = grows.numel()
+    if c["kind"] == "dense" and hash_place:
+        dt = torch.float32 if c["dtype"] == "f32" else torch.float64
+        x = bench_data.dense_normal_rows(grows, d, seed=mix64(SEED, 2), dtype=dt, device=local)
+        nnz_local = rows * d
+        x_bytes = rows * d * x.element_size()
+        del grows
+    elif c["kind"] == "dense":
         dt = torch.float32 if c["dtype"] == "f32" else torch.float64
         x = bench_data.dense_normal(rows, d, seed=mix64(SEED, 2), dtype=dt, row0=r0, device=local)
         nnz_local = rows * d
@@ -277,10 +297,13 @@ def run_ours(args):
 
     # transform construction (per-transform work, timed separately: the reference's
     # countgauss_new is likewise outside countgauss_apply)
-    t0 = time.perf_counter()
-    t = cg.api.countgauss_new_shard(m, B, n, r0, rows, t_seed, ctx=ctx)
-    torch.cuda.synchronize()
-    construct_ms = (time.perf_counter() - t0) * 1e3
+    if hash_place:
+        t, construct_ms = t_hash, construct_hash_ms
+    else:
+        t0 = time.perf_counter()
+        t = cg.api.countgauss_new_shard(m, B, n, r0, rows, t_seed, ctx=ctx)
+        torch.cuda.synchronize()
+        construct_ms = (time.perf_counter() - t0) * 1e3
 
     stream = torch.cuda.current_stream(dev)
     zbuf = torch.empty((d, m), dtype=torch.float64, device=dev)  # contiguous storage of Z^T
@@ -288,7 +311,8 @@ def run_ours(args):
 
     from paper_1606_05732_b200.distributed import combine
 
-    sxbuf = torch.empty((B, d), dtype=torch.float64, device=dev) if world > 1 and args.combine != "z" else None
+    sxbuf = torch.empty((B, d), dtype=torch.float64, device=dev) if world > 1 and args.combine in ("sx", "g") else None
+    sxT = torch.empty((d, B), dtype=torch.float64, device=dev) if world > 1 and args.combine == "cols" else None
 
     def step():
         if world == 1 or args.combine == "z":
@@ -296,6 +320,10 @@ def run_ours(args):
             if world > 1:
                 dist.all_reduce(zbuf)  # partial Z of every row shard -> full Z on every rank
             return z
+        if args.combine == "cols":
+            cg.api.countsketch_apply_into(t, x, sxT.t())  # partial S.X, column-major
+            return combine("cols", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxT,
+                           stage2=lambda blk, c0, c1: cg.api.gauss_gemm(t, blk.t()).t())
         cg.api.countsketch_apply_into(t, x, sxbuf)  # partial S.X (row-major B x d)
         if args.combine == "sx":
             return combine("sx", world=world, rank=rank, B=B, d=d, partial_sx=sxbuf,
@@ -431,10 +459,15 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": workload_name(args.config, c), "n": n, "d": d, "B": B, "m": m,
-                "rows_per_rank": rows, "nnz_per_rank": int(nnz_local), "mean_row_nnz": nnz_local / rows, "parallelism": f"rows sharded x{world} ({args.scaling} scaling: "
+                "rows_per_rank": rows, "nnz_per_rank": int(nnz_local), "mean_row_nnz": nnz_local / rows,
+                "placement": ("hash: each rank holds the rows hashing into its bucket range, in (bucket, row) order "
+                              "(SURVEY 8e ablation C): the sketch reads X sequentially, S.X slices are final, stage 2 "
+                              "is split-K over G[:, b0:b1)") if hash_place else "rows: contiguous row shards",
+                "parallelism": f"rows sharded x{world} ({args.scaling} scaling: "
                 + ("the config's n rows per rank" if args.scaling == "weak" else "the config's n rows split across ranks")
                 + ")" + ({"z": ", NCCL all-reduce of Z", "sx": ", NCCL reduce-scatter of S.X + split-K stage 2 + all-reduce of Z",
-                       "g": ", NCCL all-reduce of S.X + G's m rows split over ranks + all-gather of Z"}[args.combine]
+                       "g": ", NCCL all-reduce of S.X + G's m rows split over ranks + all-gather of Z",
+                       "cols": ", NCCL column reduce-scatter of S.X + split-N stage 2 + all-gather of Z"}[args.combine]
                       if world > 1 else ""),
                 "input_dtype": c.get("dtype", "f32"), "accumulate": "f64 (S.X and G.(S.X))",
                 "l2": f"inputs larger than L2 ({x_bytes / 1e9:.2f} GB X per rank), no flush",
@@ -474,9 +507,13 @@ def main():
                     help="weak: each rank sketches the config's n rows (X has N*n rows); strong: n split N ways")
     ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
                     help="cgx_set_option before timing (A/B of kernel variants)")
-    ap.add_argument("--combine", default="z", choices=["z", "sx", "g"],
+    ap.add_argument("--placement", default="rows", choices=["rows", "hash"],
+                    help="rows: contiguous row shards; hash: each rank holds the rows hashing into its bucket "
+                         "range, in bucket order (SURVEY 8e ablation C; dense configs; combine = all-reduce of Z)")
+    ap.add_argument("--combine", default="z", choices=["z", "sx", "g", "cols"],
                     help="N>1 combine: z = all-reduce of Z; sx = reduce-scatter of S.X + split-K stage 2 + "
-                         "all-reduce; g = all-reduce of S.X + G's m rows split over ranks + all-gather")
+                         "all-reduce; g = all-reduce of S.X + G's m rows split over ranks + all-gather; "
+                         "cols = column reduce-scatter of S.X + split-N stage 2 + all-gather")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3", file=sys.stderr)

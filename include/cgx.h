@@ -178,6 +178,19 @@ int cgx_countsketch_batch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_
                                const double* u, int64_t ld, int64_t n, int64_t d, int u_mem, double* su,
                                double* gram, int out_mem, void* stream);
 
+/* Hash-partitioned row placement (SURVEY 8e ablation C): buckets [b0, b1) of
+ * countgauss_new(t_seed, m, buckets, input_dim) as a transform of their own.  Its rows are
+ * the full transform's rows hashing into [b0, b1), in (bucket, global row) order -- a rank
+ * that holds exactly those rows, in that order, sketches them with a sequential read and
+ * no reduction: S.X of the shard = rows [b0, b1) of the full S.X (bit-identical), and its
+ * G is G[:, b0:b1), so countgauss_apply gives the split-K partial Z_p (sum over ranks = Z).
+ * cgx_xform_info reports buckets = b1-b0 and input_dim = the shard's row count. */
+int cgx_countgauss_bucket_shard(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
+                                int64_t b0, int64_t b1, cgx_xform** out);
+/* Global row index of each local row of a transform (input_dim entries): a bucket shard's
+ * row list, or row0 + k for row shards and ordinary transforms. */
+int cgx_xform_rows(cgx_ctx* ctx, const cgx_xform* xf, int64_t* rows, int mem, void* stream);
+
 /* Split of G's m rows across ranks (north star's multi-GPU final product):
  * z = G[r0:r1, :] . sx -- (r1-r0) x d column-major -- with sx the full row-major B x d S.X
  * (e.g. after an all-reduce of the partial sketches). */
@@ -203,6 +216,10 @@ int cgx_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d, int
  * (oracle/cgoracle.c cgo_normal_f32); dtype F64 stores the exact widening. */
 int cgx_gen_dense_normal(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype,
                          int layout, void* x_dev, void* stream); /* rows [row0, row0+n) */
+/* The same values for an arbitrary list of n global rows (device int64 array): the rows of
+ * a bucket-shard transform (cgx_xform_rows). */
+int cgx_gen_dense_normal_rows(cgx_ctx* ctx, uint64_t seed, const int64_t* rows_dev, int64_t n, int64_t d,
+                              int dtype, int layout, void* x_dev, void* stream);
 /* CSR n x d with Bernoulli(density) entries (int32 cols, fp32 N(0,1) values).  Call once
  * with cols/vals NULL to get row offsets and *nnz_out, then again with buffers. */
 int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double density,

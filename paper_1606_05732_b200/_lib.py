@@ -40,6 +40,9 @@ SIGNATURES = {
     "cgx_countgauss_new_shard": (_I, [_P, _U64, _I64, _I64, _I64, _I64, _I64, _P]),
     "cgx_gauss_gemm_range": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _P, _I, _P]),
     "cgx_gauss_gemm_rows": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _P, _I, _P]),
+    "cgx_countgauss_bucket_shard": (_I, [_P, _U64, _I64, _I64, _I64, _I64, _I64, _P]),
+    "cgx_xform_rows": (_I, [_P, _P, _P, _I, _P]),
+    "cgx_gen_dense_normal_rows": (_I, [_P, _U64, _P, _I64, _I64, _I, _I, _P, _P]),
     "cgx_xform_set_gaussian_seeded": (_I, [_P, _P, _I64, _U64]),
     "cgx_xform_set_gaussian_explicit": (_I, [_P, _P, _I64, _P, _I]),
     "cgx_xform_info": (_I, [_P, _P, _P, _P, _P, _P, _P]),

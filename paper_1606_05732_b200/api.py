@@ -307,6 +307,38 @@ def countgauss_new_shard(m: int, buckets: int, input_dim: int, row0: int, rows: 
     return CountGaussTransform(_Xform(ctx, h))
 
 
+def countgauss_bucket_shard(m: int, buckets: int, input_dim: int, b0: int, b1: int, t_seed: int,
+                            ctx: Optional[Context] = None) -> CountGaussTransform:
+    """Buckets [b0, b1) of countgauss_new(m, buckets, input_dim, .) with t.seed `t_seed`, as
+    their own transform (hash-partitioned row placement, SURVEY 8e ablation C): its rows are
+    the rows hashing into [b0, b1), in (bucket, row) order (``rows()``), its S.X is rows
+    [b0, b1) of the full S.X and its G is G[:, b0:b1), so its apply is the split-K partial Z."""
+    if m < 1 or buckets < 1 or input_dim < 1:
+        raise ValueError("countgauss_new: m, buckets and input_dim must be >= 1")
+    ctx = ctx or context()
+    h = C.c_void_p()
+    check(lib.cgx_countgauss_bucket_shard(ctx.h, t_seed & _MASK, int(m), int(buckets), int(input_dim), int(b0),
+                                          int(b1), C.byref(h)))
+    return CountGaussTransform(_Xform(ctx, h))
+
+
+def xform_rows(t, device=None):
+    """Global row index of each of the transform's rows (int64): numpy, or a CUDA tensor
+    when `device` is given."""
+    xf = (t.cs if isinstance(t, CountGaussTransform) else t)._xf
+    n = xf.info()["n"]
+    if device is not None:
+        import torch
+
+        rows = torch.empty(n, dtype=torch.int64, device=device)
+        check(lib.cgx_xform_rows(xf.ctx.h, xf.h, rows.data_ptr(), CGX_MEM_DEVICE,
+                                 C.c_void_p(torch.cuda.current_stream(rows.device).cuda_stream or 1)))
+        return rows
+    rows = np.empty(n, np.int64)
+    check(lib.cgx_xform_rows(xf.ctx.h, xf.h, rows.ctypes.data, CGX_MEM_HOST, None))
+    return rows
+
+
 # ------------------------------------------------------------------------ matrices
 def _to_host(a):
     if _is_torch(a):
@@ -577,6 +609,44 @@ def _sx_rows_args(sx):
         return sx.data_ptr(), sx.shape[1], CGX_MEM_DEVICE, sx, True
     sx = np.ascontiguousarray(sx, dtype=np.float64)
     return sx.ctypes.data, sx.shape[1], CGX_MEM_HOST, sx, False
+
+
+def gauss_gemm(t: CountGaussTransform, sx, z=None):
+    """Stage 2 alone, Z = G . sx for a buckets x d S.X (numpy or CUDA torch, row- or
+    column-major, packed); m x d column-major (into `z` when given).  With a column block
+    of S.X this is the "cols" combine's split-N piece."""
+    xf = t._xf
+    if _is_torch(sx) and sx.is_cuda:
+        import torch
+
+        sx = sx.to(torch.float64)
+        if sx.dim() != 2 or sx.shape[0] != t.cs.buckets:
+            raise ValueError("gauss_gemm: sx must be buckets x d")
+        if sx.stride(0) == 1 and sx.t().is_contiguous():
+            layout = CGX_COL_MAJOR
+        else:
+            sx = sx.contiguous()
+            layout = CGX_ROW_MAJOR
+        mem, keep, dev = CGX_MEM_DEVICE, sx, True
+        ptr = sx.data_ptr()
+    else:
+        sx = np.asarray(sx.numpy() if _is_torch(sx) else sx, dtype=np.float64)
+        if sx.ndim != 2 or sx.shape[0] != t.cs.buckets:
+            raise ValueError("gauss_gemm: sx must be buckets x d")
+        if sx.flags.f_contiguous:
+            layout = CGX_COL_MAJOR
+        else:
+            sx = np.ascontiguousarray(sx)
+            layout = CGX_ROW_MAJOR
+        mem, keep, dev = CGX_MEM_HOST, sx, False
+        ptr = sx.ctypes.data
+    d = sx.shape[1]
+    if z is None:
+        z, zptr = _out(t.m, d, dev, keep)
+    else:
+        zptr = z.data_ptr()
+    check(lib.cgx_gauss_gemm(xf.ctx.h, xf.h, ptr, layout, d, mem, zptr, mem, _stream_of(keep) if dev else None))
+    return z
 
 
 def gauss_gemm_range(t: CountGaussTransform, sx_rows, b0: int, b1: int, z=None):

@@ -34,6 +34,23 @@ def dense_normal(n: int, d: int, seed: int, dtype=None, layout: str = "row", dev
     return x
 
 
+def dense_normal_rows(rows, d: int, seed: int, dtype=None, device=None):
+    """dense_normal's values for an arbitrary list of global rows (a CUDA int64 tensor, e.g.
+    api.xform_rows of a bucket shard), row-major len(rows) x d."""
+    import torch
+
+    dtype = dtype or torch.float32
+    ctx = context(device)
+    dev = torch.device("cuda", ctx.device)
+    rows = rows.to(device=dev, dtype=torch.int64).contiguous()
+    n = rows.numel()
+    x = torch.empty((n, d), dtype=dtype, device=dev)
+    dt = CGX_F32 if dtype == torch.float32 else CGX_F64
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream or 1)
+    check(lib.cgx_gen_dense_normal_rows(ctx.h, seed, rows.data_ptr(), n, d, dt, CGX_ROW_MAJOR, x.data_ptr(), stream))
+    return x
+
+
 def csr_zipf(n: int, d: int, seed: int, s_len: float = 1.5, cap: int = 512, s_col: float = 1.1, device=None):
     """Config-5 style heavy-tailed CSR (see cgx_gen_csr_zipf): Zipf(s_len) target row
     lengths capped at `cap`, Zipf(s_col)-skewed columns, fp32 N(0,1) values."""

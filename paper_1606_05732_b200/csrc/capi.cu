@@ -197,6 +197,7 @@ void free_xform(cgx_xform* xf) {
     cudaDeviceSynchronize();
     pool_free(xf->ctx, xf->perm);
     pool_free(xf->ctx, xf->offsets);
+    pool_free(xf->ctx, xf->grows);
     drop_g(xf);
     delete xf;
 }
@@ -581,6 +582,71 @@ int cgx_countgauss_new_shard(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t b
             throw;
         }
         *out = xf;
+    });
+}
+
+int cgx_countgauss_bucket_shard(cgx_ctx* ctx, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
+                                int64_t b0, int64_t b1, cgx_xform** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (m < 1 || buckets < 1 || input_dim < 1)
+            fail(CGX_EINVAL, "countgauss_new: m, buckets and input_dim must be >= 1");
+        if (b0 < 0 || b1 <= b0 || b1 > buckets)
+            fail(CGX_EINVAL, "countgauss_bucket_shard: need 0 <= b0 < b1 <= buckets");
+        CallScope sc(ctx, nullptr);
+        // the full map (rows of every bucket, seeded), then its bucket range as a transform
+        cgx_xform* full = new_xform(ctx, buckets, input_dim);
+        cgx_xform* xf = nullptr;
+        try {
+            full->t_seed = t_seed;
+            full->map_seed = rng_draw(mix64(t_seed, 1), 0);
+            full->g_seed = mix64(t_seed, 2);
+            full->m = m;
+            full->has_g = true;
+            build_perm_seeded(ctx, full, sc.st);
+            uint32_t o[2];
+            CGX_CUDA(cudaMemcpyAsync(&o[0], full->offsets + b0, 4, cudaMemcpyDeviceToHost, sc.st));
+            CGX_CUDA(cudaMemcpyAsync(&o[1], full->offsets + b1, 4, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+            const int64_t count = (int64_t)o[1] - (int64_t)o[0];
+            if (count < 1) fail(CGX_EINVAL, "countgauss_bucket_shard: no rows hash into the bucket range");
+            xf = new_xform(ctx, b1 - b0, count);
+            xf->grows = (uint32_t*)pool_alloc(ctx, sizeof(uint32_t) * (size_t)count);
+            xf->t_seed = t_seed;
+            xf->map_seed = full->map_seed;
+            xf->g_seed = full->g_seed;
+            xf->seeded_map = false;
+            xf->m = m;
+            xf->has_g = true;
+            launch_bucket_shard(ctx, full, b0, b1 - b0, o[0], xf, sc.st);
+            // G[:, b0:b1) of the full transform, held like an explicit G
+            CGX_CUDA(cudaMalloc((void**)&xf->g_dev, sizeof(double) * (size_t)(m * (b1 - b0))));
+            xf->g_explicit = true;
+            launch_gen_gauss(ctx, full, b0, b1 - b0, xf->g_dev, sc.st);
+            sc.sync();
+        } catch (...) {
+            free_xform(xf);
+            free_xform(full);
+            throw;
+        }
+        free_xform(full);
+        *out = xf;
+    });
+}
+
+int cgx_xform_rows(cgx_ctx* ctx, const cgx_xform* xf, int64_t* rows, int mem, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(mem);
+        CallScope sc(ctx, stream);
+        const size_t bytes = sizeof(int64_t) * (size_t)xf->n;
+        int64_t* rd = mem == CGX_MEM_HOST ? (int64_t*)ctx->xstage.get(bytes) : rows;
+        launch_xform_rows(ctx, xf, rd, sc.st);
+        if (mem == CGX_MEM_HOST) {
+            CGX_CUDA(cudaMemcpyAsync(rows, rd, bytes, cudaMemcpyDeviceToHost, sc.st));
+            sc.sync();
+        }
     });
 }
 
@@ -1073,7 +1139,20 @@ int cgx_gen_dense_normal(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, i
         if (n * d == 0) return;
         CallScope sc(ctx, stream);
         if (row0 < 0) fail(CGX_EINVAL, "cgx_gen_dense_normal: negative row0");
-        launch_gen_dense(ctx, seed, row0, n, d, dtype, layout, x_dev, sc.st);
+        launch_gen_dense(ctx, seed, row0, nullptr, n, d, dtype, layout, x_dev, sc.st);
+    });
+}
+
+int cgx_gen_dense_normal_rows(cgx_ctx* ctx, uint64_t seed, const int64_t* rows_dev, int64_t n, int64_t d, int dtype,
+                              int layout, void* x_dev, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        dsize(dtype);
+        if (n < 0 || d < 0) fail(CGX_EINVAL, "cgx_gen_dense_normal_rows: negative size");
+        if (n * d == 0) return;
+        if (!rows_dev) fail(CGX_EINVAL, "cgx_gen_dense_normal_rows: null rows");
+        CallScope sc(ctx, stream);
+        launch_gen_dense(ctx, seed, 0, rows_dev, n, d, dtype, layout, x_dev, sc.st);
     });
 }
 

@@ -248,6 +248,42 @@ bool prep_explicit(cgx_ctx* ctx, const int64_t* hash, const double* sign, int64_
     return hbad == 0;
 }
 
+namespace {
+__global__ void bucket_shard_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ offsets,
+                                    int64_t b0, int64_t nb, uint32_t o0, int64_t count, uint32_t* __restrict__ perm_l,
+                                    uint32_t* __restrict__ offsets_l, uint32_t* __restrict__ grows) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride) {
+        const uint32_t pe = perm[o0 + k];
+        perm_l[k] = (uint32_t)k | (pe & kNegBit);
+        grows[k] = pe & kRowMask;
+    }
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= nb; j += stride)
+        offsets_l[j] = offsets[b0 + j] - o0;
+}
+} // namespace
+
+void launch_bucket_shard(cgx_ctx* ctx, const cgx_xform* full, int64_t b0, int64_t nb, uint32_t o0, cgx_xform* local,
+                         cudaStream_t s) {
+    bucket_shard_kernel<<<ctx->num_sms * 8, 256, 0, s>>>(full->perm, full->offsets, b0, nb, o0, local->n, local->perm,
+                                                         local->offsets, local->grows);
+    count_launch(ctx);
+    check_launch("bucket_shard");
+}
+
+namespace {
+__global__ void xform_rows_kernel(const uint32_t* __restrict__ grows, int64_t row0, int64_t n, int64_t* __restrict__ rows) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        rows[k] = grows ? (int64_t)grows[k] : row0 + k;
+}
+} // namespace
+
+void launch_xform_rows(cgx_ctx* ctx, const cgx_xform* xf, int64_t* rows, cudaStream_t s) {
+    xform_rows_kernel<<<ctx->num_sms * 4, 256, 0, s>>>(xf->grows, xf->row0, xf->n, rows);
+    count_launch(ctx);
+    check_launch("xform_rows");
+}
+
 void launch_fill_hash_sign(cgx_ctx* ctx, const cgx_xform* xf, int64_t* hash, double* sign, cudaStream_t s) {
     const int64_t threads = xf->B * 32;
     fill_hash_sign_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(xf->perm, xf->offsets, xf->B, hash, sign);

@@ -18,7 +18,8 @@ namespace cgx {
 namespace {
 
 template <typename T>
-__global__ void gen_dense_kernel(uint64_t seed, int64_t row0, int64_t n, int64_t d, int layout, T* x) {
+__global__ void gen_dense_kernel(uint64_t seed, int64_t row0, const int64_t* __restrict__ rows, int64_t n, int64_t d,
+                                 int layout, T* x) {
     const int64_t total = n * d;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         // e enumerates the destination in its own layout for coalesced stores
@@ -30,7 +31,8 @@ __global__ void gen_dense_kernel(uint64_t seed, int64_t row0, int64_t n, int64_t
             j = e / n;
             i = e - j * n;
         }
-        x[e] = (T)datagen_normal(seed, (uint64_t)((row0 + i) * d + j));
+        const int64_t gi = rows ? rows[i] : row0 + i;  // global row: the value is a function of (row, column)
+        x[e] = (T)datagen_normal(seed, (uint64_t)(gi * d + j));
     }
 }
 
@@ -101,13 +103,13 @@ __global__ void gen_csr_fill_kernel(uint64_t mseed, uint64_t vseed, int64_t n, i
 
 } // namespace
 
-void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype, int layout, void* x,
-                      cudaStream_t s) {
+void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, const int64_t* rows, int64_t n, int64_t d, int dtype,
+                      int layout, void* x, cudaStream_t s) {
     const int blocks = ctx->num_sms * 16;
     if (dtype == CGX_F32)
-        gen_dense_kernel<float><<<blocks, 256, 0, s>>>(seed, row0, n, d, layout, (float*)x);
+        gen_dense_kernel<float><<<blocks, 256, 0, s>>>(seed, row0, rows, n, d, layout, (float*)x);
     else
-        gen_dense_kernel<double><<<blocks, 256, 0, s>>>(seed, row0, n, d, layout, (double*)x);
+        gen_dense_kernel<double><<<blocks, 256, 0, s>>>(seed, row0, rows, n, d, layout, (double*)x);
     count_launch(ctx);
     check_launch("gen_dense");
 }

@@ -92,6 +92,7 @@ struct cgx_xform {
     bool g_pool = false;           // g_dev is a resident copy from the pool (else cudaMalloc'd explicit G)
     uint32_t* perm = nullptr;      // n entries: row | neg<<31, sorted by (bucket, row)
     uint32_t* offsets = nullptr;   // B+1 bucket boundaries into perm
+    uint32_t* grows = nullptr;     // bucket-shard transforms: global row index of each local row
 };
 
 namespace cgx {
@@ -103,6 +104,12 @@ void build_perm_explicit(cgx_ctx* ctx, cgx_xform* xf, const uint32_t* keys_dev, 
 bool prep_explicit(cgx_ctx* ctx, const int64_t* hash, const double* sign, int64_t n, int64_t B, uint32_t* keys,
                    uint32_t* vals, cudaStream_t s);
 void launch_fill_hash_sign(cgx_ctx* ctx, const cgx_xform* xf, int64_t* hash, double* sign, cudaStream_t s);
+// Buckets [b0, b0+nb) of `full` as their own transform: local rows = the full transform's
+// rows of those buckets in (bucket, row) order, so local perm is the identity (+ signs).
+// global row index of each local row (bucket shards: grows; row shards: row0 + k)
+void launch_xform_rows(cgx_ctx* ctx, const cgx_xform* xf, int64_t* rows, cudaStream_t s);
+void launch_bucket_shard(cgx_ctx* ctx, const cgx_xform* full, int64_t b0, int64_t nb, uint32_t o0, cgx_xform* local,
+                         cudaStream_t s);
 
 // sketch_dense.cu: SX (row-major B x d, fp64) from row-major X.
 void launch_sketch_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int64_t ld, int64_t n,
@@ -162,7 +169,8 @@ void launch_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d,
                             int64_t* tie_flags, cudaStream_t s);
 
 // datagen.cu
-void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int dtype, int layout, void* x,
+void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, const int64_t* rows, int64_t n, int64_t d, int dtype,
+                      int layout, void* x,
                       cudaStream_t s);
 struct CsrGenSpec {
     bool zipf = false;

@@ -17,6 +17,10 @@ T.X is linear, so the partials combine after either stage:
   m rows of G split across ranks, stage 2 divided by P with no further reduction), and the
   row blocks are all-gathered.  Z's rows are exact per rank (no cross-rank fp sum in
   stage 2); communication is ~2 B*d*8 + m*d*8 per rank.
+* ``"cols"``: the column-range alternative.  The partial sketches are column-major, so a
+  reduce-scatter hands rank p columns [c_p, c_{p+1}) of the summed S.X; rank p computes
+  Z[:, c_p:c_{p+1}) = G . S.X[:, c_p:c_{p+1}) (split-N: all of G on every rank, stage 2
+  divided by P) and the column blocks are all-gathered.
 
 The collectives go through ``torch.distributed`` (NCCL on the GPUs; gloo in the CPU
 tests).  Results equal the single-GPU T.X up to fp reassociation across ranks.
@@ -62,7 +66,13 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
     mode "g":  partial_sx (B x d, row-major) is all-reduced; stage2(sx, r0, r1) returns
                rows [r0, r1) of Z ((r1-r0) x d) for g_row_range(m, world, rank), and the
                row blocks are all-gathered into Z (m x d, row-major tensor).
+    mode "cols": partial_sx is a contiguous (d, B) tensor (S.X column-major); columns are
+               reduce-scattered, stage2(sx_cols, c0, c1) gets the (c1-c0, B) block and
+               returns Z[:, c0:c1) transposed ((c1-c0) x m); the blocks are all-gathered
+               into Z (m x d, column-major view).
     """
+    if mode in ("g", "cols") and m is None:
+        raise ValueError(f"combine: mode '{mode}' needs m")
     import torch
     import torch.distributed as dist
 
@@ -70,8 +80,6 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
         dist.all_reduce(partial_z, group=group)
         return partial_z
     if mode == "g":
-        if m is None:
-            raise ValueError("combine: mode 'g' needs m")
         dist.all_reduce(partial_sx, group=group)
         r0, r1 = g_row_range(m, world, rank)
         per = (m + world - 1) // world
@@ -81,8 +89,25 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
         out = torch.empty((per * world, d), dtype=blk.dtype, device=blk.device)
         dist.all_gather_into_tensor(out, blk, group=group)
         return out[:m]
+    if mode == "cols":
+        # partial_sx: B x d column-major, i.e. a contiguous (d, B) tensor of S.X columns
+        per = (d + world - 1) // world
+        flat = partial_sx.reshape(d, B)
+        if per * world != d:
+            pad = torch.zeros((per * world - d, B), dtype=flat.dtype, device=flat.device)
+            flat = torch.cat([flat, pad], 0)
+        out = torch.empty((per, B), dtype=flat.dtype, device=flat.device)
+        dist.reduce_scatter_tensor(out, flat.contiguous(), group=group)
+        c0 = min(d, rank * per)
+        c1 = min(d, c0 + per)
+        zt = torch.zeros((per, m), dtype=flat.dtype, device=flat.device)  # Z[:, c0:c1) transposed
+        if c1 > c0:
+            zt[: c1 - c0] = stage2(out[: c1 - c0], c0, c1)
+        gathered = torch.empty((per * world, m), dtype=zt.dtype, device=zt.device)
+        dist.all_gather_into_tensor(gathered, zt, group=group)
+        return gathered[:d].t()  # m x d, column-major view
     if mode != "sx":
-        raise ValueError("combine: mode must be 'z', 'sx' or 'g'")
+        raise ValueError("combine: mode must be 'z', 'sx', 'g' or 'cols'")
     # reduce_scatter_tensor needs equal chunks: pad B up to a multiple of world.
     per = (B + world - 1) // world
     flat = partial_sx.reshape(B, d)

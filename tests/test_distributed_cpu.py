@@ -2,7 +2,9 @@
 -- contiguous row shards, per-rank transforms from the shared seed over *global* row
 indices, and the three combine modes ("z": all-reduce of Z; "sx": bucket-range
 reduce-scatter of S.X, split-K stage 2, all-reduce; "g": all-reduce of S.X, G's m rows
-split over ranks, all-gather of Z's row blocks) -- reproduces the single-device T.X.
+split over ranks, all-gather of Z's row blocks; "cols": column-range reduce-scatter of
+S.X, split-N stage 2, all-gather of Z's column blocks; "hash": hash-partitioned row
+placement, final S.X slices, split-K stage 2, all-reduce of Z) -- reproduces the single-device T.X.
 The per-rank compute is the oracle here (no GPU); on the box it is libcgx."""
 import os
 import socket
@@ -39,6 +41,21 @@ def _worker(rank, world, port, mode, out_path):
     x = _problem()
     r0, r1 = shard_range(N, world, rank)
     _, cs_seed, g_seed = O.countgauss_seeds(SEED)
+    if mode == "hash":
+        # hash-partitioned placement (ablation C): this rank holds the rows hashing into its
+        # bucket range, in (bucket, row) order; its S.X slice is final, stage 2 is split-K
+        b0, b1 = bucket_range(B, world, rank)
+        h_all, s_all = O.hash_sign(cs_seed, B, N)
+        rows = np.nonzero((h_all >= b0) & (h_all < b1))[0]
+        rows = rows[np.lexsort((rows, h_all[rows]))]
+        sx_p = O.sketch_dense(h_all[rows] - b0, s_all[rows], b1 - b0, x[rows])
+        Gs = O.gaussian(g_seed, M, b1 - b0, c0=b0)
+        z = torch.from_numpy(np.ascontiguousarray(O.gemm(Gs, sx_p)))
+        z = combine("z", world=world, rank=rank, B=B, d=D, partial_z=z)
+        if rank == 0:
+            np.save(out_path, z.numpy())
+        dist.destroy_process_group()
+        return
     h, s = O.hash_sign(cs_seed, B, r1 - r0, i0=r0)  # global row indices, shared seed
     sx_p = O.sketch_dense(h, s, B, x[r0:r1])  # (B, D) partial
     if mode == "z":
@@ -51,6 +68,14 @@ def _worker(rank, world, port, mode, out_path):
             return torch.from_numpy(np.ascontiguousarray(O.gemm(G[g0:g1], sx.numpy())))
         z = combine("g", world=world, rank=rank, B=B, d=D, m=M,
                     partial_sx=torch.from_numpy(np.ascontiguousarray(sx_p)), stage2=stage2_rows)
+    elif mode == "cols":
+        G = O.gaussian(g_seed, M, B)
+
+        def stage2_cols(sx_cols, c0, c1):  # (c1-c0, B) block of S.X columns -> Z[:, c0:c1)^T
+            return torch.from_numpy(np.ascontiguousarray(O.gemm(G, sx_cols.numpy().T).T))
+        z = combine("cols", world=world, rank=rank, B=B, d=D, m=M,
+                    partial_sx=torch.from_numpy(np.ascontiguousarray(sx_p.T)), stage2=stage2_cols)
+        z = z.contiguous()
     else:
         def stage2(sx_slice, b0, b1):
             if b1 <= b0:
@@ -65,7 +90,7 @@ def _worker(rank, world, port, mode, out_path):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("mode", ["z", "sx", "g"])
+@pytest.mark.parametrize("mode", ["z", "sx", "g", "cols", "hash"])
 def test_multi_rank_combine_matches_single_device(tmp_path, mode, world):
     out = str(tmp_path / f"z_{mode}.npy")
     mp.spawn(_worker, args=(world, _free_port(), mode, out), nprocs=world, join=True)

@@ -726,7 +726,65 @@ def test_row_shards_recompose(cg, restatement, world, g_mode):
     zr = cg.api.gauss_gemm_rows(full, sx_dev, g0, g1)
     torch.cuda.synchronize()
     assert rel_fro(zr.cpu().numpy(), z_g[g0:g1]) <= 1e-15
+    # "cols" combine: column blocks of S.X through stage 2 (split-N), host and device
+    z_c = np.zeros((m, d))
+    for rank in range(world):
+        per = (d + world - 1) // world
+        c0, c1 = min(d, rank * per), min(d, rank * per + per)
+        if c1 > c0:
+            z_c[:, c0:c1] = cg.api.gauss_gemm(full, np.asfortranarray(sx_sum[:, c0:c1]))
+    assert rel_fro(z_c, z_ref) <= Z_TOL
+    sxT = torch.from_numpy(np.ascontiguousarray(sx_sum.T)).cuda()  # (d, B): S.X column-major
+    zc_dev = cg.api.gauss_gemm(full, sxT[: d // 2].t())
+    torch.cuda.synchronize()
+    assert np.array_equal(zc_dev.cpu().numpy(), z_c[:, : d // 2]) or rel_fro(zc_dev.cpu().numpy(), z_c[:, : d // 2]) <= 1e-15
     with pytest.raises(Exception):
         cg.api.gauss_gemm_rows(full, sx_sum, 3, 3)
     with pytest.raises(Exception):
         cg.api.gauss_gemm_rows(full, sx_sum, 0, m + 1)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_bucket_shards_hash_placement(cg, restatement, world):
+    """SURVEY 8e ablation C (hash-partitioned row placement): the bucket-range transform
+    (cgx_countgauss_bucket_shard) holds exactly the rows hashing into [b0, b1) in (bucket,
+    row) order, its hash/sign/G are the full transform's restricted to them, its S.X of
+    X[rows] is rows [b0, b1) of the full S.X bit-for-bit, and the shards' applies sum to Z."""
+    import torch
+
+    from paper_1606_05732_b200 import bench_data
+    from paper_1606_05732_b200.distributed import bucket_range
+
+    n, d, B, m, seed = 30011, 20, 1009, 12, 777
+    x = np.random.default_rng(world).standard_normal((n, d))
+    full = cg.countgauss_new(m, B, n, cg.SeededRng(seed))
+    z_ref, sx_ref = restatement.countgauss(seed, m, B, x=x)
+    h_full, s_full, g_full = full.cs.hash, full.cs.sign, full.g
+    z_sum = np.zeros((m, d))
+    seen = []
+    for rank in range(world):
+        b0, b1 = bucket_range(B, world, rank)
+        t = cg.api.countgauss_bucket_shard(m, B, n, b0, b1, full.seed)
+        rows = cg.api.xform_rows(t)
+        want = np.nonzero((h_full >= b0) & (h_full < b1))[0]
+        want = want[np.lexsort((want, h_full[want]))]  # (bucket, row) order
+        assert np.array_equal(rows, want)
+        seen.append(rows)
+        assert t.cs.buckets == b1 - b0 and t.cs.input_dim == len(rows)
+        assert np.array_equal(t.cs.hash, h_full[rows] - b0) and np.array_equal(t.cs.sign, s_full[rows])
+        assert np.array_equal(t.g, g_full[:, b0:b1])
+        xs = np.ascontiguousarray(x[rows])
+        assert np.array_equal(cg.countsketch_apply(t, xs), sx_ref[b0:b1])
+        z_sum += cg.countgauss_apply(t, xs)
+        # the same rows, generated on the device from their global indices
+        rows_dev = cg.api.xform_rows(t, device="cuda")
+        xg = bench_data.dense_normal_rows(rows_dev, 8, seed=99)
+        xa = bench_data.dense_normal(n, 8, seed=99)
+        torch.cuda.synchronize()
+        assert torch.equal(xg, xa[rows_dev])
+    assert np.array_equal(np.sort(np.concatenate(seen)), np.arange(n))
+    assert rel_fro(z_sum, z_ref) <= Z_TOL
+    with pytest.raises(ValueError):
+        cg.api.countgauss_bucket_shard(m, B, n, 5, 5, full.seed)
+    with pytest.raises(ValueError):
+        cg.api.countgauss_bucket_shard(m, B, n, 0, B + 1, full.seed)
