@@ -330,6 +330,10 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     // split-K CTA a read-modify-write of its partial tile.)
     int64_t S = (48ll << 20) / (8 * m);
     S = S < BK ? BK : S / BK * BK;
+    // G already in memory: one pass over all of K (no per-chunk ramp, tail and partial
+    // read-modify-write; the tiles of a split run concurrently, so their G and S.X slices
+    // are shared through L2)
+    if ((gready || xf->g_dev) && ctx->opt_gemm_chunks == 0) S = K;
     if (S > K) S = (K + BK - 1) / BK * BK;
     const int64_t tm = (m + BM - 1) / BM, tn = (d + BN - 1) / BN;
     const int64_t resident = (int64_t)ctx->num_sms * (FM * FN > 16 ? 1 : (NT <= 256 ? 512 / NT : 1));  // CTAs per wave
