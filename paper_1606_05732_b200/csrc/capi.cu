@@ -1210,6 +1210,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_g_resident = value;
         else if (k == "gemm_ws" && (value == 0 || value == 1))
             ctx->opt_gemm_ws = value;
+        else if (k == "gemm_tile" && (value == 0 || value == 1))
+            ctx->opt_gemm_tile = value;
         else if (k == "gemm_chunks" && (value == 0 || value == 1))
             ctx->opt_gemm_chunks = value;
         else

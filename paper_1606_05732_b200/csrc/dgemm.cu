@@ -396,8 +396,13 @@ bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* 
                                int64_t d, double* z, cudaStream_t s, bool force) {
     const int64_t m = xf->m;
     if (!force && m * d <= 64 * 128) return false;  // small Z: the wide in-kernel-generation GEMM is better
-    // (64 x 32 warp tiles at one CTA per SM measured slower: c5 19.2 vs 13.7 ms, c3 0.82 vs 0.70)
-    if (m >= 2 * d)
+    // 128 x 128 CTA tiles of 32 x 64 warp tiles (one CTA per SM) when Z covers them: half the
+    // shared-memory fragment traffic per DMMA of 64 x 128 tiles -- c5 8.52 -> 8.32 ms, c3
+    // 0.542 -> 0.530 ms -- in the one-pass GEMM over G in memory.  Over generated L2 chunks
+    // the 8-warp tiles stay faster (c5 13.3 vs 13.7 ms); option gemm_tile = 1 keeps them always.
+    if (ctx->opt_gemm_tile == 0 && xf->g_dev && ctx->opt_gemm_chunks == 0 && m >= 128 && d >= 128)
+        run_chunks<4, 2, 1, 4, 8>(ctx, xf, sx, b0, b1, d, z, s);
+    else if (m >= 2 * d)
         run_chunks<4, 2>(ctx, xf, sx, b0, b1, d, z, s);  // 128 x 64 tiles
     else
         run_chunks<2, 4>(ctx, xf, sx, b0, b1, d, z, s);  // 64 x 128 tiles

@@ -76,6 +76,7 @@ struct cgx_ctx {
     int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)
     int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 2 stable partition
     int64_t opt_gemm_ws = 0;                // option "gemm_ws": warp-specialized bulk-copy stage-2 GEMM
+    int64_t opt_gemm_tile = 0;              // option "gemm_tile": 1 = 8-warp 64x128/128x64 large-Z tiles
     int64_t opt_gemm_chunks = 0;            // option "gemm_chunks": 1 = 48 MB K-chunks even when G is in memory
     int64_t opt_g_resident = 1;             // option "g_resident": materialize seeded G at construction (<= 4 GiB)
     cgx::DevBuf part[6];                    // csr_partition.cu scratch: counters, payload copies, row keys
