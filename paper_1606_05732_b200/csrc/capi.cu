@@ -1198,6 +1198,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->fuse_mode = (int)value;
         else if (k == "rows_per_task" && value >= 1)
             ctx->opt_rows_per_task = value;
+        else if (k == "tail_tasks" && value >= 0 && value <= 64)
+            ctx->opt_tail_tasks = value;
         else if (k == "grid_waves" && value >= 1)
             ctx->opt_grid_waves = value;
         else if (k == "ws_gw" && value >= 0 && value <= 8)

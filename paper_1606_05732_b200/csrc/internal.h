@@ -71,6 +71,7 @@ struct cgx_ctx {
     bool force_fuse = false;               // option "fuse"=2: one-pass kernel even when G is in memory
     int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps fused, 2 warp-specialized
     int64_t opt_rows_per_task = 1024;       // option "rows_per_task": dense stream-kernel task size
+    int64_t opt_tail_tasks = 2;             // option "tail_tasks": single-bucket tasks per warp at the end
     int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
     int64_t opt_ws_gw = 0;                  // option "ws_gw": buckets per sketch warp per tile (0 = auto)
     int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)

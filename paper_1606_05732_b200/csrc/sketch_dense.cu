@@ -326,11 +326,13 @@ __device__ __forceinline__ void stream_buckets_async(const T* __restrict__ x, in
 
 // Persistent stream sketch over the cp.async ring (option async_stages = S): same tasks
 // and output as sketch_dense_stream.  Shared memory: per warp S x 32 x CB ring + S masks.
+// Tasks are handed out in bucket order: groups of G buckets for the first B1 buckets, then
+// single buckets, so the last tasks -- which set the kernel's tail -- are short.
 template <typename T, int V, int S>
 __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ x, int64_t ld, int64_t d,
                                                           const uint32_t* __restrict__ perm,
                                                           const uint32_t* __restrict__ offsets, int64_t B,
-                                                          int64_t nchunks, int G, double* __restrict__ sx,
+                                                          int64_t nchunks, int G, int64_t B1, double* __restrict__ sx,
                                                           unsigned* __restrict__ next_task) {
     constexpr int CW = 32 * V;
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -338,7 +340,8 @@ __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ 
     T* ring = reinterpret_cast<T*>(dsm) + (size_t)warp * S * 32 * CW;
     uint32_t* sneg = reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(dsm) + (size_t)(blockDim.x >> 5) * S * 32 * CW) +
                      warp * S;
-    const int64_t ngroups = (B + G - 1) / G;
+    const int64_t ng0 = B1 / G;  // B1 is a multiple of G
+    const int64_t ngroups = ng0 + (B - B1);
     const int64_t ntasks = ngroups * nchunks;
     for (;;) {
         unsigned t = 0;
@@ -350,8 +353,8 @@ __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ 
         const int64_t col0 = cw0 + (int64_t)lane * V;
         const bool colok = col0 < d;
         const int qv = (int)min((int64_t)(CW * sizeof(T) / 16), (d - cw0) * (int64_t)sizeof(T) / 16);
-        const int64_t b0 = bg * G;
-        const int nb = (int)min((int64_t)G, B - b0);
+        const int64_t b0 = bg < ng0 ? bg * G : B1 + (bg - ng0);
+        const int nb = bg < ng0 ? G : 1;
         double* out = sx + b0 * d + col0;
         stream_buckets_async<T, V, S>(x, ld, cw0, qv, perm, offsets, b0, nb, ring, sneg,
                                       [&](int i, const double (&acc)[V]) {
@@ -569,10 +572,14 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
             CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem));
             int64_t blocks = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);
             if (blocks > (tasks + W - 1) / W) blocks = (tasks + W - 1) / W;
+            // tail: the last ~2 single-bucket tasks per warp (option tail_tasks, per warp)
+            const int64_t tail = ctx->opt_tail_tasks * blocks * W / nchunks;
+            int64_t B1 = xf->B - tail;
+            B1 = B1 < 0 ? 0 : B1 / G * G;
             unsigned* ctr = (unsigned*)ctx->sched.get(sizeof(unsigned));
             CGX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
-            kern<<<(unsigned)blocks, 32 * W, smem, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks, (int)G, sx,
-                                                        ctr);
+            kern<<<(unsigned)blocks, 32 * W, smem, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks, (int)G, B1,
+                                                        sx, ctr);
             count_launch(ctx);
             check_launch("sketch_dense_async");
             return;
