@@ -190,11 +190,15 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
 //  * the next row group's perm entries and row offsets are loaded while the current group
 //    is processed, and a group's item loads are issued kW waves at a time.
 // Adds happen in exactly the serial kernel's order, so S.X is bit-identical to it.
+//  * warps are persistent and pull tasks of G consecutive buckets from a counter, the last
+//    ones single buckets (B1 = buckets in G-groups), so no SM idles while a late CTA wave
+//    finishes.
 template <typename TV, typename TI>
 __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64_t* __restrict__ rowptr, const TI* __restrict__ cols,
                                                        const TV* __restrict__ vals, const uint32_t* __restrict__ perm,
                                                        const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
-                                                       double* __restrict__ sx, int cbits) {
+                                                       double* __restrict__ sx, int cbits, int G, int64_t B1,
+                                                       unsigned* __restrict__ next_task) {
     constexpr int kW = CGX_CSR_KW;
     extern __shared__ double smem[];
     __shared__ uint8_t s_tbl[8][32];
@@ -205,7 +209,17 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
     uint8_t* tag = reinterpret_cast<uint8_t*>(smem + (size_t)warps_per_cta * d) + (size_t)wid * d;
     uint8_t* tbl = s_tbl[wid];
 
-    for (int64_t b = (int64_t)blockIdx.x * warps_per_cta + wid; b < B; b += (int64_t)gridDim.x * warps_per_cta) {
+    (void)warps_per_cta;
+    const int64_t ng0 = B1 / G;
+    const int64_t ntasks = ng0 + (B - B1);
+    for (;;) {
+      unsigned tk = 0;
+      if (lane == 0) tk = atomicAdd(next_task, 1u);
+      const int64_t task = __shfl_sync(0xffffffffu, tk, 0);
+      if (task >= ntasks) break;
+      const int64_t tb0 = task < ng0 ? task * G : B1 + (task - ng0);
+      const int64_t tb1 = task < ng0 ? tb0 + G : tb0 + 1;
+      for (int64_t b = tb0; b < tb1; ++b) {
         for (int64_t j = lane; j < d; j += 32) acc[j] = 0.0;
         __syncwarp();
         const uint32_t beg = offsets[b], end = offsets[b + 1];
@@ -288,6 +302,7 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
         __syncwarp();
         for (int64_t j = lane; j < d; j += 32) sx[b * d + j] = acc[j];
         __syncwarp();
+      }
     }
 }
 
@@ -316,12 +331,24 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
             const size_t sm = per_warp_l * wl + 8;
             auto lk = sketch_csr_lean<TV, TI>;
             CGX_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            int per_sm = 0;
+            CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, wl * 32, sm));
             int64_t nb = (xf->B + wl - 1) / wl;
-            const int64_t cap = (int64_t)ctx->num_sms * 32;
+            const int64_t cap = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);  // persistent: one wave
             if (nb > cap) nb = cap;
             int cb = 1;
             while (((int64_t)1 << (cb - 1)) < d) ++cb;
-            lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, cb);
+            // tasks of ~rows_per_task rows (whole buckets), single buckets for the last
+            // tail_tasks per warp
+            const int64_t rows_per_bucket = xf->n / xf->B + 1;
+            int64_t G = ctx->opt_rows_per_task / rows_per_bucket;
+            G = G < 1 ? 1 : (G > 64 ? 64 : G);
+            int64_t B1 = xf->B - ctx->opt_tail_tasks * nb * wl;
+            B1 = B1 < 0 ? 0 : B1 / G * G;
+            unsigned* ctr = (unsigned*)ctx->sched.get(sizeof(unsigned));
+            CGX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+            lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, cb, (int)G, B1,
+                                                 ctr);
             count_launch(ctx);
             check_launch("sketch_csr_lean");
             return;
