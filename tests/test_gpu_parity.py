@@ -788,3 +788,63 @@ def test_bucket_shards_hash_placement(cg, restatement, world):
         cg.api.countgauss_bucket_shard(m, B, n, 5, 5, full.seed)
     with pytest.raises(ValueError):
         cg.api.countgauss_bucket_shard(m, B, n, 0, B + 1, full.seed)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
+def test_full_size_checksums(cg, cfg):
+    """BASELINE configs c3/c4/c5 at FULL size (too large for the CPU oracle), through
+    size-independent exact properties.  X is made integer-valued (rounded 8x the config's
+    values) so every fp64 sum below is exact whatever its order:
+      * per bucket: sum_j SX[b, j] == sum_{i: h(i)=b} s_i * sum_j X[i, j]   (all B buckets)
+      * dense c4, per column: sum_b SX[b, j] == sum_i s_i X[i, j]
+    and Z matches G @ SX (cuBLAS fp64) within 1e-12 relative Frobenius."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1606_05732_b200 import bench_data
+    from paper_1606_05732_b200._lib import CGX_MEM_DEVICE, check, lib
+
+    cfgs = {"c3": dict(n=1 << 26, d=256, B=262144, m=128), "c4": dict(n=1 << 25, d=128, B=131072, m=32),
+            "c5": dict(n=1 << 27, d=512, B=1 << 20, m=256)}
+    c = cfgs[cfg]
+    n, d, B, m = c["n"], c["d"], c["B"], c["m"]
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(12345))
+    dev = torch.device("cuda")
+    h = torch.empty(n, dtype=torch.int64, device=dev)
+    s = torch.empty(n, dtype=torch.float64, device=dev)
+    check(lib.cgx_fill_hash_sign(t._xf.ctx.h, t._xf.h, h.data_ptr(), s.data_ptr(), CGX_MEM_DEVICE, C.c_void_p(1)))
+    if cfg == "c4":
+        x = bench_data.dense_normal(n, d, seed=oracle.mix64(12345, 4))
+        x.mul_(8).round_()
+        rowsum = torch.empty(n, dtype=torch.float64, device=dev)
+        colsum = torch.zeros(d, dtype=torch.float64, device=dev)
+        step = 1 << 22
+        for r0 in range(0, n, step):
+            blk = x[r0:r0 + step].double()
+            rowsum[r0:r0 + step] = blk.sum(1)
+            colsum += (blk * s[r0:r0 + step, None]).sum(0)
+            del blk
+    else:
+        if cfg == "c3":
+            x = bench_data.csr_bernoulli(n, d, 0.01, seed=oracle.mix64(12345, 3))
+        else:
+            x = bench_data.csr_zipf(n, d, seed=oracle.mix64(12345, 5))
+        x.values.mul_(8).round_()
+        cs = torch.zeros(x.nnz() + 1, dtype=torch.float64, device=dev)
+        torch.cumsum(x.values.double(), 0, out=cs[1:])
+        rowsum = cs[x.row_offsets[1:]] - cs[x.row_offsets[:-1]]
+        del cs
+        colsum = None
+    torch.cuda.synchronize()
+    sx = cg.countsketch_apply(t, x)  # B x d column-major view
+    want = torch.zeros(B, dtype=torch.float64, device=dev).index_add_(0, h, s * rowsum)
+    assert torch.equal(sx.sum(1), want)
+    if colsum is not None:
+        assert torch.equal(sx.sum(0), colsum)
+    z = cg.countgauss_apply(t, x)
+    g = torch.empty((B, m), dtype=torch.float64, device=dev)  # column-major m x B
+    check(lib.cgx_fill_gaussian(t._xf.ctx.h, t._xf.h, g.data_ptr(), CGX_MEM_DEVICE, C.c_void_p(1)))
+    z_ref = g.t() @ sx
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(z - z_ref) / torch.linalg.norm(z_ref)).item() <= Z_TOL
