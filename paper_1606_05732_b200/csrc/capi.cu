@@ -406,6 +406,8 @@ int cgx_init(int device, cgx_ctx** out) {
         CGX_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
         CGX_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         CGX_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        CGX_CUDA(cudaMalloc((void**)&ctx->task_ctr, sizeof(unsigned long long)));
+        CGX_CUDA(cudaMemsetAsync(ctx->task_ctr, 0, sizeof(unsigned long long), ctx->stream));
         CGX_CUDA(cudaEventRecord(ctx->done, ctx->stream));
         *out = ctx;
     });
@@ -435,6 +437,7 @@ int cgx_free(cgx_ctx* ctx) {
         ctx->gchunk.release();
         for (DevBuf& b : ctx->part) b.release();
         cudaStreamDestroy(ctx->stream);
+        cudaFree(ctx->task_ctr);
         delete ctx;
     });
 }

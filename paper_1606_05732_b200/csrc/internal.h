@@ -53,7 +53,13 @@ struct cgx_ctx {
     cgx::DevBuf sx, zpart, xstage, tmp;     // scratch (tmp: scan.cu only)
     cgx::DevBuf sort_k[2], sort_v[2], sort_hist, counts;  // transform construction
     cgx::DevBuf hstage_dev;                 // device landing zone for host inputs
-    cgx::DevBuf sched;                      // work-queue counters of persistent kernels
+    cgx::DevBuf sched;                      // small per-call flags (construct.cu)
+    // Work queue of the persistent kernels: one 64-bit counter that is never reset.  A
+    // launch handing `ntasks` tasks to `warps` persistent warps advances it by exactly
+    // ntasks + warps (every warp's last fetch fails), so the host knows each launch's base
+    // and no memset precedes the launch.
+    unsigned long long* task_ctr = nullptr;
+    unsigned long long task_base = 0;
     cgx::DevBuf gen_tables;                 // synthetic-input generator tables
     cudaStream_t aux = nullptr;             // side stream: G generation overlapping the sketch
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -99,6 +105,13 @@ struct cgx_xform {
 };
 
 namespace cgx {
+
+// Base of a persistent-kernel launch's tasks on ctx->task_ctr (see cgx_ctx::task_ctr).
+inline unsigned long long take_tasks(cgx_ctx* ctx, int64_t ntasks, int64_t warps) {
+    const unsigned long long b = ctx->task_base;
+    ctx->task_base += (unsigned long long)(ntasks + warps);
+    return b;
+}
 
 // construct.cu
 void build_perm_seeded(cgx_ctx* ctx, cgx_xform* xf, cudaStream_t s);

@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
                                                        const TV* __restrict__ vals, const uint32_t* __restrict__ perm,
                                                        const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
                                                        double* __restrict__ sx, int cbits, int G, int64_t B1,
-                                                       unsigned* __restrict__ next_task) {
+                                                       unsigned long long* __restrict__ next_task,
+                                                       unsigned long long task_base) {
     constexpr int kW = CGX_CSR_KW;
     extern __shared__ double smem[];
     __shared__ uint8_t s_tbl[8][32];
@@ -213,9 +214,9 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
     const int64_t ng0 = B1 / G;
     const int64_t ntasks = ng0 + (B - B1);
     for (;;) {
-      unsigned tk = 0;
-      if (lane == 0) tk = atomicAdd(next_task, 1u);
-      const int64_t task = __shfl_sync(0xffffffffu, tk, 0);
+      unsigned long long tk = 0;
+      if (lane == 0) tk = atomicAdd(next_task, 1ull) - task_base;
+      const int64_t task = (int64_t)__shfl_sync(0xffffffffu, tk, 0);
       if (task >= ntasks) break;
       const int64_t tb0 = task < ng0 ? task * G : B1 + (task - ng0);
       const int64_t tb1 = task < ng0 ? tb0 + G : tb0 + 1;
@@ -345,10 +346,9 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
             G = G < 1 ? 1 : (G > 64 ? 64 : G);
             int64_t B1 = xf->B - ctx->opt_tail_tasks * nb * wl;
             B1 = B1 < 0 ? 0 : B1 / G * G;
-            unsigned* ctr = (unsigned*)ctx->sched.get(sizeof(unsigned));
-            CGX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+            const unsigned long long base = take_tasks(ctx, B1 / G + xf->B - B1, nb * wl);
             lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, cb, (int)G, B1,
-                                                 ctr);
+                                                 ctx->task_ctr, base);
             count_launch(ctx);
             check_launch("sketch_csr_lean");
             return;

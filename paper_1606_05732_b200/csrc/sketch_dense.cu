@@ -333,7 +333,8 @@ __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ 
                                                           const uint32_t* __restrict__ perm,
                                                           const uint32_t* __restrict__ offsets, int64_t B,
                                                           int64_t nchunks, int G, int64_t B1, double* __restrict__ sx,
-                                                          unsigned* __restrict__ next_task) {
+                                                          unsigned long long* __restrict__ next_task,
+                                                          unsigned long long task_base) {
     constexpr int CW = 32 * V;
     extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -344,9 +345,9 @@ __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ 
     const int64_t ngroups = ng0 + (B - B1);
     const int64_t ntasks = ngroups * nchunks;
     for (;;) {
-        unsigned t = 0;
-        if (lane == 0) t = atomicAdd(next_task, 1u);
-        const int64_t task = __shfl_sync(0xffffffffu, t, 0);
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(next_task, 1ull) - task_base;
+        const int64_t task = (int64_t)__shfl_sync(0xffffffffu, t, 0);
         if (task >= ntasks) break;
         const int64_t bg = task / nchunks;
         const int64_t cw0 = (task - bg * nchunks) * CW;
@@ -576,10 +577,9 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
             const int64_t tail = ctx->opt_tail_tasks * blocks * W / nchunks;
             int64_t B1 = xf->B - tail;
             B1 = B1 < 0 ? 0 : B1 / G * G;
-            unsigned* ctr = (unsigned*)ctx->sched.get(sizeof(unsigned));
-            CGX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+            const unsigned long long base = take_tasks(ctx, (B1 / G + xf->B - B1) * nchunks, blocks * W);
             kern<<<(unsigned)blocks, 32 * W, smem, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks, (int)G, B1,
-                                                        sx, ctr);
+                                                        sx, ctx->task_ctr, base);
             count_launch(ctx);
             check_launch("sketch_dense_async");
             return;
