@@ -112,6 +112,15 @@ inline unsigned long long take_tasks(cgx_ctx* ctx, int64_t ntasks, int64_t warps
     ctx->task_base += (unsigned long long)(ntasks + warps);
     return b;
 }
+// After a persistent-kernel launch: if the launch was rejected the counter did not advance,
+// so restart the queue at zero before reporting the error (a stale base would make every
+// later launch see its tasks as taken).
+inline void tasks_launched(cgx_ctx* ctx, cudaStream_t s) {
+    if (cudaPeekAtLastError() != cudaSuccess) {
+        cudaMemsetAsync(ctx->task_ctr, 0, sizeof(unsigned long long), s);
+        ctx->task_base = 0;
+    }
+}
 
 // construct.cu
 void build_perm_seeded(cgx_ctx* ctx, cgx_xform* xf, cudaStream_t s);

@@ -350,6 +350,7 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
             lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, cb, (int)G, B1,
                                                  ctx->task_ctr, base);
             count_launch(ctx);
+            tasks_launched(ctx, s);
             check_launch("sketch_csr_lean");
             return;
         }

@@ -581,6 +581,7 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
             kern<<<(unsigned)blocks, 32 * W, smem, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks, (int)G, B1,
                                                         sx, ctx->task_ctr, base);
             count_launch(ctx);
+            tasks_launched(ctx, s);
             check_launch("sketch_dense_async");
             return;
         }
