@@ -235,10 +235,19 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and "WORLD_SIZE" in os.environ:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    # CGX_BENCH_BACKEND=gloo: functional check of the N>1 plumbing with every rank on the
+    # visible GPU(s) (host-side collectives, no device-side waits between ranks); its
+    # timings mean nothing.  The measured path is NCCL with one GPU per rank.
+    backend = os.environ.get("CGX_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_1606_05732_b200 as cg
     from paper_1606_05732_b200 import bench_data
@@ -314,22 +323,43 @@ def run_ours(args):
     sxbuf = torch.empty((B, d), dtype=torch.float64, device=dev) if world > 1 and args.combine in ("sx", "g") else None
     sxT = torch.empty((d, B), dtype=torch.float64, device=dev) if world > 1 and args.combine == "cols" else None
 
+    comb_ev = []  # (start, end) CUDA events around the combine phase of each timed step
+
+    def mark():
+        if timing_combine:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
+        return None
+
     def step():
         if world == 1 or args.combine == "z":
             cg.api.countgauss_apply_into(t, x, z)
             if world > 1:
+                e0 = mark()
                 dist.all_reduce(zbuf)  # partial Z of every row shard -> full Z on every rank
+                if e0 is not None:
+                    comb_ev.append((e0, mark()))
             return z
         if args.combine == "cols":
             cg.api.countsketch_apply_into(t, x, sxT.t())  # partial S.X, column-major
-            return combine("cols", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxT,
-                           stage2=lambda blk, c0, c1: cg.api.gauss_gemm(t, blk.t()).t())
-        cg.api.countsketch_apply_into(t, x, sxbuf)  # partial S.X (row-major B x d)
-        if args.combine == "sx":
-            return combine("sx", world=world, rank=rank, B=B, d=d, partial_sx=sxbuf,
-                           stage2=lambda sl, b0, b1: cg.api.gauss_gemm_range(t, sl, b0, b1))
-        return combine("g", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
-                       stage2=lambda sx, r0, r1: cg.api.gauss_gemm_rows(t, sx, r0, r1))
+            e0 = mark()
+            out = combine("cols", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxT,
+                          stage2=lambda blk, c0, c1: cg.api.gauss_gemm(t, blk.t()).t())
+        else:
+            cg.api.countsketch_apply_into(t, x, sxbuf)  # partial S.X (row-major B x d)
+            e0 = mark()
+            if args.combine == "sx":
+                out = combine("sx", world=world, rank=rank, B=B, d=d, partial_sx=sxbuf,
+                              stage2=lambda sl, b0, b1: cg.api.gauss_gemm_range(t, sl, b0, b1))
+            else:
+                out = combine("g", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
+                              stage2=lambda sx, r0, r1: cg.api.gauss_gemm_rows(t, sx, r0, r1))
+        if e0 is not None:
+            comb_ev.append((e0, mark()))
+        return out
+
+    timing_combine = False
 
     for _ in range(args.warmup):
         step()
@@ -343,11 +373,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        timing_combine = world > 1
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        timing_combine = False
         if world > 1:
             dist.barrier()
     launches = ctx.launches - launches0
@@ -476,7 +508,11 @@ def run_ours(args):
                       if c["m"] * c["B"] * 8 <= (4 << 30) and not any(o.startswith("g_resident=0") for o in args.opt)
                       else "generated inside the apply kernels"),
                 "options": args.opt,
-                "stage_ms": {"sketch": sk_avg_ms, "gemm": gm_ms / max(gm_n, 1)},
+                "stage_ms": {"sketch": sk_avg_ms, "gemm": gm_ms / max(gm_n, 1),
+                             **({"combine": sum(a.elapsed_time(b) for a, b in comb_ev) / len(comb_ev),
+                                 "combine_what": "rank 0: the NCCL collectives"
+                                 + (" and the stage 2 inside the combine" if args.combine != "z" else "")}
+                                if comb_ev else {})},
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": kernel_name,
