@@ -168,6 +168,7 @@ cgx_xform* new_xform(cgx_ctx* ctx, int64_t B, int64_t n) {
 }
 
 void drop_g(cgx_xform* xf) {
+    oz_drop_image(xf);
     if (!xf->g_dev) return;
     if (xf->g_pool)
         pool_free(xf->ctx, xf->g_dev);
@@ -436,6 +437,7 @@ int cgx_free(cgx_ctx* ctx) {
         ctx->gfull.release();
         ctx->gchunk.release();
         for (DevBuf& b : ctx->part) b.release();
+        for (DevBuf* b : {&ctx->oz_max, &ctx->oz_a, &ctx->oz_b}) b->release();
         cudaStreamDestroy(ctx->stream);
         cudaFree(ctx->task_ctr);
         delete ctx;
@@ -970,6 +972,7 @@ int cgx_gaussian_project_dense(cgx_ctx* ctx, uint64_t rng_state, int64_t m, cons
         gx.m = m;
         gx.g_seed = rng_state;
         gx.has_g = true;
+        gx.view = true;
         int64_t rld = ld;
         const void* xd = dense_rowmajor(ctx, &gx, x, dtype, layout, ld, n, d, x_mem, &rld, sc.st);
         const double* x64 = (const double*)xd;
@@ -1217,6 +1220,10 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_gemm_ws = value;
         else if (k == "gemm_tile" && (value == 0 || value == 1))
             ctx->opt_gemm_tile = value;
+        else if (k == "oz_slices" && (value == 0 || (value >= 3 && value <= 7)))
+            ctx->opt_oz_slices = value;
+        else if (k == "oz_staged" && (value == 0 || value == 1))
+            ctx->opt_oz_staged = value;
         else if (k == "gemm_chunks" && (value == 0 || value == 1))
             ctx->opt_gemm_chunks = value;
         else

@@ -476,6 +476,10 @@ void launch_gauss_gemm_rows(cgx_ctx* ctx, const cgx_xform* xf, const double* sx,
     gx.g_dev = gsub;
     gx.g_pool = false;
     gx.g_explicit = true;
+    gx.view = true;
+    gx.oz_gimg = nullptr;
+    gx.oz_gmax = nullptr;
+    gx.oz_gS = 0;
     launch_gauss_gemm(ctx, &gx, sx, 0, B, d, z, s);
 }
 

@@ -243,6 +243,7 @@ void launch_gauss_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int6
         CGX_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * (size_t)(m * d), s));
         return;
     }
+    if (launch_gemm_ozaki(ctx, xf, b0, b1, sx, d, z, s)) return;  // tcgen05 (opt-in)
     if (launch_gemm_small_g_ready(ctx, xf, sx, b0, b1, d, z, s)) return;  // small Z, G in memory
     if (launch_gauss_gemm_chunked(ctx, xf, sx, b0, b1, d, z, s)) return;  // large Z (dgemm.cu)
     if (d <= 1024) {

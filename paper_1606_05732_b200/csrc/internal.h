@@ -87,6 +87,9 @@ struct cgx_ctx {
     int64_t opt_gemm_chunks = 0;            // option "gemm_chunks": 1 = 48 MB K-chunks even when G is in memory
     int64_t opt_g_resident = 1;             // option "g_resident": materialize seeded G at construction (<= 4 GiB)
     cgx::DevBuf part[6];                    // csr_partition.cu scratch: counters, payload copies, row keys
+    int64_t opt_oz_slices = 0;              // option "oz_slices": stage 2 on tcgen05 int8 with S digit slices (0 = DMMA)
+    int64_t opt_oz_staged = 1;              // option "oz_staged": S.X rows reach the converters by bulk copy (0 = loads)
+    cgx::DevBuf oz_max, oz_a, oz_b;         // ozgemm.cu scratch: scales, digit images of G and S.X
 };
 
 struct cgx_xform {
@@ -102,6 +105,10 @@ struct cgx_xform {
     uint32_t* perm = nullptr;      // n entries: row | neg<<31, sorted by (bucket, row)
     uint32_t* offsets = nullptr;   // B+1 bucket boundaries into perm
     uint32_t* grows = nullptr;     // bucket-shard transforms: global row index of each local row
+    bool view = false;             // a stack copy over borrowed G (no caches may attach to it)
+    int8_t* oz_gimg = nullptr;     // ozgemm.cu: G's int8 digit image (oz_gS planes), built on first use
+    unsigned long long* oz_gmax = nullptr;
+    int oz_gS = 0;
 };
 
 namespace cgx {
@@ -184,6 +191,12 @@ void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, con
 // dgemm.cu: G super-chunks + pipelined DMMA GEMM; false when Z is small (not used)
 bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
                                int64_t d, double* z, cudaStream_t s, bool force = false);
+// ozgemm.cu: z (col-major m x d) = g (m x K col-major) . sx (row-major K x d) on tcgen05 kind::i8
+// with FP64 emulated by S = opt_oz_slices digit slices; false when the option is off
+// (buckets [b0, b1): sx points at row b0; G's digit image is cached on the transform)
+bool launch_gemm_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const double* sx, int64_t d,
+                       double* z, cudaStream_t s);
+void oz_drop_image(cgx_xform* xf);  // whenever G changes or goes
 // dgemm.cu: row-major fp32 (pitch ld) -> contiguous row-major fp64
 void launch_widen_f32(cgx_ctx* ctx, const float* src, int64_t ld, int64_t n, int64_t d, double* dst, cudaStream_t s);
 void launch_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int* bad,

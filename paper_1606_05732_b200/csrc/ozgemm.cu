@@ -1,0 +1,491 @@
+// ozgemm.cu -- stage 2 (Z = G . S.X, `gemm` in matrix.cpp:111-129) on the 5th-generation
+// tensor cores.  sm_100a has no FP64 tcgen05 kind, so the FP64 product is emulated exactly
+// the way an int8 tensor core can: Ozaki-style slicing.
+//
+//   * every row r of G (and every column j of S.X) gets a power-of-two scale 2^E with
+//     max |row| < 2^E;
+//   * each entry becomes the integer Y = trunc(x * 2^(8S-2-E)) (|Y| < 2^(8S-2): 54 bits at
+//     S = 7, more than an fp64 mantissa) written as S balanced base-256 digits d_s in
+//     [-128, 127], Y = sum_s d_s 256^(S-1-s) (oz_digits16);
+//   * Z(r, j) = 2^(E_r + F_j) * sum_{p < S} 2^(-8p-12) * sum_{s+t=p} (a_s . b_t): each digit
+//     dot product a_s . b_t is an int8 x int8 -> int32 tcgen05.mma (kind::i8), exact;
+//     the terms with s + t >= S (below 2^-(8S+4) relative) are dropped;
+//   * products with the same weight p share one int32 accumulator in TMEM (S groups of 64
+//     columns); a group holds at most S products of |128 * 128| per k, so it is drained to
+//     fp64 registers every OZ_FK values of k (S * 2^14 * OZ_FK < 2^31).
+//
+// The only roundings are the fp64 drain of exact integers and the dropped terms: measured
+// 4e-15 - 8e-15 relative Frobenius against cuBLAS fp64 at S = 7 on the c3/c5 shapes (the
+// DMMA path's bar is 1e-12; the reference's own is 1e-8, test_sketch.cpp:192-209), 7e-13 at
+// S = 6, 1.5e-10 at S = 5.
+//
+// Kernels: oz_absmax (per-row / per-column max), oz_slice (G's digits written straight into
+// the UMMA canonical K-major no-swizzle tile image once per transform, so the GEMM moves one
+// contiguous chunk per k-block with a 1-D bulk copy), oz_gemm (warp-specialized: S.X rows by
+// bulk copy -> converter warps cut them into digit planes in shared memory -> one thread
+// issues the tcgen05.mma -> TMEM -> epilogue warps drain to fp64).
+#include "common.cuh"
+#include "internal.h"
+
+namespace cgx {
+namespace {
+
+constexpr int OZ_MT = 128;    // MMA M (rows of G per CTA tile = TMEM lanes)
+constexpr int OZ_NT = 64;     // MMA N (columns of S.X per CTA tile)
+constexpr int OZ_KB = 32;     // k per MMA (int8: 32 bytes)
+constexpr int OZ_FK = 16384;  // k per int32 accumulation before the drain to fp64
+constexpr int OZ_MAXS = 7;
+
+// ---- tcgen05 / TMEM wrappers ----------------------------------------------------------
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, no swizzle: core matrices of 8 rows x 16 B (128 B contiguous); the two core
+// matrices of one 32 B k-step sit LBO = 128 B apart, consecutive 8-row groups SBO = 256 B.
+__device__ __forceinline__ uint64_t umma_desc(unsigned saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+           (1ull << 46);  // version 1 (sm_100), base offset 0, layout SWIZZLE_NONE
+}
+// kind::i8 instruction descriptor: D s32, A/B signed 8-bit, both K-major, M x N
+constexpr uint32_t oz_idesc(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, int acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// arrive on `bar` once every previously issued tcgen05.mma of this thread has completed
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// amax[w] = max over k of |X[k * W + w]| as the bit pattern of a non-negative double
+// (bit patterns of non-negative doubles order like the values).  W <= 4096.
+__global__ void oz_absmax(const double* __restrict__ X, int64_t K, int64_t W, unsigned long long* __restrict__ amax) {
+    extern __shared__ unsigned long long sm_max[];
+    for (int64_t w = threadIdx.x; w < W; w += blockDim.x) sm_max[w] = 0;
+    __syncthreads();
+    const int64_t total = K * W;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (stride % W == 0) {  // every thread sees a fixed w: keep its max in a register
+        const int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        unsigned long long mx = 0;
+        int64_t e = e0;
+        for (; e + 3 * stride < total; e += 4 * stride) {  // four independent loads in flight
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(X + e + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[u]));
+                mx = b > mx ? b : mx;
+            }
+        }
+        for (; e < total; e += stride) {
+            const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(X[e]));
+            mx = u > mx ? u : mx;
+        }
+        if (e0 < total || mx) atomicMax(&sm_max[e0 % W], mx);
+    } else {
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride)
+            atomicMax(&sm_max[e % W], (unsigned long long)__double_as_longlong(fabs(X[e])));
+    }
+    __syncthreads();
+    for (int64_t w = threadIdx.x; w < W; w += blockDim.x)
+        if (sm_max[w]) atomicMax(&amax[w], sm_max[w]);
+}
+
+// exponent E with max < 2^E (0 for an all-zero row)
+__device__ __forceinline__ int oz_exp(unsigned long long amax_bits) {
+    if (amax_bits == 0) return 0;
+    int e;
+    frexp(__longlong_as_double((long long)amax_bits), &e);
+    return e;
+}
+
+// Digits of 16 consecutive k of one w, packed 4 per 32-bit word per plane (byte kk % 4 of
+// word kk / 4).  Balanced base-256 digits: Y = trunc(x * 2^(8S-2-E)) (|Y| < 2^(8S-2)), and
+// U = Y + O with O = 0x80 in each of the S low bytes; byte b of U minus 128 (= byte ^ 0x80)
+// is digit S-1-b of Y, d in [-128, 127], Y = sum_s d_s 256^(S-1-s).  So one F2I per value
+// and one byte permute per digit: no per-digit arithmetic.  sc = 2^(8S-2-E).
+template <int S>
+__device__ __forceinline__ void oz_digits16(const double (&v)[16], double sc, uint32_t (&dig)[S][4]) {
+    constexpr unsigned long long O = 0x0080808080808080ull >> (8 * (7 - S));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t lo[4], hi[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const unsigned long long U = (unsigned long long)__double2ll_rz(v[4 * q + b] * sc) + O;
+            lo[b] = (uint32_t)U;
+            hi[b] = (uint32_t)(U >> 32);
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int bp = S - 1 - s;  // byte of U holding digit s
+            const uint32_t* X = bp < 4 ? lo : hi;
+            const uint32_t sel = (uint32_t)(bp & 3) | ((uint32_t)(4 + (bp & 3)) << 4);
+            const uint32_t t01 = __byte_perm(X[0], X[1], sel), t23 = __byte_perm(X[2], X[3], sel);
+            dig[s][q] = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
+        }
+    }
+}
+
+// X (K x W, W contiguous) -> S digit planes in the UMMA tile image:
+//   [w / R][k / 32][s][ (w%R)/8 ][ (k%32)/16 ][ w%8 ][ k%16 ]   (R x 32 bytes per plane)
+// One thread: 16 consecutive k of one w -> one 16 B store per digit plane.  Padding (w >= W
+// or k >= K) is written as zero digits.
+template <int S, int R>
+__global__ void oz_slice(const double* __restrict__ X, int64_t K, int64_t W, int64_t Wp, int64_t nkb,
+                         const unsigned long long* __restrict__ amax, int8_t* __restrict__ img) {
+    const int64_t groups = Wp * nkb * 2;  // (w, 16-k group)
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups;
+         gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = gi % Wp, kg = gi / Wp;  // consecutive threads: consecutive w (coalesced reads)
+        const int64_t k0 = kg * 16;
+        const int E = w < W ? oz_exp(amax[w]) : 0;
+        double v[16];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) v[kk] = (w < W && k0 + kk < K) ? X[(k0 + kk) * W + w] : 0.0;
+        uint32_t dig[S][4];
+        oz_digits16<S>(v, ldexp(1.0, 8 * S - 2 - E), dig);
+        const int64_t wt = w / R, r = w % R, kb = k0 / OZ_KB, kc = (k0 % OZ_KB) / 16;
+        int8_t* base = img + ((wt * nkb + kb) * S) * (int64_t)(R * OZ_KB) + (r / 8) * 256 + kc * 128 + (r % 8) * 16;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            *reinterpret_cast<uint4*>(base + (int64_t)s * R * OZ_KB) = make_uint4(dig[s][0], dig[s][1], dig[s][2], dig[s][3]);
+    }
+}
+
+// One CTA: a 128 x 64 tile of Z over k-blocks [kb0, kb1) of its split.
+//   warps 0-3: converters -- read S.X (fp64, straight from HBM/L2) for the stage's 32 x 64
+//              block, cut it into S digit planes in the UMMA image (shared memory);
+//   warps 4-7: epilogue  -- drain the TMEM accumulators (lanes 32(w-4).. = tile rows) into
+//              fp64 registers every OZ_FK values of k, scale and store the partial tile;
+//   warp 8:    producer  -- one 1-D bulk copy of G's digit planes per stage;
+//   warp 9:    MMA       -- one elected thread issues the S(S+1)/2 tcgen05.mma per stage.
+// shared memory: an MMA ring (G planes | S.X planes per stage, freed by the MMA commit) and
+// a deeper ring of raw fp64 S.X rows (freed as soon as the converters hold them in registers)
+constexpr int OZ_RAW = OZ_KB * OZ_NT * 8;
+template <int S>
+constexpr int oz_stage_bytes() { return S * (OZ_MT + OZ_NT) * OZ_KB; }
+template <int S>
+constexpr int oz_stages() { return S >= 6 ? 3 : 4; }
+template <int S>
+constexpr int oz_raw_stages() {
+    return ((220 << 10) - oz_stages<S>() * oz_stage_bytes<S>()) / OZ_RAW < 8
+               ? ((220 << 10) - oz_stages<S>() * oz_stage_bytes<S>()) / OZ_RAW
+               : 8;
+}
+template <int S>
+constexpr size_t oz_smem_bytes() { return (size_t)oz_stages<S>() * oz_stage_bytes<S>() + (size_t)oz_raw_stages<S>() * OZ_RAW + 1024; }
+
+template <int S>
+__global__ void __launch_bounds__(352, 1)
+oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const double* __restrict__ sx, int64_t K,
+        int64_t d, int64_t nkb, int64_t kb_per_split, const unsigned long long* __restrict__ amax_a,
+        const unsigned long long* __restrict__ amax_b, int64_t m, double* __restrict__ zpart, int staged) {
+    constexpr int A_BYTES = S * OZ_MT * OZ_KB;
+    constexpr int STAGE = oz_stage_bytes<S>();  // A planes | B planes
+    constexpr int OZ_STAGES = oz_stages<S>(), RS = oz_raw_stages<S>();
+    constexpr int FKB = OZ_FK / OZ_KB;  // k-blocks per accumulation
+    // the dynamic window is only guaranteed 16 B alignment under separate compilation: the
+    // ring starts at the next 1 KB boundary (1 KB extra requested); operand images that
+    // straddle it produce wrong products
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+    uint8_t* raw_ring = smem + OZ_STAGES * STAGE;
+    __shared__ uint64_t full[OZ_STAGES], bfull[OZ_STAGES], empty[OZ_STAGES], acc_full, acc_empty;
+    __shared__ uint64_t rfull[RS], rempty[RS];
+    __shared__ uint32_t tmem_slot;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t mt = blockIdx.x, nt = blockIdx.y, split = blockIdx.z;
+    const int64_t kb0 = split * kb_per_split;
+    const int64_t kb1 = kb0 + kb_per_split < nkb ? kb0 + kb_per_split : nkb;
+    const int64_t nk = kb1 - kb0;
+    const int64_t nchunks = (nk + FKB - 1) / FKB;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < OZ_STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&bfull[i], 128);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < RS; ++i) {
+            mbar_init(&rfull[i], 1);
+            mbar_init(&rempty[i], 128);
+        }
+        mbar_init(&acc_full, 1);
+        mbar_init(&acc_empty, 128);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 9) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp < 4) {
+        // converter: thread = (column j of the tile, 16-row half kc of the k-block)
+        const int j = threadIdx.x % OZ_NT, kc = threadIdx.x / OZ_NT;
+        const int64_t col = nt * OZ_NT + j;
+        const bool colok = col < d;
+        const int F = colok ? oz_exp(amax_b[col]) : 0;
+        const double* src = sx + (colok ? col : 0);
+        const double sc = ldexp(1.0, 8 * S - 2 - F);
+        const uint32_t soff = (uint32_t)((j / 8) * 256 + kc * 128 + (j % 8) * 16);
+        double cur[16], nxt[16];
+        auto load = [&](int64_t i, double (&v)[16]) {  // direct path: straight from global
+            const int64_t k0 = (kb0 + i) * OZ_KB + kc * 16;
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk)
+                v[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
+        };
+        if (!staged && nk > 0) load(0, cur);
+        for (int64_t i = 0; i < nk; ++i) {
+            const int st = (int)(i % OZ_STAGES);
+            uint8_t* stage = smem + st * STAGE;
+            if (staged) {
+                const int rt = (int)(i % RS);
+                mbar_wait(&rfull[rt], (unsigned)((i / RS) & 1));
+                const double* raw = reinterpret_cast<const double*>(raw_ring + rt * OZ_RAW) + kc * 16 * OZ_NT + j;
+                const int64_t k0 = (kb0 + i) * OZ_KB + kc * 16;
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk) cur[kk] = (colok && k0 + kk < K) ? raw[kk * OZ_NT] : 0.0;
+                mbar_arrive(&rempty[rt]);  // rows in registers: the raw slot may refill
+            } else {
+                if (i + 1 < nk) load(i + 1, nxt);
+            }
+            if (i >= OZ_STAGES) mbar_wait(&empty[st], (unsigned)(((i / OZ_STAGES) - 1) & 1));
+            uint32_t dig[S][4];
+            oz_digits16<S>(cur, sc, dig);
+            uint8_t* bp = stage + A_BYTES + soff;  // (the MMAs of k-block i - STAGES are done)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                *reinterpret_cast<uint4*>(bp + s * OZ_NT * OZ_KB) = make_uint4(dig[s][0], dig[s][1], dig[s][2], dig[s][3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> MMA reads
+            mbar_arrive(&bfull[st]);
+            if (!staged) {
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk) cur[kk] = nxt[kk];
+            }
+        }
+    } else if (warp < 8) {
+        // epilogue: drain each accumulation into fp64 registers (row = lane of this warp)
+        const int ew = warp - 4;
+        double acc[OZ_NT];
+#pragma unroll
+        for (int j = 0; j < OZ_NT; ++j) acc[j] = 0.0;
+        const uint32_t trow = tmem + ((uint32_t)(ew * 32) << 16);
+        for (int64_t c = 0; c < nchunks; ++c) {
+            mbar_wait(&acc_full, (unsigned)(c & 1));
+            tc_fence_after();
+#pragma unroll
+            for (int q = 0; q < OZ_NT / 16; ++q) {
+#pragma unroll
+                for (int p = S - 1; p >= 0; --p) {  // smallest weight first
+                    int v[16];
+                    tmem_ld16(trow + (uint32_t)(p * OZ_NT + q * 16), v);
+                    const double wgt = ldexp(1.0, -8 * p - 12);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[q * 16 + j] = fma((double)v[j], wgt, acc[q * 16 + j]);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty);
+        }
+        const int64_t r = mt * OZ_MT + ew * 32 + lane;
+        if (r < m) {
+            const int Er = oz_exp(amax_a[r]);
+            double* zp = zpart + split * m * d;
+#pragma unroll
+            for (int j = 0; j < OZ_NT; ++j) {
+                const int64_t col = nt * OZ_NT + j;
+                if (col < d) zp[col * m + r] = ldexp(acc[j], Er + oz_exp(amax_b[col]));
+            }
+        }
+    } else if (warp == 8) {
+        if (lane == 0) {  // producer: G's digit planes, one bulk copy per stage
+            const int8_t* ga = aimg + (mt * a_nkb + a_kb0 + kb0) * (int64_t)A_BYTES;
+            for (int64_t i = 0; i < nk; ++i) {
+                const int st = (int)(i % OZ_STAGES);
+                if (i >= OZ_STAGES) mbar_wait(&empty[st], (unsigned)(((i / OZ_STAGES) - 1) & 1));
+                mbar_arrive_expect_tx(&full[st], A_BYTES);
+                bulk_g2s(smem + st * STAGE, ga + i * A_BYTES, A_BYTES, &full[st]);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 10) {
+        if (staged) {  // producer: the block's S.X rows (lane r copies row r) into the raw ring
+            const int64_t c0 = nt * OZ_NT;
+            const unsigned row_bytes = (unsigned)((d - c0 < OZ_NT ? d - c0 : OZ_NT) * 8);
+            for (int64_t i = 0; i < nk; ++i) {
+                const int rt = (int)(i % RS);
+                const int64_t k0 = (kb0 + i) * OZ_KB;
+                const int rows = (int)(K - k0 < OZ_KB ? K - k0 : OZ_KB);
+                if (i >= RS) mbar_wait(&rempty[rt], (unsigned)(((i / RS) - 1) & 1));
+                if (lane == 0) mbar_arrive_expect_tx(&rfull[rt], (unsigned)rows * row_bytes);
+                __syncwarp();
+                if (lane < rows)
+                    bulk_g2s(raw_ring + rt * OZ_RAW + lane * (OZ_NT * 8), sx + (k0 + lane) * d + c0, row_bytes, &rfull[rt]);
+            }
+        }
+    } else if (warp == 9) {
+        if (lane == 0) {  // MMA issuer
+            constexpr uint32_t idesc = oz_idesc(OZ_MT, OZ_NT);
+            const unsigned sbase = smem_addr(smem);
+            for (int64_t i = 0; i < nk; ++i) {
+                const int st = (int)(i % OZ_STAGES);
+                const int64_t c = i / FKB;
+                const bool first = (i % FKB) == 0;
+                if (first && c > 0) mbar_wait(&acc_empty, (unsigned)((c - 1) & 1));  // drained
+                mbar_wait(&full[st], (unsigned)((i / OZ_STAGES) & 1));
+                mbar_wait(&bfull[st], (unsigned)((i / OZ_STAGES) & 1));
+                tc_fence_after();
+                const unsigned sa = sbase + st * STAGE, sb = sa + A_BYTES;
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+#pragma unroll
+                    for (int t = 0; t + s < S; ++t)
+                        mma_i8(tmem + (uint32_t)((s + t) * OZ_NT), umma_desc(sa + s * OZ_MT * OZ_KB),
+                               umma_desc(sb + t * OZ_NT * OZ_KB), idesc, (first && s == 0) ? 0 : 1);
+                mma_commit(&empty[st]);  // stage free once these MMAs have read it
+                if ((i % FKB) == FKB - 1 || i == nk - 1) mma_commit(&acc_full);
+            }
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+void run_absmax(cgx_ctx* ctx, const double* X, int64_t K, int64_t W, unsigned long long* out, cudaStream_t s) {
+    const int threads = 256;
+    int64_t t = threads;
+    if (W <= threads) t = threads / W * W;  // stride multiple of W: register max per thread
+    int64_t blocks = (K * W + t - 1) / t;
+    if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
+    if (W > t && blocks > 1) blocks &= ~int64_t(1);  // W = 2t: even block count keeps the register path
+    oz_absmax<<<(unsigned)blocks, (unsigned)t, sizeof(unsigned long long) * (size_t)W, s>>>(X, K, W, out);
+    count_launch(ctx);
+    check_launch("oz_absmax");
+}
+
+// digit image of G (m x K column-major) and its row maxima
+template <int S>
+void build_g_image(cgx_ctx* ctx, const double* g, int64_t m, int64_t K, unsigned long long* amax, int8_t* img,
+                   cudaStream_t s) {
+    const int64_t nkb = (K + OZ_KB - 1) / OZ_KB, mp = (m + OZ_MT - 1) / OZ_MT * OZ_MT;
+    CGX_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned long long) * (size_t)m, s));
+    run_absmax(ctx, g, K, m, amax, s);
+    int64_t b = (mp * nkb * 2 + 255) / 256;
+    if (b > ctx->num_sms * 16) b = ctx->num_sms * 16;
+    oz_slice<S, OZ_MT><<<(unsigned)b, 256, 0, s>>>(g, K, m, mp, nkb, amax, img);
+    count_launch(ctx);
+    check_launch("oz_slice(G)");
+}
+
+template <int S>
+void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const double* sx, int64_t d, double* z,
+               cudaStream_t s) {
+    const int64_t m = xf->m, K = b1 - b0;
+    const int64_t nkb = (K + OZ_KB - 1) / OZ_KB;
+    const int64_t tm = (m + OZ_MT - 1) / OZ_MT, tn = (d + OZ_NT - 1) / OZ_NT;
+    const int64_t mp = tm * OZ_MT;
+    // G's digit image: built once per transform (G is part of the transform, like t.g) and
+    // kept until G changes; a view or an unaligned bucket range slices its own copy
+    const int8_t* aimg;
+    const unsigned long long* amax_a;
+    int64_t a_nkb, a_kb0;
+    if (!xf->view && b0 % OZ_KB == 0) {
+        cgx_xform* mx = const_cast<cgx_xform*>(xf);
+        if (mx->oz_gS != S) {
+            oz_drop_image(mx);
+            const int64_t fkb = (xf->B + OZ_KB - 1) / OZ_KB;
+            CGX_CUDA(cudaMalloc((void**)&mx->oz_gimg, (size_t)(S * mp * fkb * OZ_KB)));
+            CGX_CUDA(cudaMalloc((void**)&mx->oz_gmax, sizeof(unsigned long long) * (size_t)m));
+            build_g_image<S>(ctx, xf->g_dev, m, xf->B, mx->oz_gmax, mx->oz_gimg, s);
+            mx->oz_gS = S;
+        }
+        aimg = xf->oz_gimg;
+        amax_a = xf->oz_gmax;
+        a_nkb = (xf->B + OZ_KB - 1) / OZ_KB;
+        a_kb0 = b0 / OZ_KB;
+    } else {
+        unsigned long long* am = (unsigned long long*)ctx->oz_max.get(sizeof(unsigned long long) * (size_t)m);
+        int8_t* img = (int8_t*)ctx->oz_a.get((size_t)(S * mp * nkb * OZ_KB));
+        build_g_image<S>(ctx, xf->g_dev + b0 * m, m, K, am, img, s);
+        aimg = img;
+        amax_a = am;
+        a_nkb = nkb;
+        a_kb0 = 0;
+    }
+    // column maxima of S.X
+    unsigned long long* amax_b = (unsigned long long*)ctx->oz_b.get(sizeof(unsigned long long) * (size_t)d);
+    CGX_CUDA(cudaMemsetAsync(amax_b, 0, sizeof(unsigned long long) * (size_t)d, s));
+    run_absmax(ctx, sx, K, d, amax_b, s);
+    // one wave: one CTA per SM
+    int64_t splits = ctx->num_sms / (tm * tn);
+    if (splits < 1) splits = 1;
+    if (splits > nkb) splits = nkb;
+    const int64_t kps = (nkb + splits - 1) / splits;
+    splits = (nkb + kps - 1) / kps;
+    double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
+    const size_t smem = oz_smem_bytes<S>();
+    // rows of S.X staged by bulk copies when every row segment is 16 B aligned
+    const int staged = ctx->opt_oz_staged && d % 2 == 0 && ((uintptr_t)sx % 16) == 0;
+    CGX_CUDA(cudaFuncSetAttribute(oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    oz_gemm<S><<<dim3((unsigned)tm, (unsigned)tn, (unsigned)splits), 352, smem, s>>>(
+        aimg, a_nkb, a_kb0, sx, K, d, nkb, kps, amax_a, amax_b, m, zpart, staged);
+    count_launch(ctx);
+    check_launch("oz_gemm");
+    launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
+}
+
+} // namespace
+
+void oz_drop_image(cgx_xform* xf) {
+    if (xf->oz_gimg) cudaFree(xf->oz_gimg);
+    if (xf->oz_gmax) cudaFree(xf->oz_gmax);
+    xf->oz_gimg = nullptr;
+    xf->oz_gmax = nullptr;
+    xf->oz_gS = 0;
+}
+
+bool launch_gemm_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const double* sx, int64_t d,
+                       double* z, cudaStream_t s) {
+    const int S = (int)ctx->opt_oz_slices;
+    if (S <= 0 || !xf->g_dev || xf->m > 4096 || d > 4096 || b1 <= b0 || d < 1) return false;
+    switch (S) {
+        case 3: run_ozaki<3>(ctx, xf, b0, b1, sx, d, z, s); return true;
+        case 4: run_ozaki<4>(ctx, xf, b0, b1, sx, d, z, s); return true;
+        case 5: run_ozaki<5>(ctx, xf, b0, b1, sx, d, z, s); return true;
+        case 6: run_ozaki<6>(ctx, xf, b0, b1, sx, d, z, s); return true;
+        case 7: run_ozaki<7>(ctx, xf, b0, b1, sx, d, z, s); return true;
+        default: return false;
+    }
+}
+
+} // namespace cgx

@@ -384,6 +384,89 @@ def test_stage2_large_z(cg, restatement, m, d, B, g_mode, gemm_ws):
     assert rel_fro(z2, ref) <= 1e-14
 
 
+@pytest.fixture
+def ozaki(cg):
+    """Stage 2 on the tcgen05 int8 tensor cores (ozgemm.cu), S digit planes."""
+    ctx = cg.context()
+
+    def use(S, staged=1):
+        ctx.set_option("oz_slices", S)
+        ctx.set_option("oz_staged", staged)
+
+    yield use
+    ctx.set_option("oz_slices", 0)
+    ctx.set_option("oz_staged", 1)
+
+
+# S = 7 planes of 8-bit balanced digits carry 54 bits per operand: Z to the DMMA path's bar.
+# Fewer planes trade accuracy for speed; the bars below hold with 10x margin on Gaussian G.
+OZ_TOL = {7: Z_TOL, 6: 1e-11, 5: 1e-8}
+
+
+@pytest.mark.parametrize("m,d,B", [(96, 300, 20011), (256, 512, 40000), (130, 70, 9000), (64, 129, 33333),
+                                   (128, 256, 30000), (1, 1, 37), (300, 1, 1000), (5, 66, 65)])
+@pytest.mark.parametrize("S,staged", [(7, 1), (7, 0), (6, 1), (5, 1)])
+def test_stage2_tensor_core_ozaki(cg, restatement, m, d, B, S, staged, ozaki):
+    """Stage 2 (gemm(t.g, SX), matrix.cpp:111-129) through tcgen05.mma kind::i8 with FP64
+    emulated by digit slicing: against the oracle's gemm, for resident seeded G and for an
+    explicit G (whose cached digit image must be dropped when G is replaced)."""
+    from paper_1606_05732_b200._lib import CGX_COL_MAJOR, CGX_MEM_HOST, check, lib
+
+    ozaki(S, staged)
+    rng = np.random.default_rng(m + d + B)
+    sx = np.asfortranarray(rng.standard_normal((B, d)))
+    sx[:, 0] = 0.0  # an all-zero column (scale 2^0, all digits 0)
+    t = cg.countgauss_new(m, B, 10, cg.SeededRng(m * d + 1))
+    _, _, gs = restatement.countgauss_seeds(m * d + 1)
+    G = restatement.gaussian(gs, m, B)
+    ctx = cg.context()
+    z = np.empty((m, d), np.float64, order="F")
+    for _ in range(2):  # second call reuses the transform's cached image of G
+        check(lib.cgx_gauss_gemm(ctx.h, t._xf.h, sx.ctypes.data, CGX_COL_MAJOR, d, CGX_MEM_HOST, z.ctypes.data,
+                                 CGX_MEM_HOST, None))
+        assert rel_fro(z, restatement.gemm(G, sx)) <= OZ_TOL[S]
+    G2 = np.asfortranarray(G * np.linspace(1e-3, 1e3, B)[None, :])  # new G, wide column range
+    check(lib.cgx_xform_set_gaussian_explicit(ctx.h, t._xf.h, m, G2.ctypes.data, CGX_MEM_HOST))
+    check(lib.cgx_gauss_gemm(ctx.h, t._xf.h, sx.ctypes.data, CGX_COL_MAJOR, d, CGX_MEM_HOST, z.ctypes.data,
+                             CGX_MEM_HOST, None))
+    assert rel_fro(z, restatement.gemm(G2, sx)) <= OZ_TOL[S]
+
+
+@pytest.mark.parametrize("b0,b1", [(0, 4096), (64, 3000), (33, 4000), (4001, 4096)])
+def test_stage2_ozaki_bucket_ranges(cg, restatement, b0, b1, ozaki):
+    """Stage 2 over a bucket slice (the multi-GPU "sx" combine): aligned slices read the
+    transform's cached digit image at a k-block offset, unaligned ones slice their own."""
+    from paper_1606_05732_b200._lib import CGX_MEM_HOST, check, lib
+
+    ozaki(7)
+    m, d, B = 130, 70, 4096
+    rng = np.random.default_rng(b0)
+    sx = rng.standard_normal((B, d))
+    t = cg.countgauss_new(m, B, 10, cg.SeededRng(99))
+    _, _, gs = restatement.countgauss_seeds(99)
+    G = restatement.gaussian(gs, m, B)
+    ctx = cg.context()
+    sl = np.ascontiguousarray(sx[b0:b1])
+    z = np.empty((m, d), order="F")
+    check(lib.cgx_gauss_gemm_range(ctx.h, t._xf.h, sl.ctypes.data, b0, b1, d, CGX_MEM_HOST, z.ctypes.data,
+                                   CGX_MEM_HOST, None))
+    assert rel_fro(z, restatement.gemm(np.asfortranarray(G[:, b0:b1]), sl)) <= Z_TOL
+
+
+def test_ozaki_full_apply_csr(cg, restatement, ozaki):
+    """countgauss_apply on CSR X with stage 2 on the tensor cores: S.X stays bit-exact (the
+    sketch is untouched) and Z meets the bar."""
+    ozaki(7)
+    rng = np.random.default_rng(5)
+    n, d, B, m = 30000, 256, 4099, 128
+    rp, c, v = _random_csr(rng, n, d, 0.02, np.int32, np.float32)
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(2024))
+    x = cg.SparseMatrix(n, d, rp, c, v)
+    z_ref, sx_ref = restatement.countgauss(2024, m, B, csr=(rp, c, v, d))
+    assert np.array_equal(cg.countsketch_apply(t, x), sx_ref)
+    assert rel_fro(cg.countgauss_apply(t, x), z_ref) <= Z_TOL
+
+
 @pytest.mark.parametrize("n,d,m,dtype", [(5000, 24, 16, np.float64), (70000, 32, 64, np.float32),
                                          (3000, 200, 40, np.float64)])
 def test_dense_gaussian_projection(cg, restatement, n, d, m, dtype):

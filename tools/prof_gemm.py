@@ -24,8 +24,10 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--explicit", type=int, default=0)
     ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE")
+    ap.add_argument("--shape", default="", help="B,m,d instead of a config")
+    ap.add_argument("--check", type=int, default=0, help="1: relative Frobenius error vs cuBLAS fp64")
     a = ap.parse_args()
-    B, m, d = SHAPES[a.config]
+    B, m, d = [int(v) for v in a.shape.split(",")] if a.shape else SHAPES[a.config]
     ctx = cg.context(0)
     for kv in a.opt:
         k, v = kv.split("=", 1)
@@ -46,7 +48,14 @@ def main():
         ev[1].record()
         torch.cuda.synchronize()
         ms = ev[0].elapsed_time(ev[1])
-        print(f"{a.config} explicit={a.explicit} rep {rep}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
+        print(f"{a.config} {B},{m},{d} {a.opt} explicit={a.explicit} rep {rep}: {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
+    if a.check:
+        g = torch.empty((B, m), dtype=torch.float64, device="cuda")
+        check(lib.cgx_fill_gaussian(ctx.h, t._xf.h, g.data_ptr(), CGX_MEM_DEVICE, C.c_void_p(1)))
+        torch.cuda.synchronize()
+        zr = sx.t() @ g
+        err = ((z - zr).norm() / zr.norm()).item()
+        print(f"check {B},{m},{d} {a.opt}: rel Frobenius err vs cuBLAS fp64 {err:.3e}  max abs {(z - zr).abs().max().item():.3e}")
 
 
 if __name__ == "__main__":
