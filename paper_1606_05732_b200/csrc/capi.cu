@@ -1222,6 +1222,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_gemm_tile = value;
         else if (k == "oz_slices" && (value == 0 || (value >= 3 && value <= 7)))
             ctx->opt_oz_slices = value;
+        else if (k == "oz_min_z" && value >= 0)
+            ctx->opt_oz_min_z = value;
         else if (k == "oz_staged" && (value == 0 || value == 1))
             ctx->opt_oz_staged = value;
         else if (k == "gemm_chunks" && (value == 0 || value == 1))

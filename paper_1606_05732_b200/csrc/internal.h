@@ -87,7 +87,8 @@ struct cgx_ctx {
     int64_t opt_gemm_chunks = 0;            // option "gemm_chunks": 1 = 48 MB K-chunks even when G is in memory
     int64_t opt_g_resident = 1;             // option "g_resident": materialize seeded G at construction (<= 4 GiB)
     cgx::DevBuf part[6];                    // csr_partition.cu scratch: counters, payload copies, row keys
-    int64_t opt_oz_slices = 0;              // option "oz_slices": stage 2 on tcgen05 int8 with S digit slices (0 = DMMA)
+    int64_t opt_oz_slices = 7;              // option "oz_slices": stage 2 on tcgen05 int8 with S digit planes (0 = DMMA)
+    int64_t opt_oz_min_z = 16384;           // option "oz_min_z": smallest m*d that takes the tcgen05 stage 2
     int64_t opt_oz_staged = 1;              // option "oz_staged": S.X rows reach the converters by bulk copy (0 = loads)
     cgx::DevBuf oz_max, oz_a, oz_b;         // ozgemm.cu scratch: scales, digit images of G and S.X
 };

@@ -73,35 +73,43 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
 }
 
 // amax[w] = max over k of |X[k * W + w]| as the bit pattern of a non-negative double
-// (bit patterns of non-negative doubles order like the values).  W <= 4096.
+// (bit patterns of non-negative doubles order like the values).  W <= 4096.  With W even
+// and a grid stride that is a multiple of W, every thread owns one column pair and keeps
+// its maxima in registers over 16 B loads, 8 in flight.
 __global__ void oz_absmax(const double* __restrict__ X, int64_t K, int64_t W, unsigned long long* __restrict__ amax) {
     extern __shared__ unsigned long long sm_max[];
     for (int64_t w = threadIdx.x; w < W; w += blockDim.x) sm_max[w] = 0;
     __syncthreads();
-    const int64_t total = K * W;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    if (stride % W == 0) {  // every thread sees a fixed w: keep its max in a register
-        const int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        unsigned long long mx = 0;
-        int64_t e = e0;
-        for (; e + 3 * stride < total; e += 4 * stride) {  // four independent loads in flight
-            double v[4];
+    auto bits = [](double v) { return (unsigned long long)__double_as_longlong(fabs(v)); };
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    if (W % 2 == 0 && (nthr * 2) % W == 0 && ((uintptr_t)X % 16) == 0) {
+        const double2* X2 = reinterpret_cast<const double2*>(X);
+        const int64_t total = K * W / 2;
+        unsigned long long m0 = 0, m1 = 0;
+        int64_t e = tid;
+        for (; e + 7 * nthr < total; e += 8 * nthr) {
+            double2 v[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldg(X + e + u * stride);
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(X2 + e + u * nthr);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[u]));
-                mx = b > mx ? b : mx;
+            for (int u = 0; u < 8; ++u) {
+                m0 = max(m0, bits(v[u].x));
+                m1 = max(m1, bits(v[u].y));
             }
         }
-        for (; e < total; e += stride) {
-            const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(X[e]));
-            mx = u > mx ? u : mx;
+        for (; e < total; e += nthr) {
+            const double2 v = __ldg(X2 + e);
+            m0 = max(m0, bits(v.x));
+            m1 = max(m1, bits(v.y));
         }
-        if (e0 < total || mx) atomicMax(&sm_max[e0 % W], mx);
+        const int64_t w0 = (2 * tid) % W;
+        if (tid < total) {
+            atomicMax(&sm_max[w0], m0);
+            atomicMax(&sm_max[w0 + 1], m1);
+        }
     } else {
-        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride)
-            atomicMax(&sm_max[e % W], (unsigned long long)__double_as_longlong(fabs(X[e])));
+        for (int64_t e = tid; e < K * W; e += nthr) atomicMax(&sm_max[e % W], bits(X[e]));
     }
     __syncthreads();
     for (int64_t w = threadIdx.x; w < W; w += blockDim.x)
@@ -350,7 +358,6 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
         }
     } else if (warp == 9) {
         if (lane == 0) {  // MMA issuer
-            constexpr uint32_t idesc = oz_idesc(OZ_MT, OZ_NT);
             const unsigned sbase = smem_addr(smem);
             for (int64_t i = 0; i < nk; ++i) {
                 const int st = (int)(i % OZ_STAGES);
@@ -361,12 +368,20 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 mbar_wait(&bfull[st], (unsigned)((i / OZ_STAGES) & 1));
                 tc_fence_after();
                 const unsigned sa = sbase + st * STAGE, sb = sa + A_BYTES;
+                // A plane s against B planes t0 .. t0+w-1 in one MMA: the planes sit
+                // consecutively in shared memory, so they form one N = 64w operand, and the
+                // products land in groups s+t0 .. s+t0+w-1, consecutive TMEM columns.  Up to
+                // N = 256 per instruction: S(S+1)/2 products in ~S + S/2 instructions (an
+                // N = 64 MMA costs ~3x its share of the tensor pipe, tools/microbench/umma_i8.cu).
 #pragma unroll
                 for (int s = 0; s < S; ++s)
 #pragma unroll
-                    for (int t = 0; t + s < S; ++t)
-                        mma_i8(tmem + (uint32_t)((s + t) * OZ_NT), umma_desc(sa + s * OZ_MT * OZ_KB),
-                               umma_desc(sb + t * OZ_NT * OZ_KB), idesc, (first && s == 0) ? 0 : 1);
+                    for (int t0 = 0; t0 < S - s; t0 += 4) {
+                        const int w = S - s - t0 < 4 ? S - s - t0 : 4;
+                        mma_i8(tmem + (uint32_t)((s + t0) * OZ_NT), umma_desc(sa + s * OZ_MT * OZ_KB),
+                               umma_desc(sb + t0 * OZ_NT * OZ_KB), oz_idesc(OZ_MT, OZ_NT * w),
+                               (first && s == 0) ? 0 : 1);
+                    }
                 mma_commit(&empty[st]);  // stage free once these MMAs have read it
                 if ((i % FKB) == FKB - 1 || i == nk - 1) mma_commit(&acc_full);
             }
@@ -382,12 +397,17 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
 }
 
 void run_absmax(cgx_ctx* ctx, const double* X, int64_t K, int64_t W, unsigned long long* out, cudaStream_t s) {
-    const int threads = 256;
-    int64_t t = threads;
-    if (W <= threads) t = threads / W * W;  // stride multiple of W: register max per thread
-    int64_t blocks = (K * W + t - 1) / t;
-    if (blocks > ctx->num_sms * 8) blocks = ctx->num_sms * 8;
-    if (W > t && blocks > 1) blocks &= ~int64_t(1);  // W = 2t: even block count keeps the register path
+    // 256 threads; blocks chosen so that 2 * threads * blocks is a multiple of W when W is even
+    const int64_t t = 256;
+    int64_t blocks = ctx->num_sms * 4;
+    if (W % 2 == 0) {
+        const int64_t q = W / 2;  // thread count must be a multiple of q
+        auto gcd = [](int64_t a, int64_t b) { while (b) { const int64_t r = a % b; a = b; b = r; } return a; };
+        const int64_t unit = q / gcd(q, t);  // blocks must be a multiple of unit
+        blocks = (blocks + unit - 1) / unit * unit;
+    }
+    const int64_t need = (K * W / 2 + t - 1) / t;
+    if (blocks > need && W % 2 != 0) blocks = need < 1 ? 1 : need;
     oz_absmax<<<(unsigned)blocks, (unsigned)t, sizeof(unsigned long long) * (size_t)W, s>>>(X, K, W, out);
     count_launch(ctx);
     check_launch("oz_absmax");
@@ -478,6 +498,7 @@ bool launch_gemm_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1
                        double* z, cudaStream_t s) {
     const int S = (int)ctx->opt_oz_slices;
     if (S <= 0 || !xf->g_dev || xf->m > 4096 || d > 4096 || b1 <= b0 || d < 1) return false;
+    if (xf->m * d < ctx->opt_oz_min_z) return false;  // small Z: the split-K DMMA stream is faster
     switch (S) {
         case 3: run_ozaki<3>(ctx, xf, b0, b1, sx, d, z, s); return true;
         case 4: run_ozaki<4>(ctx, xf, b0, b1, sx, d, z, s); return true;

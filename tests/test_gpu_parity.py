@@ -350,10 +350,13 @@ def test_csr_zipf_config5_shape(cg, restatement):
 
 @pytest.fixture(params=[0, 1], ids=["gemm-pipelined", "gemm-warp-specialized"])
 def gemm_ws(request, cg):
+    """The DMMA stage 2 (large Z otherwise goes to the tensor-core path, ozgemm.cu)."""
     ctx = cg.context()
     ctx.set_option("gemm_ws", request.param)
+    ctx.set_option("oz_slices", 0)
     yield request.param
     ctx.set_option("gemm_ws", 0)
+    ctx.set_option("oz_slices", 7)
 
 
 @pytest.mark.parametrize("m,d,B", [(96, 300, 20011), (256, 512, 40000), (130, 70, 9000), (64, 129, 33333),
@@ -392,10 +395,12 @@ def ozaki(cg):
     def use(S, staged=1):
         ctx.set_option("oz_slices", S)
         ctx.set_option("oz_staged", staged)
+        ctx.set_option("oz_min_z", 0)  # every Z shape, not only the large ones it is chosen for
 
     yield use
-    ctx.set_option("oz_slices", 0)
+    ctx.set_option("oz_slices", 7)
     ctx.set_option("oz_staged", 1)
+    ctx.set_option("oz_min_z", 16384)
 
 
 # S = 7 planes of 8-bit balanced digits carry 54 bits per operand: Z to the DMMA path's bar.
