@@ -1222,6 +1222,14 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_gemm_tile = value;
         else if (k == "oz_slices" && (value == 0 || (value >= 3 && value <= 7)))
             ctx->opt_oz_slices = value;
+        else if (k == "oz_cluster" && (value == 1 || value == 2 || value == 4 || value == 8))
+            ctx->opt_oz_cluster = value;
+        else if (k == "oz_dbg" && value >= 0 && value <= 3)
+            ctx->opt_oz_dbg = value;
+        else if (k == "oz_st" && value >= 0 && value <= 8)
+            ctx->opt_oz_st = value;
+        else if (k == "oz_rs" && value >= 0 && value <= 8)
+            ctx->opt_oz_rs = value;
         else if (k == "oz_min_z" && value >= 0)
             ctx->opt_oz_min_z = value;
         else if (k == "oz_staged" && (value == 0 || value == 1))

@@ -6,7 +6,7 @@
 //     max |row| < 2^E;
 //   * each entry becomes the integer Y = trunc(x * 2^(8S-2-E)) (|Y| < 2^(8S-2): 54 bits at
 //     S = 7, more than an fp64 mantissa) written as S balanced base-256 digits d_s in
-//     [-128, 127], Y = sum_s d_s 256^(S-1-s) (oz_digits16);
+//     [-128, 127], Y = sum_s d_s 256^(S-1-s) (oz_digits);
 //   * Z(r, j) = 2^(E_r + F_j) * sum_{p < S} 2^(-8p-12) * sum_{s+t=p} (a_s . b_t): each digit
 //     dot product a_s . b_t is an int8 x int8 -> int32 tcgen05.mma (kind::i8), exact;
 //     the terms with s + t >= S (below 2^-(8S+4) relative) are dropped;
@@ -24,6 +24,9 @@
 // contiguous chunk per k-block with a 1-D bulk copy), oz_gemm (warp-specialized: S.X rows by
 // bulk copy -> converter warps cut them into digit planes in shared memory -> one thread
 // issues the tcgen05.mma -> TMEM -> epilogue warps drain to fp64).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -61,6 +64,40 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
                  : "memory");
+}
+// the same arrive on the mbarrier at this offset in every CTA of `mask` (cluster)
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_addr(bar)),
+        "h"(mask)
+        : "memory");
+}
+// 1-D bulk copy landing at the same offset in every CTA of `mask`, completing on each one's
+// mbarrier at `bar`'s offset
+__device__ __forceinline__ void bulk_g2s_mc(void* smem, const void* gmem, unsigned bytes, uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_addr(bar)), "h"(mask)
+        : "memory");
+}
+// TMA tile load of a 2-D tensor: box at (c0 = inner coordinate, r0 = row) -> smem, counted
+// on `bar` (out-of-range elements are zero-filled and still counted)
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int c0, int r0, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_addr(smem)),
+        "l"(map), "r"(c0), "r"(r0), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
     asm volatile(
@@ -129,11 +166,11 @@ __device__ __forceinline__ int oz_exp(unsigned long long amax_bits) {
 // U = Y + O with O = 0x80 in each of the S low bytes; byte b of U minus 128 (= byte ^ 0x80)
 // is digit S-1-b of Y, d in [-128, 127], Y = sum_s d_s 256^(S-1-s).  So one F2I per value
 // and one byte permute per digit: no per-digit arithmetic.  sc = 2^(8S-2-E).
-template <int S>
-__device__ __forceinline__ void oz_digits16(const double (&v)[16], double sc, uint32_t (&dig)[S][4]) {
+template <int S, int NV>
+__device__ __forceinline__ void oz_digits(const double (&v)[NV], double sc, uint32_t (&dig)[S][NV / 4]) {
     constexpr unsigned long long O = 0x0080808080808080ull >> (8 * (7 - S));
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NV / 4; ++q) {
         uint32_t lo[4], hi[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -169,7 +206,7 @@ __global__ void oz_slice(const double* __restrict__ X, int64_t K, int64_t W, int
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) v[kk] = (w < W && k0 + kk < K) ? X[(k0 + kk) * W + w] : 0.0;
         uint32_t dig[S][4];
-        oz_digits16<S>(v, ldexp(1.0, 8 * S - 2 - E), dig);
+        oz_digits<S, 16>(v, ldexp(1.0, 8 * S - 2 - E), dig);
         const int64_t wt = w / R, r = w % R, kb = k0 / OZ_KB, kc = (k0 % OZ_KB) / 16;
         int8_t* base = img + ((wt * nkb + kb) * S) * (int64_t)(R * OZ_KB) + (r / 8) * 256 + kc * 128 + (r % 8) * 16;
 #pragma unroll
@@ -178,46 +215,59 @@ __global__ void oz_slice(const double* __restrict__ X, int64_t K, int64_t W, int
     }
 }
 
-// One CTA: a 128 x 64 tile of Z over k-blocks [kb0, kb1) of its split.
-//   warps 0-3: converters -- read S.X (fp64, straight from HBM/L2) for the stage's 32 x 64
-//              block, cut it into S digit planes in the UMMA image (shared memory);
-//   warps 4-7: epilogue  -- drain the TMEM accumulators (lanes 32(w-4).. = tile rows) into
-//              fp64 registers every OZ_FK values of k, scale and store the partial tile;
-//   warp 8:    producer  -- one 1-D bulk copy of G's digit planes per stage;
-//   warp 9:    MMA       -- one elected thread issues the S(S+1)/2 tcgen05.mma per stage.
 // shared memory: an MMA ring (G planes | S.X planes per stage, freed by the MMA commit) and
-// a deeper ring of raw fp64 S.X rows (freed as soon as the converters hold them in registers)
+// a deeper ring of raw fp64 S.X tiles (freed as soon as the converters hold them in registers)
 constexpr int OZ_RAW = OZ_KB * OZ_NT * 8;
 template <int S>
 constexpr int oz_stage_bytes() { return S * (OZ_MT + OZ_NT) * OZ_KB; }
-template <int S>
-constexpr int oz_stages() { return S >= 6 ? 3 : 4; }
-template <int S>
-constexpr int oz_raw_stages() {
-    return ((220 << 10) - oz_stages<S>() * oz_stage_bytes<S>()) / OZ_RAW < 8
-               ? ((220 << 10) - oz_stages<S>() * oz_stage_bytes<S>()) / OZ_RAW
-               : 8;
-}
-template <int S>
-constexpr size_t oz_smem_bytes() { return (size_t)oz_stages<S>() * oz_stage_bytes<S>() + (size_t)oz_raw_stages<S>() * OZ_RAW + 1024; }
+constexpr int OZ_MAX_RING = 8;
+constexpr int OZ_SMEM_MAX = 225 << 10;  // of the 227 KB opt-in, leaving the static barriers room
+constexpr int OZ_CW = 8;                // converter warps: 256 threads = 64 columns x 4 quarters of k
+constexpr int OZ_THREADS = 32 * (OZ_CW + 7);
 
+// position in a ring of n slots: slot index and the parity of the current pass (no division
+// in the loops: the depths are runtime values)
+struct RingPos {
+    int idx = 0, n;
+    unsigned phase = 0;
+    __device__ explicit RingPos(int n_) : n(n_) {}
+    __device__ void next() {
+        if (++idx == n) {
+            idx = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
+// One CTA: a 128 x 64 tile of Z over k-blocks [kb0, kb1) of its split.
+//   warps 0-7:  converters -- take the k-block's 32 x 64 fp64 S.X tile (TMA-staged, or loaded
+//               directly), cut it into S digit planes in the UMMA image in shared memory;
+//   warps 8-11: epilogue  -- drain the TMEM accumulators (lanes 32(w-8).. = tile rows) every
+//               OZ_FK values of k, scale, and add into the split's partial tile in HBM;
+//   warp 12:    producer  -- G's digit planes, one bulk copy per k-block (multicast across a
+//               cluster of N tiles when csize > 1);
+//   warp 13:    MMA       -- one thread issues the tcgen05.mma, S + S/2 per k-block;
+//   warp 14:    producer  -- the S.X tile, one TMA load per k-block.
 template <int S>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(OZ_THREADS, 1)
 oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const double* __restrict__ sx, int64_t K,
         int64_t d, int64_t nkb, int64_t kb_per_split, const unsigned long long* __restrict__ amax_a,
-        const unsigned long long* __restrict__ amax_b, int64_t m, double* __restrict__ zpart, int staged) {
+        const unsigned long long* __restrict__ amax_b, int64_t m, double* __restrict__ zpart, int staged, int nst,
+        int nrs, int dbg, int csize, const __grid_constant__ CUtensorMap sx_map) {
     constexpr int A_BYTES = S * OZ_MT * OZ_KB;
     constexpr int STAGE = oz_stage_bytes<S>();  // A planes | B planes
-    constexpr int OZ_STAGES = oz_stages<S>(), RS = oz_raw_stages<S>();
-    constexpr int FKB = OZ_FK / OZ_KB;  // k-blocks per accumulation
+    constexpr int FKB = OZ_FK / OZ_KB;           // k-blocks per accumulation
+    constexpr int NCT = 32 * OZ_CW;              // converter threads
+    constexpr int W_EPI = OZ_CW, W_PROD = OZ_CW + 4, W_MMA = OZ_CW + 5, W_RAW = OZ_CW + 6;
+    const int OZ_STAGES = nst, RS = nrs;         // ring depths (<= OZ_MAX_RING each)
     // the dynamic window is only guaranteed 16 B alignment under separate compilation: the
     // ring starts at the next 1 KB boundary (1 KB extra requested); operand images that
     // straddle it produce wrong products
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t* raw_ring = smem + OZ_STAGES * STAGE;
-    __shared__ uint64_t full[OZ_STAGES], bfull[OZ_STAGES], empty[OZ_STAGES], acc_full, acc_empty;
-    __shared__ uint64_t rfull[RS], rempty[RS];
+    __shared__ uint64_t full[OZ_MAX_RING], bfull[OZ_MAX_RING], empty[OZ_MAX_RING], acc_full, acc_empty;
+    __shared__ uint64_t rfull[OZ_MAX_RING], rempty[OZ_MAX_RING];
     __shared__ uint32_t tmem_slot;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -230,142 +280,164 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     if (threadIdx.x == 0) {
         for (int i = 0; i < OZ_STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&bfull[i], 128);
-            mbar_init(&empty[i], 1);
+            mbar_init(&bfull[i], NCT);
+            mbar_init(&empty[i], csize);  // every CTA of the cluster has read the stage
         }
         for (int i = 0; i < RS; ++i) {
             mbar_init(&rfull[i], 1);
-            mbar_init(&rempty[i], 128);
+            mbar_init(&rempty[i], NCT);
         }
         mbar_init(&acc_full, 1);
         mbar_init(&acc_empty, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 9) {
+    if (warp == W_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&tmem_slot))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
+    if (csize > 1) cluster_sync_all();  // barriers initialized cluster-wide before any remote arrive
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
+    // cluster of csize CTAs along the N tiles: same (M tile, split), so the same G planes; each
+    // CTA fetches 1/csize of every G chunk and multicasts it to all of them
+    const unsigned crank = csize > 1 ? cluster_rank() : 0u;
+    const uint16_t cmask = (uint16_t)((1u << csize) - 1u);
 
-    if (warp < 4) {
-        // converter: thread = (column j of the tile, 16-row half kc of the k-block)
-        const int j = threadIdx.x % OZ_NT, kc = threadIdx.x / OZ_NT;
+    if (warp < OZ_CW) {
+        // converter: thread = (column j of the tile, quarter kq of the k-block: 8 values of k)
+        const int j = threadIdx.x % OZ_NT, kq = threadIdx.x / OZ_NT;
         const int64_t col = nt * OZ_NT + j;
         const bool colok = col < d;
         const int F = colok ? oz_exp(amax_b[col]) : 0;
         const double* src = sx + (colok ? col : 0);
         const double sc = ldexp(1.0, 8 * S - 2 - F);
-        const uint32_t soff = (uint32_t)((j / 8) * 256 + kc * 128 + (j % 8) * 16);
-        double cur[16], nxt[16];
-        auto load = [&](int64_t i, double (&v)[16]) {  // direct path: straight from global
-            const int64_t k0 = (kb0 + i) * OZ_KB + kc * 16;
+        // canonical K-major image: 8-row group j/8, 16 B core matrix kq/2, row j%8, byte 8(kq%2)
+        const uint32_t soff = (uint32_t)((j / 8) * 256 + (kq / 2) * 128 + (j % 8) * 16 + (kq % 2) * 8);
+        double cur[8], nxt[8];
+        auto load = [&](int64_t i, double (&v)[8]) {  // direct path: straight from global
+            const int64_t k0 = (kb0 + i) * OZ_KB + kq * 8;
 #pragma unroll
-            for (int kk = 0; kk < 16; ++kk)
-                v[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
+            for (int kk = 0; kk < 8; ++kk) v[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
         };
         if (!staged && nk > 0) load(0, cur);
-        for (int64_t i = 0; i < nk; ++i) {
-            const int st = (int)(i % OZ_STAGES);
-            uint8_t* stage = smem + st * STAGE;
-            if (staged) {
-                const int rt = (int)(i % RS);
-                mbar_wait(&rfull[rt], (unsigned)((i / RS) & 1));
-                const double* raw = reinterpret_cast<const double*>(raw_ring + rt * OZ_RAW) + kc * 16 * OZ_NT + j;
-                const int64_t k0 = (kb0 + i) * OZ_KB + kc * 16;
+        RingPos sp(OZ_STAGES), rp(RS);
+        for (int64_t i = 0; i < nk; ++i, sp.next(), rp.next()) {
+            uint8_t* stage = smem + sp.idx * STAGE;
+            if (staged) {  // TMA zero-fills past K and d
+                mbar_wait(&rfull[rp.idx], rp.phase);
+                const double* raw = reinterpret_cast<const double*>(raw_ring + rp.idx * OZ_RAW) + kq * 8 * OZ_NT + j;
 #pragma unroll
-                for (int kk = 0; kk < 16; ++kk) cur[kk] = (colok && k0 + kk < K) ? raw[kk * OZ_NT] : 0.0;
-                mbar_arrive(&rempty[rt]);  // rows in registers: the raw slot may refill
+                for (int kk = 0; kk < 8; ++kk) cur[kk] = raw[kk * OZ_NT];
             } else {
                 if (i + 1 < nk) load(i + 1, nxt);
             }
-            if (i >= OZ_STAGES) mbar_wait(&empty[st], (unsigned)(((i / OZ_STAGES) - 1) & 1));
-            uint32_t dig[S][4];
-            oz_digits16<S>(cur, sc, dig);
-            uint8_t* bp = stage + A_BYTES + soff;  // (the MMAs of k-block i - STAGES are done)
+            uint32_t dig[S][2];
+            if (dbg & 1) {  // measurement only: skip the digit arithmetic
 #pragma unroll
-            for (int s = 0; s < S; ++s)
-                *reinterpret_cast<uint4*>(bp + s * OZ_NT * OZ_KB) = make_uint4(dig[s][0], dig[s][1], dig[s][2], dig[s][3]);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> MMA reads
-            mbar_arrive(&bfull[st]);
+                for (int s2 = 0; s2 < S; ++s2)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) dig[s2][q] = (uint32_t)__double_as_longlong(cur[4 * q]) >> s2;
+            } else {
+                oz_digits<S, 8>(cur, sc, dig);
+            }
+            if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);  // MMAs of k-block i - STAGES done
+            uint8_t* bp = stage + A_BYTES + soff;
+#pragma unroll
+            for (int s = 0; s < S; ++s) *reinterpret_cast<uint2*>(bp + s * OZ_NT * OZ_KB) = make_uint2(dig[s][0], dig[s][1]);
+            // one proxy fence orders both this thread's generic accesses before the async
+            // proxy: the plane writes before the MMA reads them, and the raw-tile reads before
+            // the next TMA overwrite of that slot (releasing the slot before a fence raced at
+            // S = 6; a second fence per k-block cost c5 0.7 ms)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&bfull[sp.idx]);
+            if (staged) mbar_arrive(&rempty[rp.idx]);
             if (!staged) {
 #pragma unroll
-                for (int kk = 0; kk < 16; ++kk) cur[kk] = nxt[kk];
+                for (int kk = 0; kk < 8; ++kk) cur[kk] = nxt[kk];
             }
         }
-    } else if (warp < 8) {
-        // epilogue: drain each accumulation into fp64 registers (row = lane of this warp)
-        const int ew = warp - 4;
-        double acc[OZ_NT];
-#pragma unroll
-        for (int j = 0; j < OZ_NT; ++j) acc[j] = 0.0;
+    } else if (warp < W_PROD) {
+        // epilogue: every accumulation's integer groups -> fp64 (smallest weight first), scaled
+        // by 2^(E_r + F_j) (exact), added into the split's partial tile (row = lane)
+        const int ew = warp - W_EPI;
         const uint32_t trow = tmem + ((uint32_t)(ew * 32) << 16);
+        const int64_t r = mt * OZ_MT + ew * 32 + lane;
+        const bool rok = r < m;
+        const int Er = rok ? oz_exp(amax_a[r]) : 0;
+        double* zp = zpart + split * m * d;
         for (int64_t c = 0; c < nchunks; ++c) {
             mbar_wait(&acc_full, (unsigned)(c & 1));
             tc_fence_after();
-#pragma unroll
+#pragma unroll 1
             for (int q = 0; q < OZ_NT / 16; ++q) {
+                double part[16];
 #pragma unroll
-                for (int p = S - 1; p >= 0; --p) {  // smallest weight first
+                for (int jj = 0; jj < 16; ++jj) part[jj] = 0.0;
+#pragma unroll
+                for (int p = S - 1; p >= 0; --p) {
                     int v[16];
                     tmem_ld16(trow + (uint32_t)(p * OZ_NT + q * 16), v);
                     const double wgt = ldexp(1.0, -8 * p - 12);
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[q * 16 + j] = fma((double)v[j], wgt, acc[q * 16 + j]);
+                    for (int jj = 0; jj < 16; ++jj) part[jj] = fma((double)v[jj], wgt, part[jj]);
+                }
+                if (rok) {
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const int64_t col = nt * OZ_NT + q * 16 + jj;
+                        if (col < d) {
+                            const double v = ldexp(part[jj], Er + oz_exp(amax_b[col]));
+                            zp[col * m + r] = c == 0 ? v : zp[col * m + r] + v;
+                        }
+                    }
                 }
             }
             tc_fence_before();
             mbar_arrive(&acc_empty);
         }
-        const int64_t r = mt * OZ_MT + ew * 32 + lane;
-        if (r < m) {
-            const int Er = oz_exp(amax_a[r]);
-            double* zp = zpart + split * m * d;
-#pragma unroll
-            for (int j = 0; j < OZ_NT; ++j) {
-                const int64_t col = nt * OZ_NT + j;
-                if (col < d) zp[col * m + r] = ldexp(acc[j], Er + oz_exp(amax_b[col]));
-            }
-        }
-    } else if (warp == 8) {
+    } else if (warp == W_PROD) {
         if (lane == 0) {  // producer: G's digit planes, one bulk copy per stage
             const int8_t* ga = aimg + (mt * a_nkb + a_kb0 + kb0) * (int64_t)A_BYTES;
-            for (int64_t i = 0; i < nk; ++i) {
-                const int st = (int)(i % OZ_STAGES);
-                if (i >= OZ_STAGES) mbar_wait(&empty[st], (unsigned)(((i / OZ_STAGES) - 1) & 1));
-                mbar_arrive_expect_tx(&full[st], A_BYTES);
-                bulk_g2s(smem + st * STAGE, ga + i * A_BYTES, A_BYTES, &full[st]);
+            RingPos sp(OZ_STAGES);
+            for (int64_t i = 0; i < nk; ++i, sp.next()) {
+                if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);
+                mbar_arrive_expect_tx(&full[sp.idx], A_BYTES);
+                if (csize > 1) {
+                    const unsigned part = A_BYTES / csize;
+                    bulk_g2s_mc(smem + sp.idx * STAGE + crank * part, ga + i * A_BYTES + crank * part, part,
+                                &full[sp.idx], cmask);
+                } else {
+                    bulk_g2s(smem + sp.idx * STAGE, ga + i * A_BYTES, A_BYTES, &full[sp.idx]);
+                }
             }
         }
         __syncwarp();
-    } else if (warp == 10) {
-        if (staged) {  // producer: the block's S.X rows (lane r copies row r) into the raw ring
-            const int64_t c0 = nt * OZ_NT;
-            const unsigned row_bytes = (unsigned)((d - c0 < OZ_NT ? d - c0 : OZ_NT) * 8);
-            for (int64_t i = 0; i < nk; ++i) {
-                const int rt = (int)(i % RS);
-                const int64_t k0 = (kb0 + i) * OZ_KB;
-                const int rows = (int)(K - k0 < OZ_KB ? K - k0 : OZ_KB);
-                if (i >= RS) mbar_wait(&rempty[rt], (unsigned)(((i / RS) - 1) & 1));
-                if (lane == 0) mbar_arrive_expect_tx(&rfull[rt], (unsigned)rows * row_bytes);
-                __syncwarp();
-                if (lane < rows)
-                    bulk_g2s(raw_ring + rt * OZ_RAW + lane * (OZ_NT * 8), sx + (k0 + lane) * d + c0, row_bytes, &rfull[rt]);
+    } else if (warp == W_RAW) {
+        if (staged && lane == 0) {  // producer: the block's 32 x 64 fp64 S.X tile, one TMA load
+            // (32 row-sized bulk copies cost ~64 cycles of issue each: they bounded the GEMM)
+            RingPos rp(RS);
+            for (int64_t i = 0; i < nk; ++i, rp.next()) {
+                if (i >= RS) mbar_wait(&rempty[rp.idx], rp.phase ^ 1u);
+                mbar_arrive_expect_tx(&rfull[rp.idx], OZ_RAW);
+                tma_load_2d(raw_ring + rp.idx * OZ_RAW, &sx_map, (int)(nt * OZ_NT), (int)((kb0 + i) * OZ_KB),
+                            &rfull[rp.idx]);
             }
         }
-    } else if (warp == 9) {
+        __syncwarp();
+    } else if (warp == W_MMA) {
         if (lane == 0) {  // MMA issuer
             const unsigned sbase = smem_addr(smem);
-            for (int64_t i = 0; i < nk; ++i) {
-                const int st = (int)(i % OZ_STAGES);
+            RingPos sp(OZ_STAGES);
+            for (int64_t i = 0; i < nk; ++i, sp.next()) {
+                const int st = sp.idx;
                 const int64_t c = i / FKB;
                 const bool first = (i % FKB) == 0;
                 if (first && c > 0) mbar_wait(&acc_empty, (unsigned)((c - 1) & 1));  // drained
-                mbar_wait(&full[st], (unsigned)((i / OZ_STAGES) & 1));
-                mbar_wait(&bfull[st], (unsigned)((i / OZ_STAGES) & 1));
+                mbar_wait(&full[st], sp.phase);
+                mbar_wait(&bfull[st], sp.phase);
                 tc_fence_after();
                 const unsigned sa = sbase + st * STAGE, sb = sa + A_BYTES;
                 // A plane s against B planes t0 .. t0+w-1 in one MMA: the planes sit
@@ -374,7 +446,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 // N = 256 per instruction: S(S+1)/2 products in ~S + S/2 instructions (an
                 // N = 64 MMA costs ~3x its share of the tensor pipe, tools/microbench/umma_i8.cu).
 #pragma unroll
-                for (int s = 0; s < S; ++s)
+                for (int s = 0; s < ((dbg & 2) ? 1 : S); ++s)
 #pragma unroll
                     for (int t0 = 0; t0 < S - s; t0 += 4) {
                         const int w = S - s - t0 < 4 ? S - s - t0 : 4;
@@ -382,7 +454,10 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                                umma_desc(sb + t0 * OZ_NT * OZ_KB), oz_idesc(OZ_MT, OZ_NT * w),
                                (first && s == 0) ? 0 : 1);
                     }
-                mma_commit(&empty[st]);  // stage free once these MMAs have read it
+                if (csize > 1)
+                    mma_commit_mc(&empty[st], cmask);  // stage free in every CTA's view
+                else
+                    mma_commit(&empty[st]);  // stage free once these MMAs have read it
                 if ((i % FKB) == FKB - 1 || i == nk - 1) mma_commit(&acc_full);
             }
         }
@@ -390,7 +465,8 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 9) {
+    if (csize > 1) cluster_sync_all();  // no CTA leaves while its peers may still multicast into it
+    if (warp == W_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
@@ -466,19 +542,71 @@ void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     unsigned long long* amax_b = (unsigned long long*)ctx->oz_b.get(sizeof(unsigned long long) * (size_t)d);
     CGX_CUDA(cudaMemsetAsync(amax_b, 0, sizeof(unsigned long long) * (size_t)d, s));
     run_absmax(ctx, sx, K, d, amax_b, s);
-    // one wave: one CTA per SM
-    int64_t splits = ctx->num_sms / (tm * tn);
+    // ring depths: the MMA ring as configured (default 3 stages at S >= 6, else 4), the raw
+    // S.X ring takes what is left (<= 8)
+    int nst = ctx->opt_oz_st > 0 ? (int)ctx->opt_oz_st : (S >= 6 ? 3 : 4);
+    const int64_t stage_bytes = oz_stage_bytes<S>();
+    if (nst > OZ_MAX_RING) nst = OZ_MAX_RING;
+    while (nst > 2 && nst * stage_bytes + 2 * OZ_RAW + 1024 > OZ_SMEM_MAX) --nst;
+    int nrs = (int)((OZ_SMEM_MAX - 1024 - nst * stage_bytes) / OZ_RAW);
+    if (ctx->opt_oz_rs > 0 && ctx->opt_oz_rs < nrs) nrs = (int)ctx->opt_oz_rs;
+    if (nrs > OZ_MAX_RING) nrs = OZ_MAX_RING;
+    const size_t smem = (size_t)(nst * stage_bytes + nrs * OZ_RAW + 1024);
+    // S.X tiles staged by TMA when its rows are 16 B aligned (a tensor map of the K x d
+    // row-major block; boxes of 32 rows x 64 columns, zero-filled past the edges)
+    CUtensorMap sx_map;
+    memset(&sx_map, 0, sizeof(sx_map));
+    int staged = ctx->opt_oz_staged && d % 2 == 0 && ((uintptr_t)sx % 16) == 0 && K < (1ll << 31);
+    if (staged) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                encode = nullptr;
+        }
+        const cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)K};
+        const cuuint64_t gstride[1] = {(cuuint64_t)d * 8};
+        const cuuint32_t box[2] = {OZ_NT, OZ_KB}, estride[2] = {1, 1};
+        staged = encode && encode(&sx_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)sx, gdim, gstride, box, estride,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    CGX_CUDA(cudaFuncSetAttribute(oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // clusters along the N tiles share G's planes by multicast: the GEMM is bound by the
+    // operand traffic out of L2, and every N tile otherwise re-reads the same G chunks
+    int csize = (int)ctx->opt_oz_cluster;
+    while (csize > 1 && tn % csize) csize >>= 1;
+    if (csize < 1) csize = 1;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = (unsigned)csize;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // one wave: as many splits as co-resident clusters allow (clusters must fit in a GPC)
+    int64_t resident = ctx->num_sms;
+    if (csize > 1) {
+        cfg.gridDim = dim3((unsigned)tm, (unsigned)tn, 1);
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, oz_gemm<S>, &cfg) == cudaSuccess && nclusters > 0)
+            resident = (int64_t)nclusters * csize;
+        cudaGetLastError();
+    }
+    int64_t splits = resident / (tm * tn);
     if (splits < 1) splits = 1;
     if (splits > nkb) splits = nkb;
     const int64_t kps = (nkb + splits - 1) / splits;
     splits = (nkb + kps - 1) / kps;
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
-    const size_t smem = oz_smem_bytes<S>();
-    // rows of S.X staged by bulk copies when every row segment is 16 B aligned
-    const int staged = ctx->opt_oz_staged && d % 2 == 0 && ((uintptr_t)sx % 16) == 0;
-    CGX_CUDA(cudaFuncSetAttribute(oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    oz_gemm<S><<<dim3((unsigned)tm, (unsigned)tn, (unsigned)splits), 352, smem, s>>>(
-        aimg, a_nkb, a_kb0, sx, K, d, nkb, kps, amax_a, amax_b, m, zpart, staged);
+    cfg.gridDim = dim3((unsigned)tm, (unsigned)tn, (unsigned)splits);
+    CGX_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm<S>, aimg, a_nkb, a_kb0, sx, K, d, nkb, kps, amax_a, amax_b, m, zpart,
+                                staged, nst, nrs, (int)ctx->opt_oz_dbg, csize, sx_map));
     count_launch(ctx);
     check_launch("oz_gemm");
     launch_reduce_splits(ctx, zpart, splits, m * d, z, s);

@@ -56,6 +56,11 @@ def main():
         zr = sx.t() @ g
         err = ((z - zr).norm() / zr.norm()).item()
         print(f"check {B},{m},{d} {a.opt}: rel Frobenius err vs cuBLAS fp64 {err:.3e}  max abs {(z - zr).abs().max().item():.3e}")
+        if err > 1e-10:  # per 64-column tile of Z (rows of the (d, m) tensor) and 128-row tile
+            for c0 in range(0, d, 64):
+                for r0 in range(0, m, 128):
+                    zt, rt = z[c0:c0 + 64, r0:r0 + 128], zr[c0:c0 + 64, r0:r0 + 128]
+                    print(f"  tile cols {c0}.. rows {r0}..: {((zt - rt).norm() / rt.norm()).item():.3e}")
 
 
 if __name__ == "__main__":
