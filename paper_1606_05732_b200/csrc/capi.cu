@@ -118,6 +118,7 @@ struct CallScope {
     cudaStream_t st;
     std::lock_guard<std::recursive_mutex> lock;
     CallScope(cgx_ctx* c, void* stream) : ctx(c), st(stream ? (cudaStream_t)stream : c->stream), lock(c->mu) {
+        ctx->oz_colmax_for = nullptr;  // column maxima left by a sketch are valid within one call only
         CGX_CUDA(cudaSetDevice(ctx->device));
         CGX_CUDA(cudaStreamWaitEvent(st, ctx->done, 0));
     }

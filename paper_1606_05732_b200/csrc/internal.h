@@ -93,7 +93,9 @@ struct cgx_ctx {
     int64_t opt_oz_dbg = 0;                 // option "oz_dbg": measurement-only shortcuts (1 no digits, 2 one MMA)
     int64_t opt_oz_st = 0, opt_oz_rs = 0;   // options "oz_st"/"oz_rs": ring depths of the tcgen05 stage 2 (0 = auto)
     int64_t opt_oz_staged = 1;              // option "oz_staged": S.X rows reach the converters by bulk copy (0 = loads)
-    cgx::DevBuf oz_max, oz_a, oz_b;         // ozgemm.cu scratch: scales, digit images of G and S.X
+    cgx::DevBuf oz_max, oz_a, oz_b;         // (oz_b: column maxima of S.X)
+    const double* oz_colmax_for = nullptr;  // S.X whose column maxima the sketch left in oz_b
+    int64_t oz_colmax_d = 0;         // ozgemm.cu scratch: scales, digit images of G and S.X
 };
 
 struct cgx_xform {
@@ -201,6 +203,7 @@ bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* 
 bool launch_gemm_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const double* sx, int64_t d,
                        double* z, cudaStream_t s);
 void oz_drop_image(cgx_xform* xf);  // whenever G changes or goes
+bool oz_stage2_applies(const cgx_ctx* ctx, const cgx_xform* xf, int64_t d);
 // dgemm.cu: row-major fp32 (pitch ld) -> contiguous row-major fp64
 void launch_widen_f32(cgx_ctx* ctx, const float* src, int64_t ld, int64_t n, int64_t d, double* dst, cudaStream_t s);
 void launch_inverse_normal_cdf(cgx_ctx* ctx, const double* p, double* out, int64_t count, int* bad,

@@ -538,10 +538,14 @@ void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
         a_nkb = nkb;
         a_kb0 = 0;
     }
-    // column maxima of S.X
+    // column maxima of S.X: already folded in by the sketch that produced it (the CSR gather),
+    // or one pass here
     unsigned long long* amax_b = (unsigned long long*)ctx->oz_b.get(sizeof(unsigned long long) * (size_t)d);
-    CGX_CUDA(cudaMemsetAsync(amax_b, 0, sizeof(unsigned long long) * (size_t)d, s));
-    run_absmax(ctx, sx, K, d, amax_b, s);
+    if (!(ctx->oz_colmax_for == sx && ctx->oz_colmax_d == d && b0 == 0 && b1 == xf->B)) {
+        CGX_CUDA(cudaMemsetAsync(amax_b, 0, sizeof(unsigned long long) * (size_t)d, s));
+        run_absmax(ctx, sx, K, d, amax_b, s);
+    }
+    ctx->oz_colmax_for = nullptr;
     // ring depths: the MMA ring as configured (default 3 stages at S >= 6, else 4), the raw
     // S.X ring takes what is left (<= 8)
     int nst = ctx->opt_oz_st > 0 ? (int)ctx->opt_oz_st : (S >= 6 ? 3 : 4);
@@ -622,11 +626,19 @@ void oz_drop_image(cgx_xform* xf) {
     xf->oz_gS = 0;
 }
 
+bool oz_stage2_applies(const cgx_ctx* ctx, const cgx_xform* xf, int64_t d) {
+    const int64_t S = ctx->opt_oz_slices;
+    return S >= 3 && S <= 7 && xf->g_dev && xf->m <= 4096 && d >= 1 && d <= 4096 &&
+           xf->m * d >= ctx->opt_oz_min_z;  // small Z: the split-K DMMA stream is faster
+}
+
 bool launch_gemm_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const double* sx, int64_t d,
                        double* z, cudaStream_t s) {
     const int S = (int)ctx->opt_oz_slices;
-    if (S <= 0 || !xf->g_dev || xf->m > 4096 || d > 4096 || b1 <= b0 || d < 1) return false;
-    if (xf->m * d < ctx->opt_oz_min_z) return false;  // small Z: the split-K DMMA stream is faster
+    if (!oz_stage2_applies(ctx, xf, d) || b1 <= b0) {
+        ctx->oz_colmax_for = nullptr;
+        return false;
+    }
     switch (S) {
         case 3: run_ozaki<3>(ctx, xf, b0, b1, sx, d, z, s); return true;
         case 4: run_ozaki<4>(ctx, xf, b0, b1, sx, d, z, s); return true;

@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
                                                        const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
                                                        double* __restrict__ sx, int cbits, int G, int64_t B1,
                                                        unsigned long long* __restrict__ next_task,
-                                                       unsigned long long task_base) {
+                                                       unsigned long long task_base,
+                                                       unsigned long long* __restrict__ colmax) {
     constexpr int kW = CGX_CSR_KW;
     extern __shared__ double smem[];
     __shared__ uint8_t s_tbl[8][32];
@@ -209,8 +210,14 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
     double* acc = smem + (size_t)wid * d;
     uint8_t* tag = reinterpret_cast<uint8_t*>(smem + (size_t)warps_per_cta * d) + (size_t)wid * d;
     uint8_t* tbl = s_tbl[wid];
-
-    (void)warps_per_cta;
+    // optional: per-column max |S.X| for the tensor-core stage 2's scales (ozgemm.cu), kept
+    // per CTA in shared memory and folded into `colmax` once at exit
+    unsigned long long* cmax = reinterpret_cast<unsigned long long*>(
+        smem + (((size_t)warps_per_cta * d * 9 + 7) / 8));
+    if (colmax) {
+        for (int64_t j = threadIdx.x; j < d; j += blockDim.x) cmax[j] = 0;
+        __syncthreads();
+    }
     const int64_t ng0 = B1 / G;
     const int64_t ntasks = ng0 + (B - B1);
     for (;;) {
@@ -301,9 +308,20 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
             }
         }
         __syncwarp();
-        for (int64_t j = lane; j < d; j += 32) sx[b * d + j] = acc[j];
+        for (int64_t j = lane; j < d; j += 32) {
+            sx[b * d + j] = acc[j];
+            if (colmax) {  // (a plain read first: after the first buckets the max rarely moves)
+                const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(acc[j]));
+                if (u > *(volatile unsigned long long*)&cmax[j]) atomicMax(&cmax[j], u);
+            }
+        }
         __syncwarp();
       }
+    }
+    if (colmax) {
+        __syncthreads();
+        for (int64_t j = threadIdx.x; j < d; j += blockDim.x)
+            if (cmax[j]) atomicMax(&colmax[j], cmax[j]);
     }
 }
 
@@ -329,7 +347,15 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
         int wl = (int)((96 * 1024) / per_warp_l);
         wl = wl > 8 ? 8 : wl;
         if (wl >= 1) {
-            const size_t sm = per_warp_l * wl + 8;
+            // column maxima for the tensor-core stage 2 when it will run on this S.X
+            unsigned long long* colmax = nullptr;
+            if (oz_stage2_applies(ctx, xf, d)) {
+                colmax = (unsigned long long*)ctx->oz_b.get(sizeof(unsigned long long) * (size_t)d);
+                CGX_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * (size_t)d, s));
+                ctx->oz_colmax_for = sx;
+                ctx->oz_colmax_d = d;
+            }
+            const size_t sm = (per_warp_l * wl + 7) / 8 * 8 + (colmax ? sizeof(unsigned long long) * (size_t)d : 8);
             auto lk = sketch_csr_lean<TV, TI>;
             CGX_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             int per_sm = 0;
@@ -348,7 +374,7 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
             B1 = B1 < 0 ? 0 : B1 / G * G;
             const unsigned long long base = take_tasks(ctx, B1 / G + xf->B - B1, nb * wl);
             lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, cb, (int)G, B1,
-                                                 ctx->task_ctr, base);
+                                                 ctx->task_ctr, base, colmax);
             count_launch(ctx);
             tasks_launched(ctx, s);
             check_launch("sketch_csr_lean");
