@@ -235,7 +235,7 @@ int cgx_gen_csr_zipf(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double s
 
 /* ---- instrumentation ---------------------------------------------------------------- */
 /* Context options (kernel variants for A/B runs; every variant gives the same S.X bits and
- * Z to rounding):
+ * Z to rounding -- "oz_slices" below 7 trades Z accuracy for speed, as stated):
  *   "g_resident"   1 (default): countgauss_new materializes G (<= 4 GiB) and applies read
  *                  it; 0: G is generated inside the apply kernels.  Set before construction.
  *   "fuse"         1 (default): the one-pass dense kernel (sketch + G + contraction) when G
@@ -246,7 +246,18 @@ int cgx_gen_csr_zipf(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double s
  *   "csr_mode"     0/1 (default): bucket-ordered row gather; 2: stable two-level partition.
  *   "gemm_ws"      0 (default): cp.async-pipelined DMMA stage 2; 1: warp-specialized
  *                  bulk-copy producer (large Z whose tiles divide it).
- *   "rows_per_task", "grid_waves", "ws_gw": scheduling knobs of the dense kernels. */
+ *   "oz_slices"    stage 2 (gemm, matrix.cpp:111-129) on the tcgen05 int8 tensor cores with
+ *                  FP64 emulated by S planes of 8-bit digits (ozgemm.cu): 7 (default; Z within
+ *                  ~1e-14 of fp64), 6 (~7e-13), 5 (~1.5e-10), 3-4; 0 = always the FP64 DMMA
+ *                  stage 2.  Used when G is in memory and m*d >= "oz_min_z" (16384 default;
+ *                  smaller Z streams faster through the split-K DMMA kernel).
+ *   "oz_staged"    1 (default): S.X tiles reach the converter warps by TMA; 0: direct loads.
+ *   "oz_cluster"   1 (default), 2, 4, 8: CTAs sharing G's digit planes by multicast.
+ *   "oz_st", "oz_rs": ring depths of the tensor-core stage 2 (0 = automatic).
+ *   "gemm_tile", "gemm_chunks": DMMA stage-2 tiling (128x128 one-pass default; 1 = 8-warp
+ *                  tiles / 48 MB G chunks).
+ *   "rows_per_task", "grid_waves", "ws_gw", "tail_tasks": scheduling knobs of the sketch
+ *                  kernels. */
 int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched so far. */
 uint64_t cgx_launch_count(const cgx_ctx* ctx);
