@@ -252,6 +252,8 @@ int cgx_gen_csr_zipf(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double s
  *                  stage 2.  Used when G is in memory and m*d >= "oz_min_z" (16384 default;
  *                  smaller Z streams faster through the split-K DMMA kernel).
  *   "oz_staged"    1 (default): S.X tiles reach the converter warps by TMA; 0: direct loads.
+ *   "pdl"          1 (default): stage-2 kernels are programmatic dependent launches (their
+ *                  CTAs start while the sketch drains); 0: ordinary stream order.
  *   "oz_cluster"   1 (default), 2, 4, 8: CTAs sharing G's digit planes by multicast.
  *   "oz_st", "oz_rs": ring depths of the tensor-core stage 2 (0 = automatic).
  *   "gemm_tile", "gemm_chunks": DMMA stage-2 tiling (128x128 one-pass default; 1 = 8-warp

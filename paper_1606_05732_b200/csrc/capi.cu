@@ -1223,6 +1223,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_gemm_tile = value;
         else if (k == "oz_slices" && (value == 0 || (value >= 3 && value <= 7)))
             ctx->opt_oz_slices = value;
+        else if (k == "pdl" && (value == 0 || value == 1))
+            ctx->opt_pdl = value;
         else if (k == "oz_cluster" && (value == 1 || value == 2 || value == 4 || value == 8))
             ctx->opt_oz_cluster = value;
         else if (k == "oz_dbg" && value >= 0 && value <= 3)

@@ -161,6 +161,13 @@ __device__ __forceinline__ float datagen_normal(uint64_t seed, uint64_t e) {
 #undef CGX_M
 #undef CGX_A
 
+// ---- programmatic dependent launch: a dependent kernel (launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization) may be scheduled once every CTA of the
+// running kernel has called pdl_trigger (or exited); it calls pdl_wait before touching the
+// running kernel's results (returns at once when the kernel was launched normally) ----------
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- shared-memory mbarriers (producer/consumer hand-off between warp roles) ----------
 __device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {

@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(32 * WGM * WGN * KG,
               double* __restrict__ C, int accumulate) {
     constexpr int BM = 8 * FM * WGM, BN = 8 * FN * WGN, NT = 32 * WGM * WGN * KG;
     constexpr int LDA = BM + 4, LDB = BN + 4;  // padding: 2-wavefront fragment loads
+    pdl_trigger();
+    pdl_wait();  // S.X (and the partials) of the kernel before are complete
     static_assert(KG == 1 || KG == 2 || KG == 4, "BK = 16 has 4 k4-steps");
     extern __shared__ double dsm[];
     double* As = dsm;                          // [STAGES][BK][LDA]
@@ -379,8 +381,12 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
             Ach = gbuf;
         }
         const int64_t sp = (cols + kps - 1) / kps;  // splits that have work in this chunk
-        kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), nthreads, smem, s>>>(Ach, m, sx + c0 * d, d, cols, kps,
-                                                                                     zpart, first ? 0 : 1);
+        if (ws)
+            kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), nthreads, smem, s>>>(Ach, m, sx + c0 * d, d, cols,
+                                                                                         kps, zpart, first ? 0 : 1);
+        else
+            launch_pdl(ctx, kern, dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), dim3(nthreads), smem, s, Ach, m,
+                       sx + c0 * d, d, cols, kps, zpart, first ? 0 : 1);
         count_launch(ctx);
         check_launch("gemm_dmma");
         if (first && sp < splits)  // splits without work in the first chunk start at zero

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(256) gauss_gemm_kernel(const double* __restric
 constexpr int kRedGroups = 16;
 __global__ void __launch_bounds__(32 * kRedGroups) reduce_splits(const double* __restrict__ zpart, int64_t splits,
                                                                  int64_t md, double* __restrict__ z) {
+    pdl_wait();  // the partials of the kernel before are complete
     __shared__ double part[kRedGroups][33];
     const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int64_t e = (int64_t)blockIdx.x * 32 + lane;
@@ -305,7 +306,7 @@ void launch_materialize_t(cgx_ctx* ctx, const cgx_xform* xf, double* t, cudaStre
 
 void launch_reduce_splits(cgx_ctx* ctx, const double* zpart, int64_t splits, int64_t md, double* z, cudaStream_t s) {
     const int64_t blocks = (md + 31) / 32;
-    reduce_splits<<<(unsigned)blocks, 32 * kRedGroups, 0, s>>>(zpart, splits, md, z);
+    launch_pdl(ctx, reduce_splits, dim3((unsigned)blocks), dim3(32 * kRedGroups), 0, s, zpart, splits, md, z);
     count_launch(ctx);
     check_launch("reduce_splits");
 }

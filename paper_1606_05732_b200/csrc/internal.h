@@ -87,6 +87,7 @@ struct cgx_ctx {
     int64_t opt_gemm_chunks = 0;            // option "gemm_chunks": 1 = 48 MB K-chunks even when G is in memory
     int64_t opt_g_resident = 1;             // option "g_resident": materialize seeded G at construction (<= 4 GiB)
     cgx::DevBuf part[6];                    // csr_partition.cu scratch: counters, payload copies, row keys
+    int64_t opt_pdl = 1;                    // option "pdl": stage-2 kernels launched as programmatic dependents
     int64_t opt_oz_slices = 7;              // option "oz_slices": stage 2 on tcgen05 int8 with S digit planes (0 = DMMA)
     int64_t opt_oz_min_z = 16384;           // option "oz_min_z": smallest m*d that takes the tcgen05 stage 2
     int64_t opt_oz_cluster = 1;             // option "oz_cluster": CTAs sharing G's planes by multicast (1, 2, 4, 8)
@@ -247,6 +248,23 @@ void exclusive_scan_u32(cgx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t
 void exclusive_scan_i64(cgx_ctx* ctx, const int64_t* in, int64_t* out, int64_t count, cudaStream_t s);
 
 inline void count_launch(cgx_ctx* ctx, int k = 1) { ctx->launches += (uint64_t)k; }
+// Launch as a programmatic dependent of the previous kernel in the stream (option "pdl"): its
+// CTAs start while that kernel's last CTAs drain and wait in pdl_wait for its results.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(cgx_ctx* ctx, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = ctx->opt_pdl ? 1 : 0;
+    CGX_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
+}
 void* pool_alloc(cgx_ctx* ctx, size_t bytes);
 void pool_free(cgx_ctx* ctx, void* p);
 void check_launch(const char* what);

@@ -276,6 +276,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     const int64_t kb1 = kb0 + kb_per_split < nkb ? kb0 + kb_per_split : nkb;
     const int64_t nk = kb1 - kb0;
     const int64_t nchunks = (nk + FKB - 1) / FKB;
+    pdl_trigger();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < OZ_STAGES; ++i) {
@@ -301,6 +302,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     if (csize > 1) cluster_sync_all();  // barriers initialized cluster-wide before any remote arrive
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
+    pdl_wait();  // S.X and its column maxima (the sketch before) are complete
     // cluster of csize CTAs along the N tiles: same (M tile, split), so the same G planes; each
     // CTA fetches 1/csize of every G chunk and multicasts it to all of them
     const unsigned crank = csize > 1 ? cluster_rank() : 0u;
@@ -583,7 +585,7 @@ void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     while (csize > 1 && tn % csize) csize >>= 1;
     if (csize < 1) csize = 1;
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cfg.blockDim = dim3(OZ_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -591,8 +593,10 @@ void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = (unsigned)csize;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = ctx->opt_pdl ? 2 : 1;
     // one wave: as many splits as co-resident clusters allow (clusters must fit in a GPC)
     int64_t resident = ctx->num_sms;
     if (csize > 1) {

@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
                                                        unsigned long long task_base,
                                                        unsigned long long* __restrict__ colmax) {
     constexpr int kW = CGX_CSR_KW;
+    pdl_trigger();  // stage 2 may be scheduled as these CTAs drain
     extern __shared__ double smem[];
     __shared__ uint8_t s_tbl[8][32];
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

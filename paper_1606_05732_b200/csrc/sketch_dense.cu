@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ 
                                                           int64_t nchunks, int G, int64_t B1, double* __restrict__ sx,
                                                           unsigned long long* __restrict__ next_task,
                                                           unsigned long long task_base) {
+    pdl_trigger();  // stage 2 may be scheduled as these CTAs drain
     constexpr int CW = 32 * V;
     extern __shared__ __align__(16) unsigned char dsm[];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
