@@ -185,6 +185,12 @@ def test_dense_bit_exact_shapes(cg, restatement, d, dtype, order):
     z_ref, sx_ref = restatement.countgauss(seed, m, B, x=x)
     assert np.array_equal(cg.countsketch_apply(t, x), sx_ref)
     assert rel_fro(cg.countgauss_apply(t, x), z_ref) <= Z_TOL
+    # the gather's column maxima belong to its own call: a later stage 2 on other (larger)
+    # S.X must compute its own scales
+    cg.countsketch_apply(t, x)
+    big = np.random.default_rng(6).standard_normal((B, d)) * 1e6
+    _, _, gs = restatement.countgauss_seeds(2024)
+    assert rel_fro(cg.api.gauss_gemm(t, big), restatement.gemm(restatement.gaussian(gs, m, B), big)) <= Z_TOL
 
 
 def test_integer_exactness_and_linearity(cg, reference):
@@ -456,6 +462,23 @@ def test_stage2_ozaki_bucket_ranges(cg, restatement, b0, b1, ozaki):
     check(lib.cgx_gauss_gemm_range(ctx.h, t._xf.h, sl.ctypes.data, b0, b1, d, CGX_MEM_HOST, z.ctypes.data,
                                    CGX_MEM_HOST, None))
     assert rel_fro(z, restatement.gemm(np.asfortranarray(G[:, b0:b1]), sl)) <= Z_TOL
+
+
+@pytest.mark.parametrize("r0,r1", [(0, 130), (64, 130), (3, 100)])
+def test_stage2_ozaki_g_rows(cg, restatement, r0, r1, ozaki):
+    """Rows [r0, r1) of Z (the multi-GPU "g" combine) through the tensor-core stage 2: the rows
+    of G form a temporary view whose digit image is built per call, never cached on the
+    transform (which keeps its own image of all of G)."""
+    ozaki(7)
+    m, d, B = 130, 200, 5000
+    sx = np.random.default_rng(r0).standard_normal((B, d))
+    t = cg.countgauss_new(m, B, 10, cg.SeededRng(7))
+    _, _, gs = restatement.countgauss_seeds(7)
+    G = restatement.gaussian(gs, m, B)
+    zr = cg.api.gauss_gemm_rows(t, sx, r0, r1)
+    assert rel_fro(zr, restatement.gemm(np.asfortranarray(G[r0:r1]), sx)) <= Z_TOL
+    z = cg.api.gauss_gemm(t, sx)  # the full Z afterwards still uses the full G
+    assert rel_fro(z, restatement.gemm(G, sx)) <= Z_TOL
 
 
 def test_ozaki_full_apply_csr(cg, restatement, ozaki):
