@@ -1227,8 +1227,6 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_pdl = value;
         else if (k == "oz_cluster" && (value == 1 || value == 2 || value == 4 || value == 8))
             ctx->opt_oz_cluster = value;
-        else if (k == "oz_dbg" && value >= 0 && value <= 3)
-            ctx->opt_oz_dbg = value;
         else if (k == "oz_st" && value >= 0 && value <= 8)
             ctx->opt_oz_st = value;
         else if (k == "oz_rs" && value >= 0 && value <= 8)

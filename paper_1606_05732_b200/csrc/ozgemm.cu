@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const double* __restrict__ sx, int64_t K,
         int64_t d, int64_t nkb, int64_t kb_per_split, const unsigned long long* __restrict__ amax_a,
         const unsigned long long* __restrict__ amax_b, int64_t m, double* __restrict__ zpart, int staged, int nst,
-        int nrs, int dbg, int csize, const __grid_constant__ CUtensorMap sx_map) {
+        int nrs, int csize, const __grid_constant__ CUtensorMap sx_map) {
     constexpr int A_BYTES = S * OZ_MT * OZ_KB;
     constexpr int STAGE = oz_stage_bytes<S>();  // A planes | B planes
     constexpr int FKB = OZ_FK / OZ_KB;           // k-blocks per accumulation
@@ -337,14 +337,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 if (i + 1 < nk) load(i + 1, nxt);
             }
             uint32_t dig[S][2];
-            if (dbg & 1) {  // measurement only: skip the digit arithmetic
-#pragma unroll
-                for (int s2 = 0; s2 < S; ++s2)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) dig[s2][q] = (uint32_t)__double_as_longlong(cur[4 * q]) >> s2;
-            } else {
-                oz_digits<S, 8>(cur, sc, dig);
-            }
+            oz_digits<S, 8>(cur, sc, dig);
             if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);  // MMAs of k-block i - STAGES done
             uint8_t* bp = stage + A_BYTES + soff;
 #pragma unroll
@@ -448,7 +441,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 // N = 256 per instruction: S(S+1)/2 products in ~S + S/2 instructions (an
                 // N = 64 MMA costs ~3x its share of the tensor pipe, tools/microbench/umma_i8.cu).
 #pragma unroll
-                for (int s = 0; s < ((dbg & 2) ? 1 : S); ++s)
+                for (int s = 0; s < S; ++s)
 #pragma unroll
                     for (int t0 = 0; t0 < S - s; t0 += 4) {
                         const int w = S - s - t0 < 4 ? S - s - t0 : 4;
@@ -614,7 +607,7 @@ void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
     cfg.gridDim = dim3((unsigned)tm, (unsigned)tn, (unsigned)splits);
     CGX_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm<S>, aimg, a_nkb, a_kb0, sx, K, d, nkb, kps, amax_a, amax_b, m, zpart,
-                                staged, nst, nrs, (int)ctx->opt_oz_dbg, csize, sx_map));
+                                staged, nst, nrs, csize, sx_map));
     count_launch(ctx);
     check_launch("oz_gemm");
     launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
