@@ -226,6 +226,31 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------------- our arm
+def stage2_line(args, m, B, d, gemm_ms):
+    """Stage 2 (Z = G.(S.X)) against its own roofline: the int8 tcgen05 kernel (ozgemm.cu)
+    for large Z -- S(S+1)/2 digit products of 2*m*B*d int8 ops each, against the nominal
+    dense int8 rate (4.5 POPS; MEASURED_PEAKS.json holds no int8 figure) -- else the FP64
+    DMMA kernels against the measured 37.2 TFLOP/s DMMA peak."""
+    if gemm_ms <= 0:
+        return None
+    opts = dict(o.split("=", 1) for o in args.opt)
+    S = int(opts.get("oz_slices", 7))
+    min_z = int(opts.get("oz_min_z", 16384))
+    g_mem = m * B * 8 <= (4 << 30) and opts.get("g_resident", "1") != "0"
+    fp64_flop = 2.0 * m * B * d
+    if S > 0 and g_mem and m * d >= min_z and m <= 4096 and d <= 4096:
+        ops = S * (S + 1) / 2 * fp64_flop
+        tops = ops / (gemm_ms / 1e3) / 1e12
+        return {"kernel": f"oz_gemm<{S}> (tcgen05.mma kind::i8, FP64 emulated by {S} digit planes)",
+                "bound": "tensor", "achieved": tops, "peak": 4500.0, "unit": "int8 TOPS", "frac": tops / 4500.0,
+                "peak_source": "nominal dense int8 (B200)", "fp64_equiv_tflops": fp64_flop / (gemm_ms / 1e3) / 1e12,
+                "ms": gemm_ms}
+    tf = fp64_flop / (gemm_ms / 1e3) / 1e12
+    return {"kernel": "gemm_dmma (FP64 DMMA, mma.sync m8n8k4)", "bound": "tensor", "achieved": tf, "peak": 37.2,
+            "unit": "TFLOP/s", "frac": tf / 37.2, "peak_source": "measured DMMA (tools/microbench/fp64_peak.cu)",
+            "ms": gemm_ms}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -517,6 +542,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": kernel_name,
                          "bytes_per_launch": bytes_alg, "peak_source": peak_kind},
+            "stage2": stage2_line(args, m, B, d, gm_ms / max(gm_n, 1)),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
