@@ -499,7 +499,7 @@ void build_g_image(cgx_ctx* ctx, const double* g, int64_t m, int64_t K, unsigned
 }
 
 template <int S>
-void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const double* sx, int64_t d, double* z,
+bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const double* sx, int64_t d, double* z,
                cudaStream_t s) {
     const int64_t m = xf->m, K = b1 - b0;
     const int64_t nkb = (K + OZ_KB - 1) / OZ_KB;
@@ -515,8 +515,15 @@ void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
         if (mx->oz_gS != S) {
             oz_drop_image(mx);
             const int64_t fkb = (xf->B + OZ_KB - 1) / OZ_KB;
-            CGX_CUDA(cudaMalloc((void**)&mx->oz_gimg, (size_t)(S * mp * fkb * OZ_KB)));
-            CGX_CUDA(cudaMalloc((void**)&mx->oz_gmax, sizeof(unsigned long long) * (size_t)m));
+            // (7/8 of G's bytes; if HBM cannot hold it, stage 2 stays on the FP64 DMMA pipe)
+            if (cudaMalloc((void**)&mx->oz_gimg, (size_t)(S * mp * fkb * OZ_KB)) != cudaSuccess ||
+                cudaMalloc((void**)&mx->oz_gmax, sizeof(unsigned long long) * (size_t)m) != cudaSuccess) {
+                cudaGetLastError();
+                if (mx->oz_gimg) cudaFree(mx->oz_gimg);
+                mx->oz_gimg = nullptr;
+                mx->oz_gmax = nullptr;
+                return false;
+            }
             build_g_image<S>(ctx, xf->g_dev, m, xf->B, mx->oz_gmax, mx->oz_gimg, s);
             mx->oz_gS = S;
         }
@@ -611,6 +618,7 @@ void run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     count_launch(ctx);
     check_launch("oz_gemm");
     launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
+    return true;
 }
 
 } // namespace
@@ -637,11 +645,11 @@ bool launch_gemm_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1
         return false;
     }
     switch (S) {
-        case 3: run_ozaki<3>(ctx, xf, b0, b1, sx, d, z, s); return true;
-        case 4: run_ozaki<4>(ctx, xf, b0, b1, sx, d, z, s); return true;
-        case 5: run_ozaki<5>(ctx, xf, b0, b1, sx, d, z, s); return true;
-        case 6: run_ozaki<6>(ctx, xf, b0, b1, sx, d, z, s); return true;
-        case 7: run_ozaki<7>(ctx, xf, b0, b1, sx, d, z, s); return true;
+        case 3: return run_ozaki<3>(ctx, xf, b0, b1, sx, d, z, s);
+        case 4: return run_ozaki<4>(ctx, xf, b0, b1, sx, d, z, s);
+        case 5: return run_ozaki<5>(ctx, xf, b0, b1, sx, d, z, s);
+        case 6: return run_ozaki<6>(ctx, xf, b0, b1, sx, d, z, s);
+        case 7: return run_ozaki<7>(ctx, xf, b0, b1, sx, d, z, s);
         default: return false;
     }
 }
