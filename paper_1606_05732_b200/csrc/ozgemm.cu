@@ -37,7 +37,6 @@ constexpr int OZ_MT = 128;    // MMA M (rows of G per CTA tile = TMEM lanes)
 constexpr int OZ_NT = 64;     // MMA N (columns of S.X per CTA tile)
 constexpr int OZ_KB = 32;     // k per MMA (int8: 32 bytes)
 constexpr int OZ_FK = 16384;  // k per int32 accumulation before the drain to fp64
-constexpr int OZ_MAXS = 7;
 
 // ---- tcgen05 / TMEM wrappers ----------------------------------------------------------
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
