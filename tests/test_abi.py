@@ -98,3 +98,35 @@ def test_null_arguments_rejected():
     assert lib.cgx_countgauss_new(None, 1, 1, 1, 1, None) == CGX_EINVAL
     assert b"null context" in lib.cgx_last_error()
     assert lib.cgx_xform_info(None, None, None, None, None, None, None) == CGX_EINVAL
+
+
+def test_library_carries_tcgen05_int8_and_tma():
+    """The stage-2 tensor-core kernel is compiled in: tcgen05 int8 MMAs (UTCIMMA), TMEM loads
+    and TMA/bulk copies appear in the sm_100a SASS of libcgx.so."""
+    import shutil
+    import subprocess
+
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    lib = os.path.join(os.path.dirname(__file__), "..", "paper_1606_05732_b200", "libcgx.so")
+    sass = subprocess.run([cuobjdump, "-sass", lib], capture_output=True, text=True).stdout
+    for mnemonic in ("UTCIMMA", "UTMALDG", "UBLKCP"):
+        assert mnemonic in sass, mnemonic
+
+
+def test_bench_stage2_roofline_line():
+    """bench.py's stage-2 roofline object: the tcgen05 path for large Z (int8 digit products
+    against the nominal int8 rate), the DMMA path otherwise."""
+    import argparse
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    big = bench.stage2_line(argparse.Namespace(opt=[]), 256, 1 << 20, 512, 4.0)
+    assert big["unit"] == "int8 TOPS" and abs(big["achieved"] - 28 * 2.0 * 256 * (1 << 20) * 512 / 4e-3 / 1e12) < 1e-6
+    assert abs(big["fp64_equiv_tflops"] - 2.0 * 256 * (1 << 20) * 512 / 4e-3 / 1e12) < 1e-9
+    small = bench.stage2_line(argparse.Namespace(opt=[]), 64, 65536, 32, 0.03)
+    assert small["unit"] == "TFLOP/s" and "DMMA" in small["kernel"]
+    off = bench.stage2_line(argparse.Namespace(opt=["oz_slices=0"]), 256, 1 << 20, 512, 8.0)
+    assert off["unit"] == "TFLOP/s"
+    assert bench.stage2_line(argparse.Namespace(opt=[]), 256, 1 << 20, 512, 0.0) is None
