@@ -221,7 +221,12 @@ template <int S>
 constexpr int oz_stage_bytes() { return S * (OZ_MT + OZ_NT) * OZ_KB; }
 constexpr int OZ_MAX_RING = 8;
 constexpr int OZ_SMEM_MAX = 225 << 10;  // of the 227 KB opt-in, leaving the static barriers room
-constexpr int OZ_CW = 8;                // converter warps: 256 threads = 64 columns x 4 quarters of k
+#ifndef OZ_CONVERTER_WARPS
+#define OZ_CONVERTER_WARPS 8
+#endif
+constexpr int OZ_CW = OZ_CONVERTER_WARPS;   // converter warps: 32 * OZ_CW threads = 64 columns x k-groups
+constexpr int OZ_VPT = OZ_KB * OZ_NT / (32 * OZ_CW);  // values of k per converter thread (8 or 4)
+static_assert(OZ_VPT == 8 || OZ_VPT == 4, "converter warps: 8 or 16");
 constexpr int OZ_THREADS = 32 * (OZ_CW + 7);
 
 // position in a ring of n slots: slot index and the parity of the current pass (no division
@@ -308,20 +313,21 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     const uint16_t cmask = (uint16_t)((1u << csize) - 1u);
 
     if (warp < OZ_CW) {
-        // converter: thread = (column j of the tile, quarter kq of the k-block: 8 values of k)
+        // converter: thread = (column j of the tile, k-group kq of the k-block: OZ_VPT values of k)
         const int j = threadIdx.x % OZ_NT, kq = threadIdx.x / OZ_NT;
         const int64_t col = nt * OZ_NT + j;
         const bool colok = col < d;
         const int F = colok ? oz_exp(amax_b[col]) : 0;
         const double* src = sx + (colok ? col : 0);
         const double sc = ldexp(1.0, 8 * S - 2 - F);
-        // canonical K-major image: 8-row group j/8, 16 B core matrix kq/2, row j%8, byte 8(kq%2)
-        const uint32_t soff = (uint32_t)((j / 8) * 256 + (kq / 2) * 128 + (j % 8) * 16 + (kq % 2) * 8);
-        double cur[8], nxt[8];
-        auto load = [&](int64_t i, double (&v)[8]) {  // direct path: straight from global
-            const int64_t k0 = (kb0 + i) * OZ_KB + kq * 8;
+        // canonical K-major image: 8-row group j/8, 16 B core matrix, row j%8, byte within it
+        const int kofs = kq * OZ_VPT;
+        const uint32_t soff = (uint32_t)((j / 8) * 256 + (kofs / 16) * 128 + (j % 8) * 16 + (kofs % 16));
+        double cur[OZ_VPT], nxt[OZ_VPT];
+        auto load = [&](int64_t i, double (&v)[OZ_VPT]) {  // direct path: straight from global
+            const int64_t k0 = (kb0 + i) * OZ_KB + kofs;
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) v[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
+            for (int kk = 0; kk < OZ_VPT; ++kk) v[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
         };
         if (!staged && nk > 0) load(0, cur);
         RingPos sp(OZ_STAGES), rp(RS);
@@ -329,18 +335,23 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             uint8_t* stage = smem + sp.idx * STAGE;
             if (staged) {  // TMA zero-fills past K and d
                 mbar_wait(&rfull[rp.idx], rp.phase);
-                const double* raw = reinterpret_cast<const double*>(raw_ring + rp.idx * OZ_RAW) + kq * 8 * OZ_NT + j;
+                const double* raw = reinterpret_cast<const double*>(raw_ring + rp.idx * OZ_RAW) + kofs * OZ_NT + j;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) cur[kk] = raw[kk * OZ_NT];
+                for (int kk = 0; kk < OZ_VPT; ++kk) cur[kk] = raw[kk * OZ_NT];
             } else {
                 if (i + 1 < nk) load(i + 1, nxt);
             }
-            uint32_t dig[S][2];
-            oz_digits<S, 8>(cur, sc, dig);
+            uint32_t dig[S][OZ_VPT / 4];
+            oz_digits<S, OZ_VPT>(cur, sc, dig);
             if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);  // MMAs of k-block i - STAGES done
             uint8_t* bp = stage + A_BYTES + soff;
 #pragma unroll
-            for (int s = 0; s < S; ++s) *reinterpret_cast<uint2*>(bp + s * OZ_NT * OZ_KB) = make_uint2(dig[s][0], dig[s][1]);
+            for (int s = 0; s < S; ++s) {
+                if constexpr (OZ_VPT == 8)
+                    *reinterpret_cast<uint2*>(bp + s * OZ_NT * OZ_KB) = make_uint2(dig[s][0], dig[s][1]);
+                else
+                    *reinterpret_cast<uint32_t*>(bp + s * OZ_NT * OZ_KB) = dig[s][0];
+            }
             // one proxy fence orders both this thread's generic accesses before the async
             // proxy: the plane writes before the MMA reads them, and the raw-tile reads before
             // the next TMA overwrite of that slot (releasing the slot before a fence raced at
@@ -350,7 +361,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             if (staged) mbar_arrive(&rempty[rp.idx]);
             if (!staged) {
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) cur[kk] = nxt[kk];
+                for (int kk = 0; kk < OZ_VPT; ++kk) cur[kk] = nxt[kk];
             }
         }
     } else if (warp < W_PROD) {
