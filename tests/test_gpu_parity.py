@@ -437,6 +437,33 @@ def test_stage2_tensor_core_ozaki(cg, restatement, m, d, B, S, staged, ozaki):
     assert rel_fro(z, restatement.gemm(G2, sx)) <= OZ_TOL[S]
 
 
+@pytest.mark.parametrize("cluster,rs,st", [(1, 2, 0), (2, 2, 0), (4, 2, 0), (8, 6, 2), (2, 1, 4)])
+def test_stage2_ozaki_cluster_and_rings(cg, restatement, cluster, rs, st, ozaki):
+    """The tensor-core stage 2 with G's planes multicast across 1/2/4/8-CTA clusters and other
+    ring depths: same Z (the partial sums do not depend on the launch shape's sharing)."""
+    from paper_1606_05732_b200._lib import CGX_MEM_HOST, check, lib
+
+    ozaki(7)
+    ctx = cg.context()
+    ctx.set_option("oz_cluster", cluster)
+    ctx.set_option("oz_rs", rs)
+    ctx.set_option("oz_st", st)
+    try:
+        m, d, B = 256, 512, 30011
+        sx = np.random.default_rng(cluster).standard_normal((B, d))
+        t = cg.countgauss_new(m, B, 10, cg.SeededRng(11))
+        _, _, gs = restatement.countgauss_seeds(11)
+        G = restatement.gaussian(gs, m, B)
+        z = np.empty((m, d), order="F")
+        check(lib.cgx_gauss_gemm_range(ctx.h, t._xf.h, np.ascontiguousarray(sx).ctypes.data, 0, B, d, CGX_MEM_HOST,
+                                       z.ctypes.data, CGX_MEM_HOST, None))
+        assert rel_fro(z, restatement.gemm(G, sx)) <= Z_TOL
+    finally:
+        ctx.set_option("oz_cluster", 2)
+        ctx.set_option("oz_rs", 2)
+        ctx.set_option("oz_st", 0)
+
+
 @pytest.mark.parametrize("b0,b1", [(0, 4096), (64, 3000), (33, 4000), (4001, 4096)])
 def test_stage2_ozaki_bucket_ranges(cg, restatement, b0, b1, ozaki):
     """Stage 2 over a bucket slice (the multi-GPU "sx" combine): aligned slices read the
