@@ -26,7 +26,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -41,7 +40,8 @@ CONFIGS = {
     "c1": dict(kind="dense", n=65536, d=8, B=2048, m=16, dtype="f64"),
     "c2": dict(kind="dense", n=1 << 24, d=32, B=65536, m=64, dtype="f32"),
     "c3": dict(kind="csr", n=1 << 26, d=256, B=262144, m=128, density=0.01),
-    "c4": dict(kind="dense", n=1 << 25, d=128, B=131072, m=32, dtype="f32"),
+    "c4": dict(kind="dense", n=1 << 25, d=128, B=131072, m=32, dtype="f32", gen="separable", r=16, alpha=0.5,
+               sigma=0.01),
     "c5": dict(kind="csr", n=1 << 27, d=512, B=1 << 20, m=256, zipf=(1.5, 512, 1.1)),
 }
 
@@ -55,6 +55,10 @@ def mix64(a, b):
 
 
 def workload_name(cfg_name, c):
+    if c.get("gen") == "separable":
+        return (f"{cfg_name}: near-separable dense X {c['n']}x{c['d']} f32 row-major = max(A.[I_{c['r']}|H] + "
+                f"N(0,{c['sigma']}^2), 0), H Dirichlet({c['alpha']}); cg_nmf: CountGauss B={c['B']}, m={c['m']} "
+                f"+ anchor selection")
     if c["kind"] == "dense":
         return (f"{cfg_name}: dense X {c['n']}x{c['d']} {c['dtype']} row-major, CountGauss B={c['B']}, "
                 f"m={c['m']}")
@@ -63,6 +67,11 @@ def workload_name(cfg_name, c):
         return (f"{cfg_name}: CSR X {c['n']}x{c['d']} row lengths Zipf({s_len}) cap {cap}, columns Zipf({s_col}), "
                 f"fp32/int32, B={c['B']}, m={c['m']}")
     return f"{cfg_name}: CSR X {c['n']}x{c['d']} Bernoulli({c['density']}) fp32/int32, B={c['B']}, m={c['m']}"
+
+
+def data_seed(cfg_name):
+    """Seed of a config's synthetic X: mix64(s0, config id)."""
+    return mix64(SEED, int(cfg_name[1:]))
 
 
 def units_of(c, nnz=None):
@@ -79,61 +88,64 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 50 ms during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every ~0.5 ms
+    on a side thread while the timed region runs (a c2 step is 0.42 ms, so a 50 ms
+    nvidia-smi poll would see nothing).  Raises if NVML cannot be read at all."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake_slowdown": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
     def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        import pynvml as nv
+
+        self.nv = nv
+        nv.nvmlInit()
+        self.h = None
+        try:  # the CUDA ordinal's physical GPU, by PCI bus id (CUDA_VISIBLE_DEVICES-safe)
+            import torch
+
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+        self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        self.samples = []
+        self.reasons = 0
+        self.stop = threading.Event()
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+
+    def _run(self):
+        while not self.stop.is_set():
+            self._sample()
+            time.sleep(0.0005)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-            t0 = time.time()  # the timed region starts only once sampling is live
-            while not self.lines and time.time() - t0 < 5.0:
-                time.sleep(0.01)
-        except Exception:
-            self.proc = None
+        self._sample()  # fails loudly here if NVML is unusable
+        self.samples.clear()
+        self.reasons = 0
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join()
+        if not self.samples:
+            self._sample()
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines[1:]:  # lines[0] was taken before the timed region began
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        nv = self.nv
+        names = sorted(k for k, attr in self.REASONS.items() if self.reasons & int(getattr(nv, attr, 0)))
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples), "how": "NVML every ~0.5 ms during the timed region"}
 
 
 # ---------------------------------------------------------------- CPU baseline (reference)
@@ -152,14 +164,23 @@ def cpu_reference_run(cfg_name, c, steps, warmup):
     t0 = time.time()
     xf = R.countgauss_new(c["m"], c["B"], c["n"], t_seed_rng)
     construct_s = time.time() - t0
-    xm = R.dense_generated(c["n"], c["d"], mix64(SEED, 2), O)
+    if c.get("gen") == "separable":
+        xm = R.dense_separable_generated(c["n"], c["d"], data_seed(cfg_name), O, r=c["r"], alpha=c["alpha"],
+                                         sigma=c["sigma"])
+    else:
+        xm = R.dense_generated(c["n"], c["d"], data_seed(cfg_name), O)
+    # cgref_time_apply runs one untimed call, then the timed ones; the first (warmup - 1)
+    # timed samples are discarded too, so `warmup` untimed calls precede the kept samples
     ms, _ = xf.time_apply(xm, 1, max(1, steps + warmup - 1))
     ms = list(ms)[warmup - 1:] if warmup > 1 else list(ms)
     med = statistics.median(ms)
     units = c["n"] * c["d"]
+    what = "countgauss_apply (cg_nmf's product; its countgauss_new is outside the step on both arms)" \
+        if c.get("gen") == "separable" else "countgauss_apply"
     return dict(value=units / (med / 1e3), ms=ms, median_ms=med, cores=cores, construct_s=construct_s,
-                sample=(f"full {cfg_name}: countgauss_apply on fp64 column-major X (the reference layout), "
-                        f"{len(ms)} timed calls after warm-up, median; reference CSR/dense code as-is"))
+                warmup=max(warmup, 1),
+                sample=(f"full {cfg_name}: {what} on fp64 column-major X (the reference layout), "
+                        f"{len(ms)} timed calls after {max(warmup, 1)} warm-up calls, median; reference code as-is"))
 
 
 def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000):
@@ -177,9 +198,9 @@ def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000):
     rows = int(min(c["n"], max(1024, sample_nnz / mean)))
     if "zipf" in c:
         s_len, cap, s_col = c["zipf"]
-        x = bench_data.csr_zipf(rows, c["d"], seed=mix64(SEED, 5), s_len=s_len, cap=cap, s_col=s_col)
+        x = bench_data.csr_zipf(rows, c["d"], seed=data_seed(cfg_name), s_len=s_len, cap=cap, s_col=s_col)
     else:
-        x = bench_data.csr_bernoulli(rows, c["d"], c["density"], seed=mix64(SEED, 3))
+        x = bench_data.csr_bernoulli(rows, c["d"], c["density"], seed=data_seed(cfg_name))
     rp = x.row_offsets.cpu().numpy()
     ci = x.col_indices.cpu().numpy().astype(np.int64)
     vv = x.values.cpu().numpy().astype(np.float64)
@@ -197,7 +218,7 @@ def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000):
     nnz_full = c.get("nnz_full") or nnz_s * (c["n"] / rows)
     est_ms = t_sk * nnz_full / nnz_s + max(0.0, t_all - t_sk)
     return dict(value=nnz_full / (est_ms / 1e3), ms=[est_ms] * reps, median_ms=est_ms, cores=cores,
-                construct_s=construct_s,
+                construct_s=construct_s, warmup=1,
                 sample=(f"{cfg_name} rows 0..{rows} ({nnz_s} nnz) through the reference's countgauss_apply "
                         f"(serial CSR branch + OpenMP gemm): apply {t_all:.0f} ms, sketch {t_sk:.0f} ms, median of "
                         f"{reps}; full size extrapolated as sketch x nnz ratio + gemm"))
@@ -210,10 +231,10 @@ def run_reference_arm(args):
     c = CONFIGS[args.config]
     # each CPU step is a full c2 countgauss_apply (~0.1-0.3 s on a multi-core host): bound
     # the sample so the whole arm ends within a few minutes
-    r = cpu_reference_run(args.config, c, min(args.steps, 20), min(max(args.warmup, 1), 2))
+    r = cpu_reference_run(args.config, c, min(args.steps, 20), min(max(args.warmup, 1), 3))
     line = {
         "metric": METRIC, "impl": "reference", "value": r["value"], "unit": "nnz/s", "n_gpus": args.gpus,
-        "steps": len(r["ms"]), "warmup": args.warmup, "ms_per_step": r["median_ms"], "higher_is_better": True,
+        "steps": len(r["ms"]), "warmup": r["warmup"], "ms_per_step": r["median_ms"], "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config, c), "layout": "fp64 column-major (reference DenseMatrix)"},
         "cpu_baseline": {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "reference",
@@ -309,22 +330,28 @@ def run_ours(args):
         rows = grows.numel()
     if c["kind"] == "dense" and hash_place:
         dt = torch.float32 if c["dtype"] == "f32" else torch.float64
-        x = bench_data.dense_normal_rows(grows, d, seed=mix64(SEED, 2), dtype=dt, device=local)
+        if c.get("gen") == "separable":
+            raise SystemExit("--placement hash: not for the separable generator")
+        x = bench_data.dense_normal_rows(grows, d, seed=data_seed(args.config), dtype=dt, device=local)
         nnz_local = rows * d
         x_bytes = rows * d * x.element_size()
         del grows
     elif c["kind"] == "dense":
         dt = torch.float32 if c["dtype"] == "f32" else torch.float64
-        x = bench_data.dense_normal(rows, d, seed=mix64(SEED, 2), dtype=dt, row0=r0, device=local)
+        if c.get("gen") == "separable":
+            x = bench_data.dense_separable(rows, d, seed=data_seed(args.config), r=c["r"], alpha=c["alpha"],
+                                           sigma=c["sigma"], dtype=dt, row0=r0, device=local)
+        else:
+            x = bench_data.dense_normal(rows, d, seed=data_seed(args.config), dtype=dt, row0=r0, device=local)
         nnz_local = rows * d
         x_bytes = rows * d * x.element_size()
     else:
         if "zipf" in c:
             s_len, cap, s_col = c["zipf"]
-            x = bench_data.csr_zipf(rows, d, seed=mix64(SEED, 5) + r0, s_len=s_len, cap=cap, s_col=s_col,
+            x = bench_data.csr_zipf(rows, d, seed=data_seed(args.config) + r0, s_len=s_len, cap=cap, s_col=s_col,
                                     device=local)
         else:
-            x = bench_data.csr_bernoulli(rows, d, c["density"], seed=mix64(SEED, 3) + r0, device=local)
+            x = bench_data.csr_bernoulli(rows, d, c["density"], seed=data_seed(args.config) + r0, device=local)
         nnz_local = x.nnz()
         x_bytes = nnz_local * 8 + (rows + 1) * 8
     torch.cuda.synchronize()
@@ -385,9 +412,17 @@ def run_ours(args):
         return out
 
     timing_combine = False
+    nmf = c.get("gen") == "separable"
+    anchors = []
+
+    def full_step():
+        zz = step()
+        if nmf:  # cg_nmf (nmf.cpp:141-153): the anchors of Z, read back to the host
+            anchors.append(cg.select_extremes(zz, ctx=ctx))
+        return zz
 
     for _ in range(args.warmup):
-        step()
+        full_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -401,7 +436,7 @@ def run_ours(args):
         timing_combine = world > 1
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            full_step()
         ev1.record(stream)
         torch.cuda.synchronize()
         timing_combine = False
@@ -533,6 +568,9 @@ def run_ours(args):
                       if c["m"] * c["B"] * 8 <= (4 << 30) and not any(o.startswith("g_resident=0") for o in args.opt)
                       else "generated inside the apply kernels"),
                 "options": args.opt,
+                **({"anchors": anchors[-1].unioned, "anchors_stable": all(a == anchors[-1] for a in anchors),
+                    "step": "countgauss_apply + select_extremes (cg_nmf without its countgauss_new)"}
+                   if nmf else {}),
                 "stage_ms": {"sketch": sk_avg_ms, "gemm": gm_ms / max(gm_n, 1),
                              **({"combine": sum(a.elapsed_time(b) for a, b in comb_ev) / len(comb_ev),
                                  "combine_what": "rank 0: the NCCL collectives"

@@ -233,6 +233,20 @@ int cgx_gen_csr_bernoulli(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, dou
 int cgx_gen_csr_zipf(cgx_ctx* ctx, uint64_t seed, int64_t n, int64_t d, double s_len, int64_t cap, double s_col,
                      int64_t* rowptr_dev, int32_t* cols_dev, float* vals_dev, int64_t* nnz_out, void* stream);
 
+/* Config 4 (BASELINE configs[3]): near-separable nonnegative X for NMF anchor selection,
+ * X = max(A.[I_r | H] + sigma*N(0,1), 0) with A (n x r) uniform on [0,1) and the columns of
+ * H (r x (d-r)) drawn from Dirichlet(alpha): every non-anchor column of X is a convex
+ * combination of the r anchor columns 0..r-1, plus clipped noise.  Rows [row0, row0+n) of
+ * the matrix defined by `seed`; fp32 arithmetic without FMA (CPU twin in
+ * oracle/cgoracle.c).  No reference counterpart: generate_separable (nmf.cpp:12-44) mixes
+ * with normalized uniforms and has no noise. */
+int cgx_gen_separable(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int64_t r, double alpha,
+                      double sigma, int dtype, int layout, void* x_dev, void* stream);
+/* The mixing weights H of cgx_gen_separable (r x cols, column-major, fp64, host): column c
+ * is Dirichlet(alpha), the normalized Marsaglia-Tsang Gamma(alpha) draws of
+ * SeededRng(mix64(seed, 13)).  Pure host function (no context, no GPU). */
+int cgx_separable_mixing(uint64_t seed, int64_t r, int64_t cols, double alpha, double* h);
+
 /* ---- instrumentation ---------------------------------------------------------------- */
 /* Context options (kernel variants for A/B runs; every variant gives the same S.X bits and
  * Z to rounding -- "oz_slices" below 7 trades Z accuracy for speed, as stated):

@@ -87,6 +87,10 @@ class Restatement:
         L.cgo_normal_f32.argtypes = [_U64, _U64]
         L.cgo_gen_dense_f32.argtypes = [_U64, _I64, _I64, _P]
         L.cgo_gen_dense_f64_colmajor.argtypes = [_U64, _I64, _I64, _P]
+        L.cgo_sketch_csr_buckets.argtypes = [_P, _P, _I64, _I64, _P, _P, C.c_int, _P, C.c_int, _I64, _I64, _P]
+        L.cgo_gen_separable_f64_colmajor.argtypes = [_U64, _I64, _I64, _I64, _D, _D, _P]
+        L.cgo_separable_mixing.argtypes = [_U64, _I64, _I64, _D, _P]
+        L.cgo_gen_separable_f32.argtypes = [_U64, _I64, _I64, _I64, _I64, _D, _D, _P]
 
     def mix64(self, a, b):
         return int(self.lib.cgo_mix64(a, b))
@@ -138,6 +142,18 @@ class Restatement:
                                 int(vals.dtype == np.float32), n, d, _ptr(out))
         return out.T
 
+    def sketch_csr_buckets(self, hash_, sign, b0, b1, rowptr, cols, vals, n, d):
+        """Rows [b0, b1) of the serial CSR S.X (bit-identical to the full result's rows)."""
+        rowptr = np.ascontiguousarray(rowptr, np.int64)
+        cols = np.ascontiguousarray(cols)
+        vals = np.ascontiguousarray(vals)
+        out = np.empty((d, b1 - b0), np.float64)
+        self.lib.cgo_sketch_csr_buckets(_ptr(np.ascontiguousarray(hash_, np.int64)),
+                                        _ptr(np.ascontiguousarray(sign, np.float64)), b0, b1, _ptr(rowptr),
+                                        _ptr(cols), int(cols.dtype == np.int64), _ptr(vals),
+                                        int(vals.dtype == np.float32), n, d, _ptr(out))
+        return out.T
+
     def gemm(self, a, b):
         a = np.asfortranarray(a, np.float64)
         b = np.asfortranarray(b, np.float64)
@@ -176,6 +192,18 @@ class Restatement:
     def gen_dense_f32(self, seed, n, d):
         x = np.empty((n, d), np.float32)
         self.lib.cgo_gen_dense_f32(seed, n, d, _ptr(x))
+        return x
+
+    def separable_mixing(self, seed, r, cols, alpha=0.5):
+        """H (r x cols) of the config-4 generator: Dirichlet(alpha) columns."""
+        h = np.empty((cols, r), np.float64)
+        self.lib.cgo_separable_mixing(seed, r, cols, alpha, _ptr(h))
+        return h.T
+
+    def gen_separable_f32(self, seed, n, d, r=16, alpha=0.5, sigma=0.01, row0=0):
+        """Rows [row0, row0+n) of the config-4 near-separable X, row-major fp32."""
+        x = np.empty((n, d), np.float32)
+        self.lib.cgo_gen_separable_f32(seed, row0, n, d, r, alpha, sigma, _ptr(x))
         return x
 
 
@@ -284,6 +312,25 @@ class Reference:
         data = C.c_void_p()
         self._check(self.lib.cgref_dense_alloc(n, d, C.byref(h), C.byref(data)))
         restatement.lib.cgo_gen_dense_f64_colmajor(seed, n, d, data)
+        return RefMatrix(self, h, False, n, d)
+
+    def dense_alloc(self, n, d):
+        """A zero n x d DenseMatrix held by the reference and a writable numpy view of its
+        column-major storage (d x n, row j = column j), filled in place by the caller so a
+        multi-GB input is never held twice."""
+        h = C.c_void_p()
+        data = C.c_void_p()
+        self._check(self.lib.cgref_dense_alloc(n, d, C.byref(h), C.byref(data)))
+        view = np.ctypeslib.as_array((C.c_double * (n * d)).from_address(data.value)).reshape(d, n)
+        return RefMatrix(self, h, False, n, d), view
+
+    def dense_separable_generated(self, n, d, seed, restatement, r=16, alpha=0.5, sigma=0.01):
+        """n x d DenseMatrix filled in place with config 4's near-separable X
+        (cgo_gen_separable_f64_colmajor, the twin of the GPU generator)."""
+        h = C.c_void_p()
+        data = C.c_void_p()
+        self._check(self.lib.cgref_dense_alloc(n, d, C.byref(h), C.byref(data)))
+        restatement.lib.cgo_gen_separable_f64_colmajor(seed, n, d, r, alpha, sigma, data)
         return RefMatrix(self, h, False, n, d)
 
     def csr(self, rowptr, cols, vals, n, d):

@@ -228,3 +228,129 @@ void cgo_gen_dense_f64_colmajor(uint64_t seed, int64_t n, int64_t d, double* x) 
     for (int64_t j = 0; j < d; ++j)
         for (int64_t i = 0; i < n; ++i) x[j * n + i] = (double)cgo_normal_f32(seed, (uint64_t)(i * d + j));
 }
+
+/* ---- config 4: near-separable X (twin of csrc/datagen.cu gen_separable_kernel and
+ * separable_mixing; BASELINE configs[3]) ---------------------------------------------
+ * Mixing weights: column c of H (r x cols, column-major) is Dirichlet(alpha), the
+ * normalized Marsaglia-Tsang Gamma(alpha) draws of the sequential stream
+ * SeededRng(mix64(seed, 13)); normals there are Acklam's rational (src/rng.cpp:13-41). */
+static double sep_gamma(uint64_t seed, uint64_t* k, double alpha) {
+    if (alpha < 1.0) {
+        double g = sep_gamma(seed, k, alpha + 1.0);
+        double u = uniform53(cgo_draw(seed, (*k)++));
+        return g * pow(u, 1.0 / alpha);
+    }
+    double dm = alpha - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * dm);
+    for (;;) {
+        double z = acklam(uniform53(cgo_draw(seed, (*k)++)));
+        double v = 1.0 + c * z;
+        if (v <= 0.0) continue;
+        v = v * v * v;
+        double u = uniform53(cgo_draw(seed, (*k)++));
+        if (log(u) < 0.5 * z * z + dm - dm * v + dm * log(v)) return dm * v;
+    }
+}
+
+void cgo_separable_mixing(uint64_t seed, int64_t r, int64_t cols, double alpha, double* h) {
+    uint64_t hseed = cgo_mix64(seed, 13), k = 0;
+    for (int64_t c = 0; c < cols; ++c) {
+        double* hc = h + c * r;
+        double sum = 0.0;
+        for (int64_t q = 0; q < r; ++q) {
+            hc[q] = sep_gamma(hseed, &k, alpha);
+            sum += hc[q];
+        }
+        for (int64_t q = 0; q < r; ++q) hc[q] = sum > 0.0 ? hc[q] / sum : 1.0 / (double)r;
+    }
+}
+
+/* X = max(A.[I_r | H] + sigma*N, 0), rows [row0, row0+n) written row-major fp32; every
+ * product and sum rounded in fp32 (this file is built with -ffp-contract=off), ascending k.
+ * The noise term is cgo_normal_f32, so entries can differ from the GPU's where that
+ * normal does (a 1-ulp libm difference in the far tails; see above). */
+static void sep_rows(uint64_t seed, int64_t row0, int64_t i, int64_t d, int64_t r, float sg, const float* hf,
+                     float* xi) {
+    int64_t hc = d - r;
+    uint64_t aseed = cgo_mix64(seed, 11), nseed = cgo_mix64(seed, 12);
+    uint64_t gi = (uint64_t)(row0 + i);
+    float a[64];
+    for (int64_t k = 0; k < r && k < 64; ++k) a[k] = (float)(cgo_draw(aseed, gi * (uint64_t)r + (uint64_t)k) >> 40) * 0x1.0p-24f;
+    for (int64_t j = 0; j < d; ++j) {
+        float base;
+        if (j < r) {
+            base = a[j];
+        } else {
+            base = 0.0f;
+            for (int64_t k = 0; k < r; ++k) base = base + a[k] * hf[k * hc + (j - r)];
+        }
+        float v = base + sg * cgo_normal_f32(nseed, gi * (uint64_t)d + (uint64_t)j);
+        xi[j] = v > 0.0f ? v : 0.0f;
+    }
+}
+
+static float* sep_hf(uint64_t seed, int64_t d, int64_t r, double alpha) {
+    int64_t hc = d - r;
+    double* h = (double*)malloc(sizeof(double) * (size_t)(r * (hc > 0 ? hc : 1)));
+    float* hf = (float*)malloc(sizeof(float) * (size_t)(r * (hc > 0 ? hc : 1)));
+    cgo_separable_mixing(seed, r, hc, alpha, h);
+    for (int64_t k = 0; k < r; ++k)
+        for (int64_t c = 0; c < hc; ++c) hf[k * hc + c] = (float)h[c * r + k];
+    free(h);
+    return hf;
+}
+
+/* X = max(A.[I_r | H] + sigma*N, 0), rows [row0, row0+n) written row-major fp32; every
+ * product and sum rounded in fp32 (this file is built with -ffp-contract=off), ascending k
+ * (r <= 64).  The noise term is cgo_normal_f32, so entries can differ from the GPU's where
+ * that normal does (a 1-ulp libm difference in the far tails; see above). */
+void cgo_gen_separable_f32(uint64_t seed, int64_t row0, int64_t n, int64_t d, int64_t r, double alpha, double sigma,
+                           float* x) {
+    float* hf = sep_hf(seed, d, r, alpha);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) sep_rows(seed, row0, i, d, r, (float)sigma, hf, x + i * d);
+    free(hf);
+}
+
+/* Rows [b0, b1) of countsketch_apply(map, SparseMatrix)'s serial branch
+ * (src/sketch.cpp:84-91): out ((b1-b0) x d, column-major) starts at +0.0 and takes every
+ * row i with hash in [b0, b1), in ascending i -- the exact per-(bucket, column) order of
+ * the full serial loop, so these rows are bit-identical to the full result's.  A
+ * full-size parity check that touches only the rows of a bucket range. */
+void cgo_sketch_csr_buckets(const int64_t* hash, const double* sign, int64_t b0, int64_t b1, const int64_t* rowptr,
+                            const void* cols, int cols64, const void* vals, int vf32, int64_t n, int64_t d,
+                            double* out) {
+    const int64_t nb = b1 - b0;
+    memset(out, 0, sizeof(double) * (size_t)(nb * d));
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t b = hash[i];
+        if (b < b0 || b >= b1) continue;
+        const double s = sign[i];
+        for (int64_t q = rowptr[i]; q < rowptr[i + 1]; ++q) {
+            const int64_t c = cols64 ? ((const int64_t*)cols)[q] : (int64_t)((const int32_t*)cols)[q];
+            const double v = vf32 ? (double)((const float*)vals)[q] : ((const double*)vals)[q];
+            out[c * nb + (b - b0)] += s * v;
+        }
+    }
+}
+
+/* The same matrix written column-major fp64 (the reference DenseMatrix layout), rows
+ * [0, n): the CPU input of the config-4 reference arm.  Row blocks keep the writes to
+ * each column contiguous. */
+void cgo_gen_separable_f64_colmajor(uint64_t seed, int64_t n, int64_t d, int64_t r, double alpha, double sigma,
+                                    double* x) {
+    const int64_t blk = 2048;
+    float* hf = sep_hf(seed, d, r, alpha);
+#pragma omp parallel
+    {
+        float* tmp = (float*)malloc(sizeof(float) * (size_t)(blk * d));
+#pragma omp for schedule(dynamic, 4)
+        for (int64_t b = 0; b < (n + blk - 1) / blk; ++b) {
+            int64_t i0 = b * blk, cnt = n - i0 < blk ? n - i0 : blk;
+            for (int64_t i = 0; i < cnt; ++i) sep_rows(seed, 0, i0 + i, d, r, (float)sigma, hf, tmp + i * d);
+            for (int64_t j = 0; j < d; ++j)
+                for (int64_t i = 0; i < cnt; ++i) x[j * n + i0 + i] = (double)tmp[i * d + j];
+        }
+        free(tmp);
+    }
+    free(hf);
+}

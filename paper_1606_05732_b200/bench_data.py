@@ -91,3 +91,33 @@ def csr_bernoulli(n: int, d: int, density: float, seed: int, device=None):
     check(lib.cgx_gen_csr_bernoulli(ctx.h, seed, n, d, density, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(),
                                     None, stream))
     return SparseMatrix(n, d, rp, cols, vals)
+
+
+def separable_mixing(seed: int, r: int, cols: int, alpha: float = 0.5):
+    """The config-4 mixing weights H (r x cols, fp64): Dirichlet(alpha) columns
+    (cgx_separable_mixing; host only)."""
+    h = np.empty((cols, r), np.float64)
+    check(lib.cgx_separable_mixing(seed, r, cols, alpha, h.ctypes.data if h.size else None))
+    return h.T
+
+
+def dense_separable(n: int, d: int, seed: int, r: int = 16, alpha: float = 0.5, sigma: float = 0.01, dtype=None,
+                    layout: str = "row", device=None, row0: int = 0):
+    """Rows [row0, row0+n) of config 4's near-separable nonnegative X (BASELINE configs[3]):
+    X = max(A.[I_r | H] + sigma*N(0,1), 0), A uniform on [0,1), H's columns Dirichlet(alpha).
+    The anchor columns are 0..r-1."""
+    import torch
+
+    dtype = dtype or torch.float32
+    ctx = context(device)
+    dev = torch.device("cuda", ctx.device)
+    if layout == "row":
+        x = torch.empty((n, d), dtype=dtype, device=dev)
+        lay = CGX_ROW_MAJOR
+    else:
+        x = torch.empty((d, n), dtype=dtype, device=dev).t()
+        lay = CGX_COL_MAJOR
+    dt = CGX_F32 if dtype == torch.float32 else CGX_F64
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream or 1)
+    check(lib.cgx_gen_separable(ctx.h, seed, row0, n, d, r, alpha, sigma, dt, lay, x.data_ptr(), stream))
+    return x

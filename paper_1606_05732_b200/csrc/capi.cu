@@ -5,6 +5,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <numeric>
@@ -1160,6 +1161,31 @@ int cgx_gen_dense_normal_rows(cgx_ctx* ctx, uint64_t seed, const int64_t* rows_d
         if (!rows_dev) fail(CGX_EINVAL, "cgx_gen_dense_normal_rows: null rows");
         CallScope sc(ctx, stream);
         launch_gen_dense(ctx, seed, 0, rows_dev, n, d, dtype, layout, x_dev, sc.st);
+    });
+}
+
+int cgx_separable_mixing(uint64_t seed, int64_t r, int64_t cols, double alpha, double* h) {
+    return guard([&] {
+        if (r < 1 || cols < 0) fail(CGX_EINVAL, "cgx_separable_mixing: need r >= 1 and cols >= 0");
+        if (!(alpha > 0.0) || !std::isfinite(alpha)) fail(CGX_EINVAL, "cgx_separable_mixing: alpha must be > 0");
+        if (!h && r * cols > 0) fail(CGX_EINVAL, "cgx_separable_mixing: null output");
+        separable_mixing(seed, r, cols, alpha, h);
+    });
+}
+
+int cgx_gen_separable(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int64_t r, double alpha,
+                      double sigma, int dtype, int layout, void* x_dev, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        dsize(dtype);
+        if (layout != CGX_COL_MAJOR && layout != CGX_ROW_MAJOR) fail(CGX_EINVAL, "cgx_gen_separable: bad layout");
+        if (n < 0 || row0 < 0) fail(CGX_EINVAL, "cgx_gen_separable: negative size");
+        if (r < 1 || r > d) fail(CGX_EINVAL, "cgx_gen_separable: need 1 <= r <= d");
+        if (!(alpha > 0.0) || !std::isfinite(alpha)) fail(CGX_EINVAL, "cgx_gen_separable: alpha must be > 0");
+        if (!(sigma >= 0.0) || !std::isfinite(sigma)) fail(CGX_EINVAL, "cgx_gen_separable: sigma must be >= 0");
+        if (n == 0) return;
+        CallScope sc(ctx, stream);
+        launch_gen_separable(ctx, seed, row0, n, d, r, alpha, sigma, dtype, layout, x_dev, sc.st);
     });
 }
 

@@ -217,6 +217,11 @@ void launch_select_extremes(cgx_ctx* ctx, const double* z, int64_t m, int64_t d,
 void launch_gen_dense(cgx_ctx* ctx, uint64_t seed, int64_t row0, const int64_t* rows, int64_t n, int64_t d, int dtype,
                       int layout, void* x,
                       cudaStream_t s);
+// config 4: H = Dirichlet(alpha) mixing weights (r x cols column-major, host) and the
+// near-separable X = max(A.[I_r | H] + sigma*N(0,1), 0), rows [row0, row0+n)
+void separable_mixing(uint64_t seed, int64_t r, int64_t cols, double alpha, double* h);
+void launch_gen_separable(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int64_t d, int64_t r, double alpha,
+                          double sigma, int dtype, int layout, void* x, cudaStream_t s);
 struct CsrGenSpec {
     bool zipf = false;
     double density = 0.0;                      // Bernoulli

@@ -130,3 +130,20 @@ def test_bench_stage2_roofline_line():
     off = bench.stage2_line(argparse.Namespace(opt=["oz_slices=0"]), 256, 1 << 20, 512, 8.0)
     assert off["unit"] == "TFLOP/s"
     assert bench.stage2_line(argparse.Namespace(opt=[]), 256, 1 << 20, 512, 0.0) is None
+
+
+@pytest.mark.parametrize("seed,r,cols,alpha", [(oracle.mix64(12345, 4), 16, 112, 0.5), (7, 3, 40, 2.5),
+                                               (99, 1, 5, 0.5), (5, 8, 0, 1.0)])
+def test_separable_mixing_matches_oracle(seed, r, cols, alpha):
+    """Config 4's Dirichlet mixing weights (host code in libcgx) == the C twin, bit for bit;
+    columns are on the simplex."""
+    from paper_1606_05732_b200 import bench_data
+
+    h = bench_data.separable_mixing(seed, r, cols, alpha)
+    assert np.array_equal(h, oracle.Restatement().separable_mixing(seed, r, cols, alpha))
+    if cols:
+        assert np.allclose(h.sum(0), 1.0, atol=1e-12) and (h >= 0).all()
+    with pytest.raises(ValueError):
+        bench_data.separable_mixing(seed, 0, cols, alpha)
+    with pytest.raises(ValueError):
+        bench_data.separable_mixing(seed, r, cols, 0.0)
