@@ -247,6 +247,12 @@ int cgx_gen_separable(cgx_ctx* ctx, uint64_t seed, int64_t row0, int64_t n, int6
  * SeededRng(mix64(seed, 13)).  Pure host function (no context, no GPU). */
 int cgx_separable_mixing(uint64_t seed, int64_t r, int64_t cols, double alpha, double* h);
 
+/* 64-bit content checksum of a host array (bytes of it), computed with the context's host
+ * worker threads (ctx may be null: one thread).  The drop-in shim uses it to verify that a
+ * transform's public fields still hold what construction wrote before taking the cached
+ * device transform ("seeded fast path"). */
+int cgx_host_checksum(cgx_ctx* ctx, const void* p, size_t bytes, uint64_t* out);
+
 /* ---- instrumentation ---------------------------------------------------------------- */
 /* Context options (kernel variants for A/B runs; every variant gives the same S.X bits and
  * Z to rounding -- "oz_slices" below 7 trades Z accuracy for speed, as stated):

@@ -68,6 +68,7 @@ SIGNATURES = {
     "cgx_gen_csr_zipf": (_I, [_P, _U64, _I64, _I64, _D, _I64, _D, _P, _P, _P, _P, _P]),
     "cgx_gen_separable": (_I, [_P, _U64, _I64, _I64, _I64, _I64, _D, _D, _I, _I, _P, _P]),
     "cgx_separable_mixing": (_I, [_U64, _I64, _I64, _D, _P]),
+    "cgx_host_checksum": (_I, [_P, _P, _SZ, _P]),
     "cgx_launch_count": (_U64, [_P]),
     "cgx_set_option": (_I, [_P, C.c_char_p, _I64]),
     "cgx_profile_enable": (_I, [_P, _I]),

@@ -214,10 +214,22 @@ int64_t csr_chunk_rows(int64_t n, int64_t B, int64_t d) {
     return chunked ? chunk_rows : 0;
 }
 
+// Host dense X -> device (hoststage.cu): fp64 values that all round-trip through fp32
+// arrive as fp32 and *dtype switches to CGX_F32 (same layout and ld).
+const void* stage_dense(cgx_ctx* ctx, const void* x, int* dtype, size_t bytes, int x_mem, cudaStream_t s) {
+    if (x_mem == CGX_MEM_DEVICE || bytes == 0) return x;
+    const size_t es = dsize(*dtype);
+    bool narrowed = false;
+    const void* d = stage_in(ctx, ctx->hin[0], ctx->hin[1], x, bytes / es, es, *dtype == CGX_F64 ? 1 : 0, &narrowed, s);
+    if (narrowed) *dtype = CGX_F32;
+    return d;
+}
+
 // Dense input -> device-resident row-major view (stages host X, transposes column-major X).
-const void* dense_rowmajor(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
+const void* dense_rowmajor(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int* dtype_io, int layout, int64_t ld,
                            int64_t n, int64_t d, int x_mem, int64_t* rld_out, cudaStream_t s) {
-    const size_t es = dsize(dtype);
+    int& dtype = *dtype_io;
+    size_t es = dsize(dtype);
     if (layout != CGX_COL_MAJOR && layout != CGX_ROW_MAJOR) fail(CGX_EINVAL, "cgx: bad layout");
     if (n != xf->n)
         fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
@@ -227,7 +239,8 @@ const void* dense_rowmajor(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int
     if (ld < std::max<int64_t>(minld, 1)) fail(CGX_EINVAL, "cgx: leading dimension too small");
     if (d == 0) return x;
     const size_t bytes = layout == CGX_COL_MAJOR ? es * (size_t)(ld * (d - 1) + n) : es * (size_t)(ld * (n - 1) + d);
-    const void* xd = to_device(ctx, ctx->hstage_dev, x, bytes, x_mem, s);
+    const void* xd = stage_dense(ctx, x, &dtype, bytes, x_mem, s);
+    es = dsize(dtype);
     *rld_out = ld;
     if (layout == CGX_COL_MAJOR) {
         void* rm = ctx->xstage.get(es * (size_t)(n * d));
@@ -241,7 +254,7 @@ const void* dense_rowmajor(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int
 // Stage 1 (dense): SX row-major (B x d) into `sx_dev`.
 void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
                       int64_t n, int64_t d, int x_mem, double* sx_dev, cudaStream_t s) {
-    const size_t es = dsize(dtype);
+    size_t es = dsize(dtype);
     if (layout != CGX_COL_MAJOR && layout != CGX_ROW_MAJOR) fail(CGX_EINVAL, "cgx: bad layout");
     if (n != xf->n)
         fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
@@ -250,7 +263,8 @@ void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtyp
     const int64_t minld = layout == CGX_COL_MAJOR ? n : d;
     if (ld < std::max<int64_t>(minld, 1)) fail(CGX_EINVAL, "cgx: leading dimension too small");
     const size_t bytes = layout == CGX_COL_MAJOR ? es * (size_t)(ld * (d ? d - 1 : 0) + n) : es * (size_t)(ld * (n - 1) + d);
-    const void* xd = to_device(ctx, ctx->hstage_dev, x, d ? bytes : 0, x_mem, s);
+    const void* xd = stage_dense(ctx, x, &dtype, d ? bytes : 0, x_mem, s);
+    es = dsize(dtype);
     int64_t rld = ld;
     if (layout == CGX_COL_MAJOR && d > 0) {
         void* rm = ctx->xstage.get(es * (size_t)(n * d));
@@ -264,21 +278,20 @@ void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtyp
     ctx->prof.end(0, s);
 }
 
-// Host CSR inputs -> one device staging allocation with three regions (device inputs pass).
-void stage_csr(cgx_ctx* ctx, const void** rp, const void** cp, int idx_type, const void** vp, size_t es, int64_t n,
+// Host CSR inputs -> device (hoststage.cu; device inputs pass).  int64 column indices that
+// all fit int32 arrive as int32 and fp64 values that all round-trip through fp32 arrive as
+// fp32: *idx_type / *dtype switch accordingly (the kernels take both widths natively).
+void stage_csr(cgx_ctx* ctx, const void** rp, const void** cp, int* idx_type, const void** vp, int* dtype, int64_t n,
                int64_t nnz, int x_mem, cudaStream_t s) {
     if (x_mem != CGX_MEM_HOST) return;
-    const size_t is = idx_type == CGX_I32 ? 4 : 8;
-    const size_t r_b = sizeof(int64_t) * (size_t)(n + 1), c_b = is * (size_t)nnz, v_b = es * (size_t)nnz;
-    const size_t a = 256;
-    const size_t off_c = (r_b + a - 1) / a * a, off_v = off_c + (c_b + a - 1) / a * a;
-    char* base = (char*)ctx->hstage_dev.get(off_v + v_b);
-    CGX_CUDA(cudaMemcpyAsync(base, *rp, r_b, cudaMemcpyHostToDevice, s));
-    if (c_b) CGX_CUDA(cudaMemcpyAsync(base + off_c, *cp, c_b, cudaMemcpyHostToDevice, s));
-    if (v_b) CGX_CUDA(cudaMemcpyAsync(base + off_v, *vp, v_b, cudaMemcpyHostToDevice, s));
-    *rp = base;
-    *cp = base + off_c;
-    *vp = base + off_v;
+    bool nr = false;
+    *rp = stage_in(ctx, ctx->hin[0], ctx->hin[1], *rp, (size_t)(n + 1), sizeof(int64_t), 0, &nr, s);
+    if (nnz == 0) return;
+    *cp = stage_in(ctx, ctx->hin[2], ctx->hin[3], *cp, (size_t)nnz, *idx_type == CGX_I32 ? 4 : 8,
+                   *idx_type == CGX_I64 ? 2 : 0, &nr, s);
+    if (nr) *idx_type = CGX_I32;
+    *vp = stage_in(ctx, ctx->hin[4], ctx->hin[5], *vp, (size_t)nnz, dsize(*dtype), *dtype == CGX_F64 ? 1 : 0, &nr, s);
+    if (nr) *dtype = CGX_F32;
 }
 
 void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
@@ -295,7 +308,8 @@ void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
     const void* rp = rowptr;
     const void* cp = cols;
     const void* vp = vals;
-    stage_csr(ctx, &rp, &cp, idx_type, &vp, es, n, nnz, x_mem, s);
+    (void)es;
+    stage_csr(ctx, &rp, &cp, &idx_type, &vp, &dtype, n, nnz, x_mem, s);
     ctx->prof.begin(0, s);
     const int64_t chunk_rows = csr_chunk_rows(n, xf->B, d);
     if (chunk_rows == 0 && csr_partition_applies(ctx, n, xf->B, d, nnz))
@@ -427,6 +441,8 @@ int cgx_free(cgx_ctx* ctx) {
             b->release();
         for (auto& kv : ctx->pool_class) cudaFree(kv.first);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        for (auto& b : ctx->hin) b.release();
+        host_pool_free(ctx);
         for (int s = 0; s < 2; ++s)
             for (auto& e : ctx->prof.ev[s]) {
                 cudaEventDestroy(e.first);
@@ -816,7 +832,7 @@ int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x,
         need_g(xf);
         CallScope sc(ctx, stream);
         int64_t rld = ld;
-        const void* xd = dense_rowmajor(ctx, xf, x, dtype, layout, ld, n, d, x_mem, &rld, sc.st);
+        const void* xd = dense_rowmajor(ctx, xf, x, &dtype, layout, ld, n, d, x_mem, &rld, sc.st);
         if (d == 0) return;
         // Overlapped stages: G (m x B, <= 64 MB, L2-resident) is generated on the side
         // stream while the streaming sketch kernel reads X on the caller's stream -- the
@@ -976,7 +992,7 @@ int cgx_gaussian_project_dense(cgx_ctx* ctx, uint64_t rng_state, int64_t m, cons
         gx.has_g = true;
         gx.view = true;
         int64_t rld = ld;
-        const void* xd = dense_rowmajor(ctx, &gx, x, dtype, layout, ld, n, d, x_mem, &rld, sc.st);
+        const void* xd = dense_rowmajor(ctx, &gx, x, &dtype, layout, ld, n, d, x_mem, &rld, sc.st);
         const double* x64 = (const double*)xd;
         if (dtype == CGX_F32 || rld != d) {
             double* w = (double*)ctx->sx.get(sizeof(double) * (size_t)(n * d));
@@ -1016,7 +1032,8 @@ int cgx_gaussian_project_csr(cgx_ctx* ctx, uint64_t rng_state, int64_t m, const 
         const void* rp = rowptr;
         const void* cp = cols;
         const void* vp = vals;
-        stage_csr(ctx, &rp, &cp, idx_type, &vp, es, n, nnz, x_mem, sc.st);
+        (void)es;
+        stage_csr(ctx, &rp, &cp, &idx_type, &vp, &dtype, n, nnz, x_mem, sc.st);
         const size_t zb = sizeof(double) * (size_t)(m * d);
         double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
         ctx->prof.begin(1, sc.st);
@@ -1161,6 +1178,18 @@ int cgx_gen_dense_normal_rows(cgx_ctx* ctx, uint64_t seed, const int64_t* rows_d
         if (!rows_dev) fail(CGX_EINVAL, "cgx_gen_dense_normal_rows: null rows");
         CallScope sc(ctx, stream);
         launch_gen_dense(ctx, seed, 0, rows_dev, n, d, dtype, layout, x_dev, sc.st);
+    });
+}
+
+int cgx_host_checksum(cgx_ctx* ctx, const void* p, size_t bytes, uint64_t* out) {
+    return guard([&] {
+        if (!out || (!p && bytes)) fail(CGX_EINVAL, "cgx_host_checksum: null argument");
+        if (ctx) {
+            std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+            *out = host_checksum(ctx, p, bytes);
+        } else {
+            *out = host_checksum(nullptr, p, bytes);
+        }
     });
 }
 

@@ -1,0 +1,271 @@
+// hoststage.cu -- host-side input staging for the as-is API: the reference's DenseMatrix /
+// SparseMatrix live in pageable std::vector storage (matrix.hpp:16-61), and a plain
+// cudaMemcpy from pageable memory runs at ~11 GB/s on the B200 box against ~55 GB/s from
+// pinned memory (tools/microbench/h2d.cu).  Host arrays therefore go through a ring of
+// pinned chunks filled by a persistent pool of host threads while the copy engine drains
+// the previous chunks.
+//
+// Lossless narrowing on the way: a chunk of fp64 values that are all exactly representable
+// in fp32 (or of int64 column indices that all fit int32) is sent at half width and
+// widened back on the device -- or, when the whole array narrowed, handed to the kernels
+// as fp32 / int32, which they take natively.  The device sees exactly the caller's values
+// in every case; the check is per chunk, and a chunk that fails it is sent at full width.
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace cgx {
+
+// ---- persistent host thread pool ---------------------------------------------------------
+struct HostPool {
+    std::vector<std::thread> th;
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::function<void(int)> job;
+    uint64_t gen = 0;
+    int pending = 0;
+    bool quit = false;
+
+    explicit HostPool(int n) {
+        for (int k = 0; k < n; ++k)
+            th.emplace_back([this, k] {
+                uint64_t seen = 0;
+                for (;;) {
+                    std::function<void(int)> f;
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return quit || gen != seen; });
+                        if (quit) return;
+                        seen = gen;
+                        f = job;
+                    }
+                    f(k + 1);
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (--pending == 0) done_cv.notify_all();
+                }
+            });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            quit = true;
+        }
+        cv.notify_all();
+        for (auto& t : th) t.join();
+    }
+    int size() const { return (int)th.size() + 1; }
+    // f(k) for k = 0 .. size()-1, k = 0 on the calling thread; returns when all are done
+    void run(const std::function<void(int)>& f) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            job = f;
+            pending = (int)th.size();
+            ++gen;
+        }
+        cv.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> lk(mu);
+        done_cv.wait(lk, [&] { return pending == 0; });
+    }
+};
+
+namespace {
+
+constexpr size_t kChunk = (size_t)32 << 20;  // source bytes per pipeline chunk
+constexpr int kSlots = 4;
+
+HostPool& pool_of(cgx_ctx* ctx) {
+    if (!ctx->hpool) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        ctx->hpool = new HostPool((int)std::min(32u, hw) - 1);
+    }
+    return *ctx->hpool;
+}
+
+void ensure_ring(cgx_ctx* ctx) {
+    if (ctx->ring) return;
+    CGX_CUDA(cudaMallocHost((void**)&ctx->ring, kChunk * kSlots));
+    for (int s = 0; s < kSlots; ++s) CGX_CUDA(cudaEventCreateWithFlags(&ctx->ring_ev[s], cudaEventDisableTiming));
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Narrow [a, b) of src into dst; false as soon as some value does not round-trip.  Cloned
+// for AVX-512 / AVX2 hosts (the B200 boxes' Xeons have both), with a baseline fallback.
+#define CGX_HOST_SIMD __attribute__((target_clones("avx512f", "avx2", "default")))
+CGX_HOST_SIMD bool narrow_f64(const double* src, float* dst, size_t a, size_t b) {
+    bool ok = true;
+    for (size_t i = a; i < b; i += 4096) {
+        const size_t e = std::min(b, i + 4096);
+        unsigned bad = 0;
+        for (size_t k = i; k < e; ++k) {
+            const float f = (float)src[k];
+            dst[k] = f;
+            bad |= (unsigned)((double)f != src[k]);
+        }
+        if (bad) {
+            ok = false;
+            break;
+        }
+    }
+    return ok;
+}
+CGX_HOST_SIMD bool narrow_i64(const int64_t* src, int32_t* dst, size_t a, size_t b) {
+    bool ok = true;
+    for (size_t i = a; i < b; i += 4096) {
+        const size_t e = std::min(b, i + 4096);
+        unsigned bad = 0;
+        for (size_t k = i; k < e; ++k) {
+            const int32_t v = (int32_t)src[k];
+            dst[k] = v;
+            bad |= (unsigned)((int64_t)v != src[k]);
+        }
+        if (bad) {
+            ok = false;
+            break;
+        }
+    }
+    return ok;
+}
+
+template <typename N, typename W>
+__global__ void widen_kernel(const N* __restrict__ src, W* __restrict__ dst, size_t count) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = (W)src[i];
+}
+
+} // namespace
+
+void host_pool_free(cgx_ctx* ctx) {
+    delete ctx->hpool;
+    ctx->hpool = nullptr;
+    if (ctx->ring) {
+        for (int s = 0; s < kSlots; ++s) cudaEventDestroy(ctx->ring_ev[s]);
+        cudaFreeHost(ctx->ring);
+        ctx->ring = nullptr;
+    }
+}
+
+// Copy `count` elements of `esize` bytes from host `src` to the device.  kind: 0 plain,
+// 1 fp64 -> fp32 narrowing allowed, 2 int64 -> int32 narrowing allowed.  Returns the device
+// pointer and sets *narrowed when the whole array arrived narrowed (then the result holds
+// count elements of esize/2 bytes).  `full` / `half` are the device landing buffers.
+const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, size_t count, size_t esize, int kind,
+                     bool* narrowed, cudaStream_t s) {
+    *narrowed = false;
+    const size_t bytes = count * esize;
+    if (bytes == 0) return src;
+    if (bytes < ((size_t)1 << 20) || is_pinned(src)) {  // small, or already DMA-able: one copy
+        void* d = full.get(bytes);
+        CGX_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));  // pageable: returns once consumed
+        return d;
+    }
+    ensure_ring(ctx);
+    HostPool& pool = pool_of(ctx);
+    char* dfull = nullptr;                 // allocated when some chunk goes at full width
+    char* dhalf = kind ? (char*)half.get(bytes / 2) : nullptr;
+    const size_t per_chunk = kChunk / esize;  // elements per chunk
+    const size_t nchunks = (count + per_chunk - 1) / per_chunk;
+    std::vector<char> chunk_narrow(nchunks, 0);
+    bool try_narrow = kind != 0;
+    const int T = pool.size();
+    for (size_t c = 0; c < nchunks; ++c) {
+        const int slot = (int)(c % kSlots);
+        CGX_CUDA(cudaEventSynchronize(ctx->ring_ev[slot]));  // the slot's previous copy (this call or an earlier one)
+        char* buf = ctx->ring + (size_t)slot * kChunk;
+        const size_t e0 = c * per_chunk, ne = std::min(per_chunk, count - e0);
+        const char* sp = (const char*)src + e0 * esize;
+        bool ok = false;
+        if (try_narrow) {
+            std::atomic<int> bad{0};
+            pool.run([&](int k) {
+                const size_t a = ne * k / T, b = ne * (k + 1) / T;
+                const bool good = kind == 1 ? narrow_f64((const double*)sp, (float*)buf, a, b)
+                                            : narrow_i64((const int64_t*)sp, (int32_t*)buf, a, b);
+                if (!good) bad.store(1);
+            });
+            ok = bad.load() == 0;
+            if (!ok) try_narrow = false;  // data that does not narrow: stop paying for the check
+        }
+        if (ok) {
+            chunk_narrow[c] = 1;
+            CGX_CUDA(cudaMemcpyAsync(dhalf + e0 * esize / 2, buf, ne * esize / 2, cudaMemcpyHostToDevice, s));
+        } else {
+            pool.run([&](int k) {
+                const size_t a = ne * esize * k / T, b = ne * esize * (k + 1) / T;
+                std::memcpy(buf + a, sp + a, b - a);
+            });
+            if (!dfull) dfull = (char*)full.get(bytes);
+            CGX_CUDA(cudaMemcpyAsync(dfull + e0 * esize, buf, ne * esize, cudaMemcpyHostToDevice, s));
+        }
+        CGX_CUDA(cudaEventRecord(ctx->ring_ev[slot], s));
+    }
+    if (!dfull) {  // every chunk narrowed
+        *narrowed = true;
+        return dhalf;
+    }
+    for (size_t c = 0; c < nchunks; ++c) {  // widen the narrowed chunks into place
+        if (!chunk_narrow[c]) continue;
+        const size_t e0 = c * per_chunk, ne = std::min(per_chunk, count - e0);
+        const unsigned blocks = (unsigned)std::min<size_t>((ne + 255) / 256, (size_t)ctx->num_sms * 8);
+        if (kind == 1)
+            widen_kernel<float, double><<<blocks, 256, 0, s>>>((const float*)dhalf + e0, (double*)dfull + e0, ne);
+        else
+            widen_kernel<int32_t, int64_t><<<blocks, 256, 0, s>>>((const int32_t*)dhalf + e0, (int64_t*)dfull + e0, ne);
+        count_launch(ctx);
+        check_launch("widen");
+    }
+    return dfull;
+}
+
+// 64-bit content checksum of a host array (the drop-in shim's check that a transform's
+// public fields still hold what construction put there).  Per 1 MiB block a multiply-mix
+// hash of its 8-byte words, combined in block order: independent of the thread count.
+uint64_t host_checksum(cgx_ctx* ctx, const void* p, size_t bytes) {
+    const size_t blk = (size_t)1 << 20;
+    const size_t nb = (bytes + blk - 1) / blk;
+    std::vector<uint64_t> part(nb);
+    auto body = [&](size_t b) {
+        const unsigned char* q = (const unsigned char*)p + b * blk;
+        const size_t len = std::min(blk, bytes - b * blk);
+        uint64_t h = 0x243F6A8885A308D3ULL ^ (uint64_t)b, h2 = 0x13198A2E03707344ULL;
+        size_t i = 0;
+        for (; i + 16 <= len; i += 16) {
+            uint64_t w0, w1;
+            std::memcpy(&w0, q + i, 8);
+            std::memcpy(&w1, q + i + 8, 8);
+            h = (h ^ w0) * 0x9E3779B97F4A7C15ULL;
+            h2 = (h2 ^ w1) * 0xBF58476D1CE4E5B9ULL;
+        }
+        for (; i < len; ++i) h = (h ^ q[i]) * 0x100000001B3ULL;
+        part[b] = fin64(h ^ fin64(h2 + len));
+    };
+    if (ctx && bytes >= ((size_t)4 << 20)) {
+        HostPool& pool = pool_of(ctx);
+        const int T = pool.size();
+        pool.run([&](int k) {
+            for (size_t b = (size_t)k; b < nb; b += (size_t)T) body(b);
+        });
+    } else {
+        for (size_t b = 0; b < nb; ++b) body(b);
+    }
+    uint64_t h = fin64(bytes);
+    for (size_t b = 0; b < nb; ++b) h = fin64(h ^ part[b]) + (uint64_t)b;
+    return h;
+}
+
+} // namespace cgx

@@ -33,6 +33,8 @@ struct DevBuf {
     void release();
 };
 
+struct HostPool;
+
 struct Profile {
     bool on = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];
@@ -68,6 +70,12 @@ struct cgx_ctx {
     void* pinned = nullptr;                 // pinned staging for pageable host inputs
     size_t pinned_bytes = 0;
     cgx::Profile prof;
+    // host-input staging (hoststage.cu): worker pool, pinned chunk ring, device landing
+    // buffers (full / narrowed width) for up to three arrays of one call
+    cgx::HostPool* hpool = nullptr;
+    char* ring = nullptr;
+    cudaEvent_t ring_ev[4] = {};
+    cgx::DevBuf hin[6];
     // Caching pool for per-transform device arrays: transforms are built and dropped at
     // high rates by Monte-Carlo callers (distcheck), and cudaMalloc/cudaFree cost more
     // than a small sketch.  Blocks are size-classed (powers of two) and reused.
@@ -250,6 +258,13 @@ void launch_batch_sketch_gram(cgx_ctx* ctx, uint64_t master, int64_t t0, int64_t
 // scan.cu: exclusive scans (in place allowed), total written to out[count] when requested
 void exclusive_scan_u32(cgx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t count, cudaStream_t s);
 void exclusive_scan_i64(cgx_ctx* ctx, const int64_t* in, int64_t* out, int64_t count, cudaStream_t s);
+
+// hoststage.cu: pipelined pinned staging of a host array with lossless narrowing (kind 1:
+// fp64 -> fp32, kind 2: int64 -> int32); *narrowed when the whole array arrived narrowed
+const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, size_t count, size_t esize, int kind,
+                     bool* narrowed, cudaStream_t s);
+uint64_t host_checksum(cgx_ctx* ctx, const void* p, size_t bytes);
+void host_pool_free(cgx_ctx* ctx);
 
 inline void count_launch(cgx_ctx* ctx, int k = 1) { ctx->launches += (uint64_t)k; }
 // Launch as a programmatic dependent of the previous kernel in the stream (option "pdl"): its
