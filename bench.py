@@ -7,9 +7,12 @@ Workload (N=1 default): BASELINE config 2 -- dense X, n = 2^24 rows x d = 32 fp3
 B = 65536 buckets, m = 64 -- the configuration the metric is quoted on (configs[1]).  A
 step is one countgauss_apply over the whole X; X (2.15 GB) is generated in HBM before the
 timed region and is larger than L2 (126 MB), so no L2 flush is needed.  For N > 1
-(torchrun, one process per GPU over NCCL) the rows are sharded contiguously ("strong"):
-each rank sketches its shard with the shared seed and the m x d partial Z's are summed
-with an NCCL all-reduce; time is the max over ranks.
+(torchrun, one process per GPU over NCCL) the config's rows are sharded contiguously
+("strong", the north star's split): each rank sketches its shard with the shared seed into
+a partial S.X, and the partials are combined the north star's way -- all-reduce of S.X and
+G's m rows split across ranks for dense configs (--combine g), reduce-scatter of S.X by
+bucket range with split-K stage 2 for CSR configs (--combine sx); --combine z / --scaling
+weak are the labelled alternatives.  Time is the max over ranks.
 
 Reported beside `value` (device-resident X):
   roofline      -- the sketch kernel (stage 1), CUDA events on its launch stream,
@@ -224,6 +227,36 @@ def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000):
                         f"{reps}; full size extrapolated as sketch x nnz ratio + gemm"))
 
 
+def run_dropin(cfg_name, c, reps=3):
+    """Times cg::countgauss_apply through the drop-in and through the reference library, in
+    one program (integration/dropin_bench.cpp), on the config's shape with fp32-valued fp64
+    entries (BASELINE's configs hold fp32 data) and, for dense configs, full-fp64 entries."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    gpu_bin, cpu_bin = os.path.join(ref, "dropin_bench_gpu"), os.path.join(ref, "dropin_bench_cpu")
+    if not (os.path.exists(gpu_bin) and os.path.exists(cpu_bin)):
+        return {"unavailable": "oracle/_ref/dropin_bench_{gpu,cpu} not built (needs /root/reference at build time)"}
+    import subprocess
+
+    def run(b, extra):
+        out = subprocess.run([b, cfg_name, str(reps)] + extra, capture_output=True, text=True, timeout=900,
+                             check=True).stdout
+        return json.loads(out.strip().splitlines()[-1])
+
+    res = {}
+    for label, extra in [("fp32_valued", [])] + ([("fp64", ["fp64"])] if cfg_name != "c3" else []):
+        gj, cj = run(gpu_bin, extra), run(cpu_bin, extra)
+        res[label] = {"value": gj["nnz_per_s"], "unit": "nnz/s", "ms_per_step": gj["ms"],
+                      "h2d_bytes_per_step": int(gj["input_bytes"]), "d2h_bytes_per_step": c["m"] * c["d"] * 8,
+                      "reference_ms": cj["ms"], "speedup_vs_reference": cj["ms"] / gj["ms"],
+                      "z_match": abs(gj["z_abs_sum"] - cj["z_abs_sum"]) <= 1e-12 * abs(cj["z_abs_sum"]),
+                      "values": gj["values"]}
+    res["how"] = ("cg::countgauss_apply(t, X) with X a reference DenseMatrix/SparseMatrix in pageable host memory "
+                  f"(fp64; CSR int64+fp64), median of {reps} after a warm-up, wall clock, through the drop-in shim "
+                  "(seeded fast path + pipelined pinned staging) vs the same program linked with the reference library "
+                  "on this host's cores; h2d_bytes = the bytes the API hands over")
+    return res
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -402,7 +435,7 @@ def run_ours(args):
             cg.api.countsketch_apply_into(t, x, sxbuf)  # partial S.X (row-major B x d)
             e0 = mark()
             if args.combine == "sx":
-                out = combine("sx", world=world, rank=rank, B=B, d=d, partial_sx=sxbuf,
+                out = combine("sx", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
                               stage2=lambda sl, b0, b1: cg.api.gauss_gemm_range(t, sl, b0, b1))
             else:
                 out = combine("g", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
@@ -512,6 +545,14 @@ def run_ours(args):
                "how": "cgx_countgauss_apply_dense with x_mem=HOST (pinned), wall clock, median"}
         del xh
 
+    # e2e through the reference's own C++ API (cg::countgauss_apply(t, DenseMatrix /
+    # SparseMatrix): fp64 column-major / int64+fp64 CSR in pageable std::vector storage),
+    # the drop-in (integration/countgauss_gpu.cpp + libcgx) against the same program linked
+    # with the reference library (integration/dropin_bench.cpp, built by oracle/Makefile).
+    e2e_dropin = None
+    if rank == 0 and world == 1 and not args.no_e2e and args.config in ("c1", "c2", "c3", "c4"):
+        e2e_dropin = run_dropin(args.config, c)
+
     # Ablation (the reference's bench reports it too, countgauss_main.cpp:535-547): the
     # dense-Gaussian projection G~.X (m x n Gaussian, generated on the GPU, never stored) on
     # the same X -- dense or CSR -- untimed by the main metric.
@@ -582,6 +623,7 @@ def run_ours(args):
                          "bytes_per_launch": bytes_alg, "peak_source": peak_kind},
             "stage2": stage2_line(args, m, B, d, gm_ms / max(gm_n, 1)),
             "e2e": e2e,
+            "e2e_dropin": e2e_dropin,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "ablation": ablation,
@@ -603,18 +645,21 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ablation", action="store_true", help="skip the dense-Gaussian G~.X ablation")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: each rank sketches the config's n rows (X has N*n rows); strong: n split N ways")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default, the north star's split): the config's n rows split N ways; weak: each "
+                         "rank sketches the config's n rows (X has N*n rows)")
     ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
                     help="cgx_set_option before timing (A/B of kernel variants)")
     ap.add_argument("--placement", default="rows", choices=["rows", "hash"],
                     help="rows: contiguous row shards; hash: each rank holds the rows hashing into its bucket "
                          "range, in bucket order (SURVEY 8e ablation C; dense configs; combine = all-reduce of Z)")
-    ap.add_argument("--combine", default="z", choices=["z", "sx", "g", "cols"],
-                    help="N>1 combine: z = all-reduce of Z; sx = reduce-scatter of S.X + split-K stage 2 + "
+    ap.add_argument("--combine", default="auto", choices=["auto", "z", "sx", "g", "cols"],
+                    help="N>1 combine (auto: g for dense configs, sx for CSR -- the north star's schemes): z = all-reduce of Z; sx = reduce-scatter of S.X + split-K stage 2 + "
                          "all-reduce; g = all-reduce of S.X + G's m rows split over ranks + all-gather; "
                          "cols = column reduce-scatter of S.X + split-N stage 2 + all-gather")
     args = ap.parse_args()
+    if args.combine == "auto":
+        args.combine = "g" if CONFIGS[args.config]["kind"] == "dense" else "sx"
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3", file=sys.stderr)
     if args.impl == "reference":

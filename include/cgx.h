@@ -253,6 +253,45 @@ int cgx_separable_mixing(uint64_t seed, int64_t r, int64_t cols, double alpha, d
  * device transform ("seeded fast path"). */
 int cgx_host_checksum(cgx_ctx* ctx, const void* p, size_t bytes, uint64_t* out);
 
+/* ---- device groups: one process, several GPUs of a node (the north star's
+ * multi-GPU split; no reference counterpart -- the reference has no distributed code, the
+ * scheme is the paper's seed sharing) ----------------------------------
+ * A group holds one context per device and one NCCL communicator per device
+ * (ncclCommInitAll over NVLink/NVSwitch; NCCL is loaded with dlopen on first use --
+ * CGX_ENCCL if it cannot be).  A group transform gives rank p the rows
+ * [row0_p, row0_p + rows_p) of countgauss_new(t_seed, m, buckets, input_dim) (contiguous
+ * shards, sizes differing by at most one); rank p builds its part of S from the shared seed
+ * for its global rows, so no map is exchanged.  The apply runs every rank on its own host
+ * thread and combines the partials over NCCL:
+ *   CGX_COMBINE_G  all-reduce of the B x d partial S.X; rank p computes rows
+ *                  [p*ceil(m/P), ...) of Z = G.S.X (G's m rows split); row blocks all-gathered
+ *   CGX_COMBINE_SX reduce-scatter of S.X by bucket range (ceil(B/P) buckets per rank);
+ *                  split-K stage 2 on the owned slice; all-reduce of Z
+ *   CGX_COMBINE_Z  both stages per rank on its shard; all-reduce of Z
+ * Z equals the single-GPU result up to floating-point reassociation across ranks. */
+enum { CGX_COMBINE_Z = 0, CGX_COMBINE_G = 1, CGX_COMBINE_SX = 2 };
+typedef struct cgx_group cgx_group;
+typedef struct cgx_gxform cgx_gxform;
+int cgx_group_init(int ndev, const int* devs, cgx_group** out);
+int cgx_group_free(cgx_group* g);
+int cgx_group_size(const cgx_group* g);
+int cgx_group_context(cgx_group* g, int rank, cgx_ctx** out); /* rank's context (owned by the group) */
+int cgx_group_countgauss_new(cgx_group* g, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
+                             cgx_gxform** out);
+int cgx_gxform_free(cgx_gxform* t);
+int cgx_gxform_shard(const cgx_gxform* t, int rank, int64_t* row0, int64_t* rows);
+/* countgauss_apply(t, DenseMatrix) over the group.  x_mem CGX_MEM_HOST: x is the whole
+ * n x d matrix on the host (layout, ld as in cgx_countgauss_apply_dense); each rank stages its
+ * row block.  x_mem CGX_MEM_DEVICE: x is an array of P device pointers, rank p's shard
+ * (rows_p x d, same layout and ld) on device p.  z_mem CGX_MEM_HOST: z is the m x d
+ * column-major result; CGX_MEM_DEVICE: z is an array of P device pointers, each receiving Z. */
+int cgx_group_countgauss_apply_dense(cgx_group* g, const cgx_gxform* t, const void* x, int dtype, int layout,
+                                     int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem, int combine);
+/* countgauss_apply(t, SparseMatrix) over the group; CSR in host memory (rowptr[0] = 0). */
+int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int64_t* rowptr, const void* cols,
+                                   int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
+                                   double* z, int z_mem, int combine);
+
 /* ---- instrumentation ---------------------------------------------------------------- */
 /* Context options (kernel variants for A/B runs; every variant gives the same S.X bits and
  * Z to rounding -- "oz_slices" below 7 trades Z accuracy for speed, as stated):

@@ -20,6 +20,7 @@ thread_local std::string g_err;
 }
 
 void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+void set_last_error(const std::string& msg) { g_err = msg; }
 
 void check_cuda(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return;
@@ -215,14 +216,20 @@ int64_t csr_chunk_rows(int64_t n, int64_t B, int64_t d) {
 }
 
 // Host dense X -> device (hoststage.cu): fp64 values that all round-trip through fp32
-// arrive as fp32 and *dtype switches to CGX_F32 (same layout and ld).
-const void* stage_dense(cgx_ctx* ctx, const void* x, int* dtype, size_t bytes, int x_mem, cudaStream_t s) {
-    if (x_mem == CGX_MEM_DEVICE || bytes == 0) return x;
+// arrive as fp32 and *dtype switches to CGX_F32.  A padded layout (ld beyond the rows of a
+// column-major X, or the columns of a row-major one -- e.g. a row block of a larger
+// matrix) is staged as its segments only and lands dense: *ld becomes n or d.
+const void* stage_dense(cgx_ctx* ctx, const void* x, int* dtype, int layout, int64_t* ld, int64_t n, int64_t d,
+                        int x_mem, cudaStream_t s) {
+    if (x_mem == CGX_MEM_DEVICE || n == 0 || d == 0) return x;
     const size_t es = dsize(*dtype);
+    const int64_t seg = layout == CGX_COL_MAJOR ? n : d, nseg = layout == CGX_COL_MAJOR ? d : n;
     bool narrowed = false;
-    const void* d = stage_in(ctx, ctx->hin[0], ctx->hin[1], x, bytes / es, es, *dtype == CGX_F64 ? 1 : 0, &narrowed, s);
+    const void* p = stage_in(ctx, ctx->hin[0], ctx->hin[1], x, (size_t)(seg * nseg), es, *dtype == CGX_F64 ? 1 : 0,
+                             &narrowed, s, (size_t)seg, (size_t)*ld);
+    *ld = seg;
     if (narrowed) *dtype = CGX_F32;
-    return d;
+    return p;
 }
 
 // Dense input -> device-resident row-major view (stages host X, transposes column-major X).
@@ -238,8 +245,7 @@ const void* dense_rowmajor(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int
     const int64_t minld = layout == CGX_COL_MAJOR ? n : d;
     if (ld < std::max<int64_t>(minld, 1)) fail(CGX_EINVAL, "cgx: leading dimension too small");
     if (d == 0) return x;
-    const size_t bytes = layout == CGX_COL_MAJOR ? es * (size_t)(ld * (d - 1) + n) : es * (size_t)(ld * (n - 1) + d);
-    const void* xd = stage_dense(ctx, x, &dtype, bytes, x_mem, s);
+    const void* xd = stage_dense(ctx, x, &dtype, layout, &ld, n, d, x_mem, s);
     es = dsize(dtype);
     *rld_out = ld;
     if (layout == CGX_COL_MAJOR) {
@@ -262,8 +268,7 @@ void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtyp
     if (d < 0) fail(CGX_EINVAL, "cgx: negative column count");
     const int64_t minld = layout == CGX_COL_MAJOR ? n : d;
     if (ld < std::max<int64_t>(minld, 1)) fail(CGX_EINVAL, "cgx: leading dimension too small");
-    const size_t bytes = layout == CGX_COL_MAJOR ? es * (size_t)(ld * (d ? d - 1 : 0) + n) : es * (size_t)(ld * (n - 1) + d);
-    const void* xd = stage_dense(ctx, x, &dtype, d ? bytes : 0, x_mem, s);
+    const void* xd = stage_dense(ctx, x, &dtype, layout, &ld, n, d, x_mem, s);
     es = dsize(dtype);
     int64_t rld = ld;
     if (layout == CGX_COL_MAJOR && d > 0) {

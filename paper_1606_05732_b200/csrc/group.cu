@@ -1,0 +1,408 @@
+// group.cu -- multi-GPU CountGauss behind the C ABI (include/cgx.h, "device groups"): one
+// process drives several GPUs of a node, for C++ callers of the drop-in (the
+// north star's split).  The reference has no distributed code; the scheme is the paper's
+// seed sharing: rank p holds rows shard_range(n, P, p) of X and builds
+// its part of S from the shared seed for its *global* rows, so no map is exchanged.  The
+// partials combine over NCCL (ncclCommInitAll: one communicator per device, NVLink /
+// NVSwitch inside the node):
+//   CGX_COMBINE_G  (default, dense): all-reduce of the B x d partial S.X, then rank p
+//                  computes rows [p*ceil(m/P), ...) of Z = G[r0:r1, :].S.X -- G's m rows
+//                  split across ranks -- and the row blocks are gathered;
+//   CGX_COMBINE_SX (CSR):  reduce-scatter of S.X by bucket range, split-K stage 2 on the
+//                  owned slice, all-reduce of Z;
+//   CGX_COMBINE_Z:         every rank runs both stages on its shard, all-reduce of Z.
+// Each device is driven by its own host thread (host-input staging blocks the host), its
+// kernels and collectives ordered on its context's stream.  NCCL is loaded with dlopen on
+// first use, so libcgx has no link-time NCCL dependency.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <nccl.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace cgx {
+namespace {
+
+struct Nccl {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclCommInitAll) CommInitAll = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclReduceScatter) ReduceScatter = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+const Nccl& nccl() {
+    static Nccl n = [] {
+        Nccl r;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            r.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return r;
+        }
+#define CGX_SYM(f)                                                      \
+    r.f = (decltype(r.f))dlsym(h, "nccl" #f);                           \
+    if (!r.f) {                                                         \
+        r.why = "libnccl.so.2 lacks nccl" #f;                           \
+        return r;                                                       \
+    }
+        CGX_SYM(CommInitAll)
+        CGX_SYM(CommDestroy)
+        CGX_SYM(AllReduce)
+        CGX_SYM(ReduceScatter)
+        CGX_SYM(AllGather)
+        CGX_SYM(GroupStart)
+        CGX_SYM(GroupEnd)
+        CGX_SYM(GetErrorString)
+#undef CGX_SYM
+        r.ok = true;
+        return r;
+    }();
+    return n;
+}
+
+void check_nccl(ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return;
+    fail(CGX_ENCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+void shard(int64_t n, int P, int p, int64_t* a, int64_t* b) {  // distributed.shard_range
+    const int64_t base = n / P, extra = n % P;
+    *a = p * base + std::min<int64_t>(p, extra);
+    *b = *a + base + (p < extra ? 1 : 0);
+}
+
+// Runs f(p) for every rank on its own host thread; rethrows the first failure.
+template <class F>
+void each_rank(int P, F&& f) {
+    std::vector<Error> errs((size_t)P);
+    std::vector<char> bad((size_t)P, 0);
+    std::vector<std::thread> th;
+    for (int p = 0; p < P; ++p)
+        th.emplace_back([&, p] {
+            try {
+                f(p);
+            } catch (const Error& e) {
+                errs[(size_t)p] = e;
+                bad[(size_t)p] = 1;
+            } catch (const std::exception& e) {
+                errs[(size_t)p] = Error{CGX_ECUDA, e.what()};
+                bad[(size_t)p] = 1;
+            }
+        });
+    for (auto& t : th) t.join();
+    for (int p = 0; p < P; ++p)
+        if (bad[(size_t)p]) throw errs[(size_t)p];
+}
+
+void ok_or_throw(int rc) {
+    if (rc != CGX_OK) fail(rc, cgx_last_error());
+}
+
+} // namespace
+} // namespace cgx
+
+struct cgx_group {
+    int P = 0;
+    std::vector<int> dev;
+    std::vector<cgx_ctx*> ctx;
+    std::vector<ncclComm_t> comm;
+    std::vector<cgx::DevBuf> sx, slice, zp, zg, rp;  // per-rank scratch (rp: Z row blocks)
+};
+
+struct cgx_gxform {
+    cgx_group* g = nullptr;
+    int64_t m = 0, B = 0, n = 0;
+    std::vector<cgx_xform*> xf;
+    std::vector<int64_t> r0, r1;
+};
+
+using namespace cgx;
+
+namespace {
+
+template <class F>
+int gguard(F&& f) {
+    try {
+        f();
+        return CGX_OK;
+    } catch (const Error& e) {
+        set_last_error(e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("out of host memory");
+        return CGX_ENOMEM;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return CGX_ECUDA;
+    }
+}
+
+// The combine step of rank p, on its context's stream, once rank p's stage 1 (or both
+// stages, for CGX_COMBINE_Z) is queued.  The NCCL calls of all ranks run concurrently from
+// their threads (one communicator per device).
+void combine_rank(cgx_group* g, const cgx_gxform* t, int p, int64_t d, int mode, double* z_host, int z_mem,
+                  double* const* z_dev) {
+    cgx_ctx* c = g->ctx[(size_t)p];
+    const Nccl& N = nccl();
+    const int P = g->P;
+    const int64_t m = t->m, B = t->B;
+    cudaStream_t st = c->stream;
+    CGX_CUDA(cudaSetDevice(c->device));
+    double* zfull = (double*)g->zg[(size_t)p].get(sizeof(double) * (size_t)(m * d));
+    if (mode == CGX_COMBINE_Z) {
+        double* zp = (double*)g->zp[(size_t)p].p;
+        check_nccl(N.AllReduce(zp, zfull, (size_t)(m * d), ncclDouble, ncclSum, g->comm[(size_t)p], st), "ncclAllReduce(Z)");
+    } else if (mode == CGX_COMBINE_SX) {
+        const int64_t per = (B + P - 1) / P;
+        double* sx = (double*)g->sx[(size_t)p].p;  // (per*P) x d row-major, zero-padded past B
+        double* sl = (double*)g->slice[(size_t)p].get(sizeof(double) * (size_t)(per * d));
+        check_nccl(N.ReduceScatter(sx, sl, (size_t)(per * d), ncclDouble, ncclSum, g->comm[(size_t)p], st),
+                   "ncclReduceScatter(S.X)");
+        const int64_t b0 = std::min(B, p * per), b1 = std::min(B, b0 + per);
+        double* zp = (double*)g->zp[(size_t)p].get(sizeof(double) * (size_t)(m * d));
+        if (b1 > b0)
+            ok_or_throw(cgx_gauss_gemm_range(c, t->xf[(size_t)p], sl, b0, b1, d, CGX_MEM_DEVICE, zp, CGX_MEM_DEVICE, st));
+        else
+            CGX_CUDA(cudaMemsetAsync(zp, 0, sizeof(double) * (size_t)(m * d), st));
+        check_nccl(N.AllReduce(zp, zfull, (size_t)(m * d), ncclDouble, ncclSum, g->comm[(size_t)p], st), "ncclAllReduce(Z)");
+    } else {  // CGX_COMBINE_G
+        double* sx = (double*)g->sx[(size_t)p].p;  // B x d row-major
+        check_nccl(N.AllReduce(sx, sx, (size_t)(B * d), ncclDouble, ncclSum, g->comm[(size_t)p], st), "ncclAllReduce(S.X)");
+        const int64_t per = (m + P - 1) / P;
+        const int64_t r0 = std::min(m, p * per), r1 = std::min(m, r0 + per);
+        // rank p's rows as a zero-padded per x d column-major block; blocks are all-gathered
+        double* blk = (double*)g->zp[(size_t)p].get(sizeof(double) * (size_t)(per * d));
+        double* all = (double*)g->slice[(size_t)p].get(sizeof(double) * (size_t)(per * P * d));
+        CGX_CUDA(cudaMemsetAsync(blk, 0, sizeof(double) * (size_t)(per * d), st));
+        if (r1 > r0) {
+            double* rows = (double*)g->rp[(size_t)p].get(sizeof(double) * (size_t)((r1 - r0) * d));
+            ok_or_throw(cgx_gauss_gemm_rows(c, t->xf[(size_t)p], sx, d, r0, r1, CGX_MEM_DEVICE, rows, CGX_MEM_DEVICE, st));
+            CGX_CUDA(cudaMemcpy2DAsync(blk, sizeof(double) * per, rows, sizeof(double) * (r1 - r0),
+                                       sizeof(double) * (r1 - r0), d, cudaMemcpyDeviceToDevice, st));
+        }
+        check_nccl(N.AllGather(blk, all, (size_t)(per * d), ncclDouble, g->comm[(size_t)p], st), "ncclAllGather(Z rows)");
+        for (int q = 0; q < P; ++q) {  // block q -> rows [q*per, ...) of the m x d column-major Z
+            const int64_t a = std::min(m, q * per), b = std::min(m, a + per);
+            if (b > a)
+                CGX_CUDA(cudaMemcpy2DAsync(zfull + a, sizeof(double) * m, all + q * per * d, sizeof(double) * per,
+                                           sizeof(double) * (b - a), d, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    if (z_mem == CGX_MEM_DEVICE) {
+        CGX_CUDA(cudaMemcpyAsync(z_dev[p], zfull, sizeof(double) * (size_t)(m * d), cudaMemcpyDeviceToDevice, st));
+    } else if (p == 0) {
+        CGX_CUDA(cudaMemcpyAsync(z_host, zfull, sizeof(double) * (size_t)(m * d), cudaMemcpyDeviceToHost, st));
+    }
+    CGX_CUDA(cudaStreamSynchronize(st));
+}
+
+// Stage 1 of rank p into the combine mode's landing buffer (or both stages for Z).
+void partial_rank(cgx_group* g, const cgx_gxform* t, int p, int64_t d, int mode,
+                  const std::function<void(cgx_ctx*, cgx_xform*, double*, bool)>& apply) {
+    cgx_ctx* c = g->ctx[(size_t)p];
+    CGX_CUDA(cudaSetDevice(c->device));
+    if (mode == CGX_COMBINE_Z) {
+        double* zp = (double*)g->zp[(size_t)p].get(sizeof(double) * (size_t)(t->m * d));
+        apply(c, t->xf[(size_t)p], zp, true);
+        return;
+    }
+    const int P = g->P;
+    const int64_t rows = mode == CGX_COMBINE_SX ? (t->B + P - 1) / P * P : t->B;
+    double* sx = (double*)g->sx[(size_t)p].get(sizeof(double) * (size_t)(rows * d));
+    if (rows > t->B)
+        CGX_CUDA(cudaMemsetAsync(sx + t->B * d, 0, sizeof(double) * (size_t)((rows - t->B) * d), c->stream));
+    apply(c, t->xf[(size_t)p], sx, false);
+}
+
+void check_mode(int mode) {
+    if (mode != CGX_COMBINE_Z && mode != CGX_COMBINE_G && mode != CGX_COMBINE_SX)
+        fail(CGX_EINVAL, "cgx_group: combine must be CGX_COMBINE_Z, CGX_COMBINE_G or CGX_COMBINE_SX");
+}
+
+} // namespace
+
+extern "C" {
+
+int cgx_group_init(int ndev, const int* devs, cgx_group** out) {
+    return gguard([&] {
+        if (!out || ndev < 1 || !devs) fail(CGX_EINVAL, "cgx_group_init: need ndev >= 1 devices");
+        const Nccl& N = nccl();
+        if (!N.ok) fail(CGX_ENCCL, "cgx_group_init: " + N.why);
+        auto* g = new cgx_group;
+        g->P = ndev;
+        g->dev.assign(devs, devs + ndev);
+        g->ctx.assign((size_t)ndev, nullptr);
+        g->comm.assign((size_t)ndev, nullptr);
+        g->sx.resize((size_t)ndev);
+        g->slice.resize((size_t)ndev);
+        g->zp.resize((size_t)ndev);
+        g->zg.resize((size_t)ndev);
+        g->rp.resize((size_t)ndev);
+        try {
+            for (int p = 0; p < ndev; ++p) ok_or_throw(cgx_init(devs[p], &g->ctx[(size_t)p]));
+            check_nccl(N.CommInitAll(g->comm.data(), ndev, devs), "ncclCommInitAll");
+        } catch (...) {
+            for (auto* c : g->ctx)
+                if (c) cgx_free(c);
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+int cgx_group_free(cgx_group* g) {
+    return gguard([&] {
+        if (!g) return;
+        for (int p = 0; p < g->P; ++p) {
+            cudaSetDevice(g->dev[(size_t)p]);
+            cudaDeviceSynchronize();
+            for (auto* b : {&g->sx[(size_t)p], &g->slice[(size_t)p], &g->zp[(size_t)p], &g->zg[(size_t)p],
+                            &g->rp[(size_t)p]})
+                b->release();
+            if (g->comm[(size_t)p]) nccl().CommDestroy(g->comm[(size_t)p]);
+            cgx_free(g->ctx[(size_t)p]);
+        }
+        delete g;
+    });
+}
+
+int cgx_group_size(const cgx_group* g) { return g ? g->P : 0; }
+
+int cgx_group_context(cgx_group* g, int rank, cgx_ctx** out) {
+    return gguard([&] {
+        if (!g || !out || rank < 0 || rank >= g->P) fail(CGX_EINVAL, "cgx_group_context: bad rank");
+        *out = g->ctx[(size_t)rank];
+    });
+}
+
+int cgx_group_countgauss_new(cgx_group* g, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
+                             cgx_gxform** out) {
+    return gguard([&] {
+        if (!g || !out) fail(CGX_EINVAL, "cgx_group_countgauss_new: null argument");
+        if (m < 1 || buckets < 1 || input_dim < 1)
+            fail(CGX_EINVAL, "countgauss_new: m, buckets and input_dim must be >= 1");
+        auto* t = new cgx_gxform;
+        t->g = g;
+        t->m = m;
+        t->B = buckets;
+        t->n = input_dim;
+        t->xf.assign((size_t)g->P, nullptr);
+        t->r0.assign((size_t)g->P, 0);
+        t->r1.assign((size_t)g->P, 0);
+        try {
+            each_rank(g->P, [&](int p) {
+                shard(input_dim, g->P, p, &t->r0[(size_t)p], &t->r1[(size_t)p]);
+                ok_or_throw(cgx_countgauss_new_shard(g->ctx[(size_t)p], t_seed, m, buckets, input_dim, t->r0[(size_t)p],
+                                                     t->r1[(size_t)p] - t->r0[(size_t)p], &t->xf[(size_t)p]));
+                ok_or_throw(cgx_synchronize(g->ctx[(size_t)p], nullptr));
+            });
+        } catch (...) {
+            for (auto* x : t->xf)
+                if (x) cgx_xform_free(x);
+            delete t;
+            throw;
+        }
+        *out = t;
+    });
+}
+
+int cgx_gxform_free(cgx_gxform* t) {
+    return gguard([&] {
+        if (!t) return;
+        for (auto* x : t->xf)
+            if (x) cgx_xform_free(x);
+        delete t;
+    });
+}
+
+int cgx_gxform_shard(const cgx_gxform* t, int rank, int64_t* row0, int64_t* rows) {
+    return gguard([&] {
+        if (!t || rank < 0 || rank >= t->g->P) fail(CGX_EINVAL, "cgx_gxform_shard: bad rank");
+        if (row0) *row0 = t->r0[(size_t)rank];
+        if (rows) *rows = t->r1[(size_t)rank] - t->r0[(size_t)rank];
+    });
+}
+
+int cgx_group_countgauss_apply_dense(cgx_group* g, const cgx_gxform* t, const void* x, int dtype, int layout,
+                                     int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem, int combine) {
+    return gguard([&] {
+        if (!g || !t || t->g != g) fail(CGX_EINVAL, "cgx_group: null group or transform of another group");
+        check_mode(combine);
+        if (n != t->n)
+            fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
+                                 std::to_string(t->n));
+        if (d < 1) fail(CGX_EINVAL, "cgx_group: X must have at least one column");
+        if (layout != CGX_COL_MAJOR && layout != CGX_ROW_MAJOR) fail(CGX_EINVAL, "cgx: bad layout");
+        const size_t es = dtype == CGX_F32 ? 4 : 8;
+        each_rank(g->P, [&](int p) {
+            const int64_t r0 = t->r0[(size_t)p], rows = t->r1[(size_t)p] - r0;
+            const void* xp;
+            int64_t lp = ld;
+            if (x_mem == CGX_MEM_DEVICE) {
+                xp = ((const void* const*)x)[p];  // rank p's shard on its device
+            } else {
+                xp = (const char*)x + es * (size_t)(layout == CGX_COL_MAJOR ? r0 : r0 * ld);
+            }
+            partial_rank(g, t, p, d, combine, [&](cgx_ctx* c, cgx_xform* xf, double* out, bool both) {
+                if (both)
+                    ok_or_throw(cgx_countgauss_apply_dense(c, xf, xp, dtype, layout, lp, rows, d, x_mem, out,
+                                                           CGX_MEM_DEVICE, nullptr));
+                else
+                    ok_or_throw(cgx_countsketch_apply_dense(c, xf, xp, dtype, layout, lp, rows, d, x_mem, out,
+                                                            CGX_ROW_MAJOR, CGX_MEM_DEVICE, nullptr));
+            });
+            combine_rank(g, t, p, d, combine, z, z_mem, (double* const*)z);
+        });
+    });
+}
+
+int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int64_t* rowptr, const void* cols,
+                                   int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
+                                   double* z, int z_mem, int combine) {
+    return gguard([&] {
+        if (!g || !t || t->g != g) fail(CGX_EINVAL, "cgx_group: null group or transform of another group");
+        check_mode(combine);
+        if (n != t->n)
+            fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
+                                 std::to_string(t->n));
+        if (d < 1 || nnz < 0) fail(CGX_EINVAL, "cgx_group: bad CSR sizes");
+        if (!rowptr || rowptr[0] != 0 || rowptr[n] != nnz) fail(CGX_EINVAL, "cgx_group: row offsets must run 0..nnz");
+        const size_t is = idx_type == CGX_I32 ? 4 : 8, vs = dtype == CGX_F32 ? 4 : 8;
+        each_rank(g->P, [&](int p) {
+            const int64_t r0 = t->r0[(size_t)p], rows = t->r1[(size_t)p] - r0;
+            const int64_t q0 = rowptr[r0], q1 = rowptr[r0 + rows];
+            // the shard's row offsets, rebased to its own nonzeros; its nonzeros stay in the
+            // caller's host arrays and are staged by the apply (pipelined, narrowed)
+            std::vector<int64_t> rp((size_t)(rows + 1));
+            for (int64_t i = 0; i <= rows; ++i) rp[(size_t)i] = rowptr[r0 + i] - q0;
+            const void* cp = (const char*)cols + is * (size_t)q0;
+            const void* vp = (const char*)vals + vs * (size_t)q0;
+            partial_rank(g, t, p, d, combine, [&](cgx_ctx* c, cgx_xform* xf, double* out, bool both) {
+                if (both)
+                    ok_or_throw(cgx_countgauss_apply_csr(c, xf, rp.data(), cp, idx_type, vp, dtype, rows, d, q1 - q0,
+                                                         CGX_MEM_HOST, out, CGX_MEM_DEVICE, nullptr));
+                else
+                    ok_or_throw(cgx_countsketch_apply_csr(c, xf, rp.data(), cp, idx_type, vp, dtype, rows, d, q1 - q0,
+                                                          CGX_MEM_HOST, out, CGX_ROW_MAJOR, CGX_MEM_DEVICE, nullptr));
+            });
+            combine_rank(g, t, p, d, combine, z, z_mem, (double* const*)z);
+        });
+    });
+}
+
+} // extern "C"

@@ -12,6 +12,9 @@
 // in every case; the check is per chunk, and a chunk that fails it is sent at full width.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -104,42 +107,50 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-// Narrow [a, b) of src into dst; false as soon as some value does not round-trip.  Cloned
-// for AVX-512 / AVX2 hosts (the B200 boxes' Xeons have both), with a baseline fallback.
+// Narrow len values of src into dst; false as soon as some value does not round-trip.
+// Cloned for AVX-512 / AVX2 hosts (the B200 boxes' Xeons have both), with a baseline
+// fallback.
 #define CGX_HOST_SIMD __attribute__((target_clones("avx512f", "avx2", "default")))
-CGX_HOST_SIMD bool narrow_f64(const double* src, float* dst, size_t a, size_t b) {
-    bool ok = true;
-    for (size_t i = a; i < b; i += 4096) {
-        const size_t e = std::min(b, i + 4096);
+CGX_HOST_SIMD bool narrow_f64(const double* src, float* dst, size_t len) {
+    for (size_t i = 0; i < len; i += 4096) {
+        const size_t e = std::min(len, i + 4096);
         unsigned bad = 0;
         for (size_t k = i; k < e; ++k) {
             const float f = (float)src[k];
             dst[k] = f;
             bad |= (unsigned)((double)f != src[k]);
         }
-        if (bad) {
-            ok = false;
-            break;
-        }
+        if (bad) return false;
     }
-    return ok;
+    return true;
 }
-CGX_HOST_SIMD bool narrow_i64(const int64_t* src, int32_t* dst, size_t a, size_t b) {
-    bool ok = true;
-    for (size_t i = a; i < b; i += 4096) {
-        const size_t e = std::min(b, i + 4096);
+CGX_HOST_SIMD bool narrow_i64(const int64_t* src, int32_t* dst, size_t len) {
+    for (size_t i = 0; i < len; i += 4096) {
+        const size_t e = std::min(len, i + 4096);
         unsigned bad = 0;
         for (size_t k = i; k < e; ++k) {
             const int32_t v = (int32_t)src[k];
             dst[k] = v;
             bad |= (unsigned)((int64_t)v != src[k]);
         }
-        if (bad) {
-            ok = false;
-            break;
-        }
+        if (bad) return false;
     }
-    return ok;
+    return true;
+}
+
+// Elements [e, e_end) of a source made of segments of `seg` elements spaced `sld`
+// elements apart (a column-major row block: seg = rows, sld = ld), as contiguous pieces:
+// fn(source element offset, destination element offset relative to e, length).
+template <class F>
+bool for_pieces(size_t e, size_t e_end, size_t seg, size_t sld, F&& fn) {
+    const size_t base = e;
+    while (e < e_end) {
+        const size_t si = e / seg, off = e - si * seg;
+        const size_t len = std::min(seg - off, e_end - e);
+        if (!fn(si * sld + off, e - base, len)) return false;
+        e += len;
+    }
+    return true;
 }
 
 template <typename N, typename W>
@@ -165,15 +176,26 @@ void host_pool_free(cgx_ctx* ctx) {
 // pointer and sets *narrowed when the whole array arrived narrowed (then the result holds
 // count elements of esize/2 bytes).  `full` / `half` are the device landing buffers.
 const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, size_t count, size_t esize, int kind,
-                     bool* narrowed, cudaStream_t s) {
+                     bool* narrowed, cudaStream_t s, size_t seg, size_t sld) {
     *narrowed = false;
     const size_t bytes = count * esize;
     if (bytes == 0) return src;
+    if (seg == 0 || seg >= count) seg = sld = count;  // contiguous
     if (bytes < ((size_t)1 << 20) || is_pinned(src)) {  // small, or already DMA-able: one copy
         void* d = full.get(bytes);
-        CGX_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));  // pageable: returns once consumed
+        if (seg == count)
+            CGX_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));  // pageable: returns once consumed
+        else
+            CGX_CUDA(cudaMemcpy2DAsync(d, seg * esize, src, sld * esize, seg * esize, count / seg,
+                                       cudaMemcpyHostToDevice, s));
         return d;
     }
+    static const bool trace = getenv("CGX_TRACE_STAGE") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    double t_wait = 0, t_narrow = 0, t_copy = 0;
+    auto since = [](std::chrono::steady_clock::time_point a) {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - a).count();
+    };
     ensure_ring(ctx);
     HostPool& pool = pool_of(ctx);
     char* dfull = nullptr;                 // allocated when some chunk goes at full width
@@ -184,36 +206,52 @@ const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, 
     bool try_narrow = kind != 0;
     const int T = pool.size();
     for (size_t c = 0; c < nchunks; ++c) {
-        const int slot = (int)(c % kSlots);
+        const int slot = (int)(ctx->ring_next++ % kSlots);  // rotates across calls: back-to-back arrays overlap
+        auto tw = std::chrono::steady_clock::now();
         CGX_CUDA(cudaEventSynchronize(ctx->ring_ev[slot]));  // the slot's previous copy (this call or an earlier one)
+        t_wait += since(tw);
+        tw = std::chrono::steady_clock::now();
         char* buf = ctx->ring + (size_t)slot * kChunk;
         const size_t e0 = c * per_chunk, ne = std::min(per_chunk, count - e0);
-        const char* sp = (const char*)src + e0 * esize;
+        const char* sp = (const char*)src;
         bool ok = false;
         if (try_narrow) {
             std::atomic<int> bad{0};
             pool.run([&](int k) {
-                const size_t a = ne * k / T, b = ne * (k + 1) / T;
-                const bool good = kind == 1 ? narrow_f64((const double*)sp, (float*)buf, a, b)
-                                            : narrow_i64((const int64_t*)sp, (int32_t*)buf, a, b);
+                const size_t a = e0 + ne * k / T, b = e0 + ne * (k + 1) / T;
+                const size_t h = esize / 2;
+                const bool good = for_pieces(a, b, seg, sld, [&](size_t so, size_t dofs, size_t len) {
+                    char* dst = buf + (a - e0 + dofs) * h;
+                    return kind == 1 ? narrow_f64((const double*)(sp + so * esize), (float*)dst, len)
+                                     : narrow_i64((const int64_t*)(sp + so * esize), (int32_t*)dst, len);
+                });
                 if (!good) bad.store(1);
             });
             ok = bad.load() == 0;
             if (!ok) try_narrow = false;  // data that does not narrow: stop paying for the check
         }
+        t_narrow += since(tw);
+        tw = std::chrono::steady_clock::now();
         if (ok) {
             chunk_narrow[c] = 1;
             CGX_CUDA(cudaMemcpyAsync(dhalf + e0 * esize / 2, buf, ne * esize / 2, cudaMemcpyHostToDevice, s));
         } else {
             pool.run([&](int k) {
-                const size_t a = ne * esize * k / T, b = ne * esize * (k + 1) / T;
-                std::memcpy(buf + a, sp + a, b - a);
+                const size_t a = e0 + ne * k / T, b = e0 + ne * (k + 1) / T;
+                for_pieces(a, b, seg, sld, [&](size_t so, size_t dofs, size_t len) {
+                    std::memcpy(buf + (a - e0 + dofs) * esize, sp + so * esize, len * esize);
+                    return true;
+                });
             });
             if (!dfull) dfull = (char*)full.get(bytes);
             CGX_CUDA(cudaMemcpyAsync(dfull + e0 * esize, buf, ne * esize, cudaMemcpyHostToDevice, s));
         }
         CGX_CUDA(cudaEventRecord(ctx->ring_ev[slot], s));
+        t_copy += since(tw);
     }
+    if (trace)
+        fprintf(stderr, "stage_in %zu B x %zu (kind %d, seg %zu): %.1f us total, wait %.1f, narrow %.1f, copy+dma %.1f\n",
+                esize, count, kind, seg, since(t_start), t_wait, t_narrow, t_copy);
     if (!dfull) {  // every chunk narrowed
         *narrowed = true;
         return dhalf;

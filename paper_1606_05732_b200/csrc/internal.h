@@ -22,6 +22,7 @@ struct Error {
 };
 
 [[noreturn]] void fail(int code, const std::string& msg);
+void set_last_error(const std::string& msg);  // the thread's cgx_last_error() text
 void check_cuda(cudaError_t e, const char* what);
 #define CGX_CUDA(call) ::cgx::check_cuda((call), #call)
 
@@ -75,6 +76,7 @@ struct cgx_ctx {
     cgx::HostPool* hpool = nullptr;
     char* ring = nullptr;
     cudaEvent_t ring_ev[4] = {};
+    uint64_t ring_next = 0;
     cgx::DevBuf hin[6];
     // Caching pool for per-transform device arrays: transforms are built and dropped at
     // high rates by Monte-Carlo callers (distcheck), and cudaMalloc/cudaFree cost more
@@ -261,8 +263,10 @@ void exclusive_scan_i64(cgx_ctx* ctx, const int64_t* in, int64_t* out, int64_t c
 
 // hoststage.cu: pipelined pinned staging of a host array with lossless narrowing (kind 1:
 // fp64 -> fp32, kind 2: int64 -> int32); *narrowed when the whole array arrived narrowed
+// (seg, sld): the source is count/seg segments of seg elements, sld elements apart (a
+// column-major row block), landing contiguous on the device; 0 = one contiguous array
 const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, size_t count, size_t esize, int kind,
-                     bool* narrowed, cudaStream_t s);
+                     bool* narrowed, cudaStream_t s, size_t seg = 0, size_t sld = 0);
 uint64_t host_checksum(cgx_ctx* ctx, const void* p, size_t bytes);
 void host_pool_free(cgx_ctx* ctx);
 

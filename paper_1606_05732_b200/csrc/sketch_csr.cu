@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <algorithm>
 #include <climits>
 
 namespace cgx {
@@ -326,6 +327,83 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
     }
 }
 
+// Boundaries of the (bucket, chunk) runs of perm: virtual bucket v = b * nc + c holds the
+// rows of bucket b with row / chunk_rows == c (perm is sorted by (bucket, row)).
+__global__ void chunk_offsets_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ offsets, int64_t B,
+                                     int64_t nc, int64_t chunk_rows, uint32_t* __restrict__ voff) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v > B * nc) return;
+    if (v == B * nc) {
+        voff[v] = offsets[B];
+        return;
+    }
+    const int64_t b = v / nc, c = v - b * nc;
+    uint32_t lo = offsets[b], hi = offsets[b + 1];  // first entry with row >= c * chunk_rows
+    const int64_t r = c * chunk_rows;
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if ((int64_t)(perm[mid] & kRowMask) < r) lo = mid + 1; else hi = mid;
+    }
+    voff[v] = lo;
+}
+
+// out[b][j] = ((0 + part[b][0][j]) + part[b][1][j]) + ...: the reference's ascending-chunk
+// reduction of the per-chunk partial buffers (sketch.cpp:106-111).
+__global__ void chunk_reduce_kernel(const double* __restrict__ part, int64_t B, int64_t nc, int64_t d,
+                                    double* __restrict__ out) {
+    const int64_t total = B * d;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / d, j = e - b * d;
+        const double* p = part + b * nc * d + j;
+        double acc = 0.0;
+        for (int64_t c = 0; c < nc; ++c) acc += p[c * d];
+        out[e] = acc;
+    }
+}
+
+// The lean gather over `nb_total` buckets delimited by `offs`, into sx (row-major nb_total x d).
+// `colmax_ok`: sx is the final S.X, so the column maxima for the tensor-core stage 2 may be
+// folded in.  False when shared memory cannot hold a warp's accumulator.
+template <typename TV, typename TI>
+bool launch_lean(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* cols, const TV* vals, int64_t d,
+                 int64_t nb_total, const uint32_t* offs, double* sx, bool colmax_ok, cudaStream_t s) {
+    const size_t per_warp_l = (sizeof(double) + 1) * (size_t)d;
+    int wl = (int)((96 * 1024) / per_warp_l);
+    wl = wl > 8 ? 8 : wl;
+    if (wl < 1) return false;
+    unsigned long long* colmax = nullptr;
+    if (colmax_ok && oz_stage2_applies(ctx, xf, d)) {
+        colmax = (unsigned long long*)ctx->oz_b.get(sizeof(unsigned long long) * (size_t)d);
+        CGX_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * (size_t)d, s));
+        ctx->oz_colmax_for = sx;
+        ctx->oz_colmax_d = d;
+    }
+    const size_t sm = (per_warp_l * wl + 7) / 8 * 8 + (colmax ? sizeof(unsigned long long) * (size_t)d : 8);
+    auto lk = sketch_csr_lean<TV, TI>;
+    CGX_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 0;
+    CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, wl * 32, sm));
+    int64_t nb = (nb_total + wl - 1) / wl;
+    const int64_t cap = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);  // persistent: one wave
+    if (nb > cap) nb = cap;
+    int cb = 1;
+    while (((int64_t)1 << (cb - 1)) < d) ++cb;
+    // tasks of ~rows_per_task rows (whole buckets), single buckets for the last tail_tasks
+    // per warp
+    const int64_t rows_per_bucket = xf->n / nb_total + 1;
+    int64_t G = ctx->opt_rows_per_task / rows_per_bucket;
+    G = G < 1 ? 1 : (G > 64 ? 64 : G);
+    int64_t B1 = nb_total - ctx->opt_tail_tasks * nb * wl;
+    B1 = B1 < 0 ? 0 : B1 / G * G;
+    const unsigned long long base = take_tasks(ctx, B1 / G + nb_total - B1, nb * wl);
+    lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, offs, nb_total, d, sx, cb, (int)G, B1,
+                                         ctx->task_ctr, base, colmax);
+    count_launch(ctx);
+    tasks_launched(ctx, s);
+    check_launch("sketch_csr_lean");
+    return true;
+}
+
 template <typename TV, typename TI, bool CHUNKED>
 void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* cols, const TV* vals, int64_t d,
             double* sx, int64_t chunk_rows, cudaStream_t s) {
@@ -343,43 +421,34 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
         CGX_CUDA(cudaMemsetAsync(sx, 0, sizeof(double) * (size_t)(xf->B * d), s));
         if (CHUNKED) gpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(xf->B * d));
     }
-    if (!CHUNKED && d <= 8192) {  // lean kernel: fp64 accumulator + byte tags per warp
-        const size_t per_warp_l = (sizeof(double) + 1) * (size_t)d;
-        int wl = (int)((96 * 1024) / per_warp_l);
-        wl = wl > 8 ? 8 : wl;
-        if (wl >= 1) {
-            // column maxima for the tensor-core stage 2 when it will run on this S.X
-            unsigned long long* colmax = nullptr;
-            if (oz_stage2_applies(ctx, xf, d)) {
-                colmax = (unsigned long long*)ctx->oz_b.get(sizeof(unsigned long long) * (size_t)d);
-                CGX_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * (size_t)d, s));
-                ctx->oz_colmax_for = sx;
-                ctx->oz_colmax_d = d;
-            }
-            const size_t sm = (per_warp_l * wl + 7) / 8 * 8 + (colmax ? sizeof(unsigned long long) * (size_t)d : 8);
-            auto lk = sketch_csr_lean<TV, TI>;
-            CGX_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            int per_sm = 0;
-            CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, wl * 32, sm));
-            int64_t nb = (xf->B + wl - 1) / wl;
-            const int64_t cap = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);  // persistent: one wave
-            if (nb > cap) nb = cap;
-            int cb = 1;
-            while (((int64_t)1 << (cb - 1)) < d) ++cb;
-            // tasks of ~rows_per_task rows (whole buckets), single buckets for the last
-            // tail_tasks per warp
-            const int64_t rows_per_bucket = xf->n / xf->B + 1;
-            int64_t G = ctx->opt_rows_per_task / rows_per_bucket;
-            G = G < 1 ? 1 : (G > 64 ? 64 : G);
-            int64_t B1 = xf->B - ctx->opt_tail_tasks * nb * wl;
-            B1 = B1 < 0 ? 0 : B1 / G * G;
-            const unsigned long long base = take_tasks(ctx, B1 / G + xf->B - B1, nb * wl);
-            lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, xf->offsets, xf->B, d, sx, cb, (int)G, B1,
-                                                 ctx->task_ctr, base, colmax);
+    if (d <= 8192) {
+        if (!CHUNKED) {
+            if (launch_lean<TV, TI>(ctx, xf, rowptr, cols, vals, d, xf->B, xf->offsets, sx, true, s)) return;
+        } else {
+            // The reference's chunked branch (sketch.cpp:74-111) computes one partial per
+            // 8192-row chunk and sums the partials in chunk order.  The partials are
+            // independent, so each (bucket, chunk) pair is a bucket of its own here: its rows
+            // are a contiguous run of the bucket's (bucket, row)-sorted perm entries, found by
+            // binary search.  The lean gather then runs over B * n_chunks virtual buckets
+            // (parallel even when B is tiny -- e.g. B = 80 in acceptance criterion 11, where
+            // one warp per bucket left the GPU idle), and a second kernel sums each output
+            // entry's partials in chunk order, starting from +0.0, as the reference does.
+            const int64_t nc = (xf->n + chunk_rows - 1) / chunk_rows;
+            const int64_t vb = xf->B * nc;
+            uint32_t* voff = (uint32_t*)ctx->counts.get(sizeof(uint32_t) * (size_t)(vb + 1));
+            double* part = (double*)ctx->zpart.get(sizeof(double) * (size_t)(vb * d));
+            chunk_offsets_kernel<<<(unsigned)((vb + 1 + 255) / 256), 256, 0, s>>>(xf->perm, xf->offsets, xf->B, nc,
+                                                                                 chunk_rows, voff);
             count_launch(ctx);
-            tasks_launched(ctx, s);
-            check_launch("sketch_csr_lean");
-            return;
+            check_launch("chunk_offsets");
+            if (launch_lean<TV, TI>(ctx, xf, rowptr, cols, vals, d, vb, voff, part, false, s)) {
+                const int64_t total = xf->B * d;
+                chunk_reduce_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)ctx->num_sms * 8), 256,
+                                      0, s>>>(part, xf->B, nc, d, sx);
+                count_launch(ctx);
+                check_launch("chunk_reduce");
+                return;
+            }
         }
     }
     auto kern = sketch_csr_kernel<TV, TI, CHUNKED>;

@@ -9,7 +9,8 @@ T.X is linear, so the partials combine after either stage:
   the seed) and the m x d partials are summed with one all-reduce.  Communication is
   m*d*8 bytes; stage 2 is replicated.
 * ``"sx"``: the B x d partial sketches (row-major, so a bucket range is contiguous) are
-  reduce-scattered; rank p owns buckets [b_p, b_{p+1}) of the summed S.X and computes
+  reduce-scattered in equal ceil(B/P)-bucket chunks (clamped to B); rank p owns buckets
+  [b_p, b_{p+1}) of the summed S.X and computes
   Z_p = G[:, b_p:b_{p+1}) . S.X[b_p:b_{p+1}) (split-K: stage 2 and G generation divided
   by P), then Z = sum_p Z_p by all-reduce.  Communication is (P-1)/P * B*d*8 per rank.
 * ``"g"``: the partial sketches are all-reduced (every rank holds the summed S.X), rank p
@@ -116,8 +117,15 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
         flat = torch.cat([flat, pad], 0)
     out = torch.empty((per, d), dtype=flat.dtype, device=flat.device)
     dist.reduce_scatter_tensor(out, flat.contiguous(), group=group)
-    b0 = rank * per
+    # rank p owns the ceil(B/world)-bucket chunk [b0, b1) clamped to B (trailing ranks may
+    # own nothing when B is small: they contribute a zero Z)
+    b0 = min(B, rank * per)
     b1 = min(B, b0 + per)
-    z = stage2(out[: max(b1 - b0, 0)], b0, max(b1, b0))
+    if b1 > b0:
+        z = stage2(out[: b1 - b0], b0, b1)
+    else:
+        if m is None:
+            raise ValueError("combine: mode 'sx' needs m when a rank owns no buckets")
+        z = torch.zeros((m, d), dtype=flat.dtype, device=flat.device).t().contiguous().t()
     dist.all_reduce(z, group=group)
     return z

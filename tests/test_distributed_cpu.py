@@ -34,7 +34,7 @@ def _problem():
     return rng.standard_normal((N, D))
 
 
-def _worker(rank, world, port, mode, out_path):
+def _worker(rank, world, port, mode, out_path, B=B):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     O = oracle.Restatement()
@@ -82,7 +82,7 @@ def _worker(rank, world, port, mode, out_path):
                 return torch.zeros((M, D), dtype=torch.float64)
             Gs = O.gaussian(g_seed, M, b1 - b0, c0=b0)
             return torch.from_numpy(np.ascontiguousarray(O.gemm(Gs, sx_slice.numpy())))
-        z = combine("sx", world=world, rank=rank, B=B, d=D,
+        z = combine("sx", world=world, rank=rank, B=B, d=D, m=M,
                     partial_sx=torch.from_numpy(np.ascontiguousarray(sx_p)), stage2=stage2)
     if rank == 0:
         np.save(out_path, z.numpy())
@@ -96,6 +96,16 @@ def test_multi_rank_combine_matches_single_device(tmp_path, mode, world):
     mp.spawn(_worker, args=(world, _free_port(), mode, out), nprocs=world, join=True)
     z = np.load(out)
     z_ref, _ = oracle.Restatement().countgauss(SEED, M, B, x=_problem())
+    assert np.linalg.norm(z - z_ref) / np.linalg.norm(z_ref) <= 1e-13
+
+
+def test_sx_combine_with_fewer_buckets_than_ranks_chunks(tmp_path):
+    """B = 5 over 4 ranks: ceil(5/4) = 2-bucket chunks, so rank 3 owns no buckets (its
+    range is clamped to [5, 5)) and contributes a zero Z."""
+    out = str(tmp_path / "z_sx5.npy")
+    mp.spawn(_worker, args=(4, _free_port(), "sx", out, 5), nprocs=4, join=True)
+    z = np.load(out)
+    z_ref, _ = oracle.Restatement().countgauss(SEED, M, 5, x=_problem())
     assert np.linalg.norm(z - z_ref) / np.linalg.norm(z_ref) <= 1e-13
 
 

@@ -1,0 +1,116 @@
+"""Device groups (group.cu): the C-ABI multi-GPU path -- row shards built from the shared
+seed, partials combined over NCCL (CGX_COMBINE_G / _SX / _Z).  One GPU is available to the
+tests, so the group has one rank here: the plumbing (NCCL communicator, collectives,
+shard bookkeeping, host and device-sharded inputs) runs for real and Z must equal the
+single-context apply within the Z bar.  The multi-rank combine arithmetic is covered on CPU
+by tests/test_distributed_cpu.py (gloo, world 2-4)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1606_05732_b200._lib import (CGX_COL_MAJOR, CGX_COMBINE_G, CGX_COMBINE_SX, CGX_COMBINE_Z, CGX_F32, CGX_F64,
+                                        CGX_I32, CGX_I64, CGX_MEM_DEVICE, CGX_MEM_HOST, CGX_ROW_MAJOR, lib)
+
+pytestmark = pytest.mark.gpu
+Z_TOL = 1e-12
+MODES = [CGX_COMBINE_G, CGX_COMBINE_SX, CGX_COMBINE_Z]
+
+
+@pytest.fixture(scope="module")
+def group(cg):
+    g = C.c_void_p()
+    devs = (C.c_int * 1)(0)
+    assert lib.cgx_group_init(1, devs, C.byref(g)) == 0, lib.cgx_last_error()
+    assert lib.cgx_group_size(g) == 1
+    yield g
+    assert lib.cgx_group_free(g) == 0
+
+
+def _gx(group, m, B, n, seed):
+    t = C.c_void_p()
+    t_seed = oracle.draw(seed, 0)
+    assert lib.cgx_group_countgauss_new(group, t_seed, m, B, n, C.byref(t)) == 0, lib.cgx_last_error()
+    r0, rows = C.c_int64(), C.c_int64()
+    assert lib.cgx_gxform_shard(t, 0, C.byref(r0), C.byref(rows)) == 0
+    assert (r0.value, rows.value) == (0, n)
+    return t
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_group_dense_host_input(cg, group, restatement, mode):
+    n, d, B, m, seed = 50000, 24, 4099, 20, 2024
+    t = _gx(group, m, B, n, seed)
+    x = restatement.gen_dense_f32(5, n, d).astype(np.float64)
+    z_ref, _ = restatement.countgauss(seed, m, B, x=x)
+    for arr, dt, lay in [(np.asfortranarray(x), CGX_F64, CGX_COL_MAJOR),
+                         (np.ascontiguousarray(x.astype(np.float32)), CGX_F32, CGX_ROW_MAJOR)]:
+        z = np.zeros((d, m), np.float64)  # column-major m x d
+        ld = n if lay == CGX_COL_MAJOR else d
+        rc = lib.cgx_group_countgauss_apply_dense(group, t, arr.ctypes.data, dt, lay, ld, n, d, CGX_MEM_HOST,
+                                                  z.ctypes.data, CGX_MEM_HOST, mode)
+        assert rc == 0, lib.cgx_last_error()
+        assert rel(z.T, z_ref) <= Z_TOL
+    assert lib.cgx_gxform_free(t) == 0
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_group_dense_device_shards(cg, group, mode):
+    import torch
+
+    from paper_1606_05732_b200 import bench_data
+
+    n, d, B, m, seed = 1 << 20, 32, 65536, 64, 7
+    t = _gx(group, m, B, n, seed)
+    x = bench_data.dense_normal(n, d, seed=3)
+    xs = (C.c_void_p * 1)(x.data_ptr())
+    zd = torch.empty((d, m), dtype=torch.float64, device="cuda")
+    zs = (C.c_void_p * 1)(zd.data_ptr())
+    torch.cuda.synchronize()
+    rc = lib.cgx_group_countgauss_apply_dense(group, t, xs, CGX_F32, CGX_ROW_MAJOR, d, n, d, CGX_MEM_DEVICE, zs,
+                                              CGX_MEM_DEVICE, mode)
+    assert rc == 0, lib.cgx_last_error()
+    tt = cg.countgauss_new(m, B, n, cg.SeededRng(seed))
+    z1 = cg.countgauss_apply(tt, x)
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(zd.t() - z1) / torch.linalg.norm(z1)).item() <= Z_TOL
+    assert lib.cgx_gxform_free(t) == 0
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_group_csr_host_input(cg, group, restatement, mode):
+    n, d, B, m, seed = 60000, 300, 5000, 16, 99
+    t = _gx(group, m, B, n, seed)
+    rng = np.random.default_rng(4)
+    lens = rng.integers(0, 12, n)
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    cols = np.concatenate([np.sort(rng.choice(d, k, replace=False)) for k in lens]).astype(np.int64)
+    vals = rng.standard_normal(rp[-1])
+    z_ref, _ = restatement.countgauss(seed, m, B, csr=(rp, cols, vals, d))
+    for ci, it in [(cols, CGX_I64), (cols.astype(np.int32), CGX_I32)]:
+        z = np.zeros((d, m), np.float64)
+        rc = lib.cgx_group_countgauss_apply_csr(group, t, rp.ctypes.data, ci.ctypes.data, it, vals.ctypes.data, CGX_F64,
+                                                n, d, int(rp[-1]), z.ctypes.data, CGX_MEM_HOST, mode)
+        assert rc == 0, lib.cgx_last_error()
+        assert rel(z.T, z_ref) <= Z_TOL
+    assert lib.cgx_gxform_free(t) == 0
+
+
+def test_group_errors(cg, group):
+    t = _gx(group, 4, 64, 100, 1)
+    x = np.zeros((100, 3))
+    z = np.zeros((3, 4))
+    assert lib.cgx_group_countgauss_apply_dense(group, t, x.ctypes.data, CGX_F64, CGX_ROW_MAJOR, 3, 100, 3,
+                                                CGX_MEM_HOST, z.ctypes.data, CGX_MEM_HOST, 7) == 1
+    assert lib.cgx_group_countgauss_apply_dense(group, t, x.ctypes.data, CGX_F64, CGX_ROW_MAJOR, 3, 99, 3,
+                                                CGX_MEM_HOST, z.ctypes.data, CGX_MEM_HOST, CGX_COMBINE_G) == 1
+    assert "rows" in lib.cgx_last_error().decode()
+    bad = C.c_void_p()
+    assert lib.cgx_group_init(0, None, C.byref(bad)) == 1
+    assert lib.cgx_gxform_free(t) == 0
