@@ -317,7 +317,9 @@ void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
     stage_csr(ctx, &rp, &cp, &idx_type, &vp, &dtype, n, nnz, x_mem, s);
     ctx->prof.begin(0, s);
     const int64_t chunk_rows = csr_chunk_rows(n, xf->B, d);
-    if (chunk_rows == 0 && csr_partition_applies(ctx, n, xf->B, d, nnz))
+    if (chunk_rows == 0 && csr_atomic_applies(ctx, xf, n, d, nnz, dtype))
+        launch_sketch_csr_atomic(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, n, d, nnz, sx_dev, s);
+    else if (chunk_rows == 0 && csr_partition_applies(ctx, n, xf->B, d, nnz))
         launch_sketch_csr_partition(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, nnz, sx_dev, s);
     else
         launch_sketch_csr(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, sx_dev, chunk_rows, s);
@@ -1273,8 +1275,12 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_ws_gw = value;
         else if (k == "async_stages" && (value == 0 || (value >= 2 && value <= 4)))
             ctx->opt_async = value;
-        else if (k == "csr_mode" && value >= 0 && value <= 2)
+        else if (k == "csr_mode" && value >= 0 && value <= 3)
             ctx->opt_csr_mode = value;
+        else if (k == "csr_slice_mb" && value >= 1 && value <= 1024)
+            ctx->opt_csr_slice_mb = value;
+        else if (k == "csr_sc" && value >= 0 && value <= 3)
+            ctx->opt_csr_sc = value;
         else if (k == "g_resident" && (value == 0 || value == 1))
             ctx->opt_g_resident = value;
         else if (k == "gemm_ws" && (value == 0 || value == 1))

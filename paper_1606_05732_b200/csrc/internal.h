@@ -91,7 +91,9 @@ struct cgx_ctx {
     int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
     int64_t opt_ws_gw = 0;                  // option "ws_gw": buckets per sketch warp per tile (0 = auto)
     int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)
-    int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 2 stable partition
+    int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 2 stable partition, 3 records + L2 atomics
+    int64_t opt_csr_slice_mb = 8;           // option "csr_slice_mb": S.X slice per partition of the record path
+    int64_t opt_csr_sc = 0;                 // option "csr_sc": record-scatter variant (rows per lane, CTAs per SM)
     int64_t opt_gemm_ws = 0;                // option "gemm_ws": warp-specialized bulk-copy stage-2 GEMM
     int64_t opt_gemm_tile = 0;              // option "gemm_tile": 1 = 8-warp 64x128/128x64 large-Z tiles
     int64_t opt_gemm_chunks = 0;            // option "gemm_chunks": 1 = 48 MB K-chunks even when G is in memory
@@ -181,6 +183,10 @@ void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr,
 
 // csr_partition.cu: the same S.X by stable two-level partition of the nonzeros (short rows)
 bool csr_partition_applies(const cgx_ctx* ctx, int64_t n, int64_t B, int64_t d, int64_t nnz);
+// csr_atomic.cu: bucket-range partitioned records + L2-resident fp64 RED (short-row CSR)
+bool csr_atomic_applies(const cgx_ctx* ctx, const cgx_xform* xf, int64_t n, int64_t d, int64_t nnz, int dtype);
+void launch_sketch_csr_atomic(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
+                              const void* vals, int64_t n, int64_t d, int64_t nnz, double* sx, cudaStream_t s);
 void launch_sketch_csr_partition(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols,
                                  int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
                                  double* sx, cudaStream_t s);
