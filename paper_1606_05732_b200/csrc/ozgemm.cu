@@ -418,6 +418,14 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                     bulk_g2s(smem + sp.idx * STAGE, ga + i * A_BYTES, A_BYTES, &full[sp.idx]);
                 }
             }
+            // producer tail: the last stages' empty[] phases count every cluster peer's commit
+            // (an asynchronous multicast arrive), so once they complete no peer still has an
+            // arrive in flight towards this CTA's shared memory when the teardown sync lets it
+            // exit
+            if (csize > 1) {
+                const int64_t i0 = nk > OZ_STAGES ? nk - OZ_STAGES : 0;
+                for (int64_t i = i0; i < nk; ++i) mbar_wait(&empty[i % OZ_STAGES], (unsigned)((i / OZ_STAGES) & 1));
+            }
         }
         __syncwarp();
     } else if (warp == W_RAW) {
@@ -474,6 +482,47 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     if (warp == W_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// Rows of G and columns of S.X that the digit planes cannot represent -- a maximum that is
+// NaN or +-Inf (bits >= 0x7ff0...), or below 2^-960 (the scale 2^(8S-2-E) would overflow)
+// -- get their Z entries recomputed here in plain fp64, the reference's way (gemm,
+// matrix.cpp:111-129: ascending l, zero S.X entries skipped, separate multiply and add), so
+// NaN and Inf propagate as they do there.  Launched after every tensor-core stage 2; a block
+// whose row / column is representable returns at once.
+__device__ __forceinline__ bool oz_bad(unsigned long long bits) {
+    const unsigned long long e = bits >> 52;
+    return e >= 0x7ff || (bits != 0 && e < 63);
+}
+
+__global__ void oz_fixup(const double* __restrict__ g, const double* __restrict__ sx, int64_t m, int64_t K, int64_t d,
+                         const unsigned long long* __restrict__ amax_a, const unsigned long long* __restrict__ amax_b,
+                         double* __restrict__ z) {
+    const int64_t b = blockIdx.x;
+    if (b < d) {  // column b of Z
+        if (!oz_bad(amax_b[b])) return;
+        for (int64_t r = threadIdx.x; r < m; r += blockDim.x) {
+            double acc = 0.0;
+            for (int64_t l = 0; l < K; ++l) {
+                const double x = sx[l * d + b];
+                if (x == 0.0) continue;
+                acc = __dadd_rn(acc, __dmul_rn(g[l * m + r], x));
+            }
+            z[b * m + r] = acc;
+        }
+    } else {  // row r of Z
+        const int64_t r = b - d;
+        if (!oz_bad(amax_a[r])) return;
+        for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+            double acc = 0.0;
+            for (int64_t l = 0; l < K; ++l) {
+                const double x = sx[l * d + j];
+                if (x == 0.0) continue;
+                acc = __dadd_rn(acc, __dmul_rn(g[l * m + r], x));
+            }
+            z[j * m + r] = acc;
+        }
     }
 }
 
@@ -628,6 +677,9 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     count_launch(ctx);
     check_launch("oz_gemm");
     launch_reduce_splits(ctx, zpart, splits, m * d, z, s);
+    oz_fixup<<<(unsigned)(d + m), 128, 0, s>>>(xf->g_dev + b0 * m, sx, m, K, d, amax_a, amax_b, z);
+    count_launch(ctx);
+    check_launch("oz_fixup");
     return true;
 }
 

@@ -986,3 +986,27 @@ def test_full_size_checksums(cg, cfg):
     z_ref = g.t() @ sx
     torch.cuda.synchronize()
     assert (torch.linalg.norm(z - z_ref) / torch.linalg.norm(z_ref)).item() <= Z_TOL
+
+
+def test_stage2_tensor_core_nan_inf_and_tiny_columns(cg, restatement):
+    """The tcgen05 stage 2 (m*d >= 16384) on S.X columns its digit planes cannot represent:
+    a NaN, a +Inf, a -Inf and a column of magnitude ~1e-300 (below 2^-960).  Those columns
+    are recomputed in plain fp64 the reference's way (ozgemm.cu oz_fixup), so NaN and Inf
+    propagate into Z as in gemm (matrix.cpp:111-129) and the tiny column keeps its
+    relative accuracy; every other column stays within the Z bar."""
+    n, d, B, m, seed = 20000, 256, 4096, 128, 31
+    x = restatement.gen_dense_f32(3, n, d).astype(np.float64)
+    x[5, 3] = np.nan
+    x[7, 10] = np.inf
+    x[11, 20] = -np.inf
+    x[:, 40] *= 1e-300
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(seed))
+    z = cg.countgauss_apply(t, x)
+    z_ref, _ = restatement.countgauss(seed, m, B, x=x)
+    assert np.array_equal(np.isnan(z), np.isnan(z_ref))
+    assert np.array_equal(np.isinf(z), np.isinf(z_ref))
+    fin = np.isfinite(z_ref)
+    assert np.array_equal(z[np.isinf(z_ref)], z_ref[np.isinf(z_ref)])
+    for j in range(d):
+        if fin[:, j].all():
+            assert np.linalg.norm(z[:, j] - z_ref[:, j]) <= 1e-12 * np.linalg.norm(z_ref[:, j]), j
