@@ -186,19 +186,22 @@ def cpu_reference_run(cfg_name, c, steps, warmup):
                         f"{len(ms)} timed calls after {max(warmup, 1)} warm-up calls, median; reference code as-is"))
 
 
-def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000):
-    """CSR configs: the reference's countgauss_apply on a bounded row sample of the config's
-    X (its first rows, same generator), timed as the whole apply (kind 1) and as the sketch
-    alone (kind 0).  The full-size time is extrapolated as sketch_ms * nnz/nnz_sample +
-    (apply_ms - sketch_ms): the serial CSR sketch is linear in nnz, and the GEMM stage
-    (m x B by B x d) does not depend on n."""
+def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000, full_nnz_max=400_000_000):
+    """CSR configs: the reference's countgauss_apply (serial CSR branch + OpenMP gemm) on the
+    config's X.  c3 (172 M nnz, ~5 s per call) runs at FULL size, median of 3 after a
+    warm-up.  c5 (2.33e9 nnz, ~2 min per call on this host) runs a bounded row sample (its
+    first rows, same generator), timed as the whole apply and as the sketch alone, and the
+    full-size time is extrapolated as sketch_ms * nnz/nnz_sample + (apply_ms - sketch_ms):
+    the serial CSR sketch is linear in nnz, and the GEMM stage (m x B by B x d) does not
+    depend on n."""
     import numpy as np
     import torch
 
     from paper_1606_05732_b200 import bench_data
 
     mean = c.get("mean_row_nnz") or (c["d"] * c.get("density", 0.0) or 17.36)
-    rows = int(min(c["n"], max(1024, sample_nnz / mean)))
+    full = c["n"] * mean <= full_nnz_max
+    rows = c["n"] if full else int(min(c["n"], max(1024, sample_nnz / mean)))
     if "zipf" in c:
         s_len, cap, s_col = c["zipf"]
         x = bench_data.csr_zipf(rows, c["d"], seed=data_seed(cfg_name), s_len=s_len, cap=cap, s_col=s_col)
@@ -211,9 +214,18 @@ def _cpu_reference_csr(cfg_name, c, R, steps, cores, sample_nnz=20_000_000):
     del x
     torch.cuda.empty_cache()
     xm = R.csr(rp, ci, vv, rows, c["d"])
+    del rp, ci, vv
     t0 = time.time()
     xf = R.countgauss_new(c["m"], c["B"], rows, SEED)
     construct_s = time.time() - t0
+    if full:
+        reps = 3
+        ms_all, _ = xf.time_apply(xm, 1, reps)  # one untimed call first (cgref_time_apply)
+        med = statistics.median(ms_all)
+        return dict(value=nnz_s / (med / 1e3), ms=list(ms_all), median_ms=med, cores=cores, construct_s=construct_s,
+                    warmup=1, sample=(f"full {cfg_name} ({nnz_s} nnz, int64 columns / fp64 values, the reference "
+                                      f"SparseMatrix): countgauss_apply (serial CSR branch + OpenMP gemm), median of "
+                                      f"{reps} after 1 warm-up call"))
     reps = max(1, min(steps, 5))
     ms_all, _ = xf.time_apply(xm, 1, reps)
     ms_sk, _ = xf.time_apply(xm, 0, reps)
@@ -503,7 +515,11 @@ def run_ours(args):
         kernel_name = ("countgauss_dense_ws (one pass: sketch + G + G.(S.X))" if fused
                        else "sketch_dense_async (stage 1: cp.async row gather -> S.X)")
     else:
-        kernel_name = "sketch_csr_lean (stage 1: bucket-ordered row gather -> S.X)"
+        opts = dict(o.split("=", 1) for o in args.opt)
+        mode = int(opts.get("csr_mode", 0))
+        record = mode == 3 or (mode == 0 and nnz_local / rows < 8.0 and B * d >= (1 << 22) and nnz_local >= (1 << 22))
+        kernel_name = ("sketch phase, CSR record path (csr_atomic.cu: count + scatter + L2-atomic accumulate -> S.X)"
+                       if record else "sketch_csr_lean (stage 1: bucket-ordered row gather -> S.X)")
     sk_avg_ms = sk_ms / max(sk_n, 1)
     achieved = bytes_alg / (sk_avg_ms / 1e3) / 1e9
     traffic = None  # DRAM bytes per launch of this kernel, from the committed ncu capture
@@ -517,6 +533,32 @@ def run_ours(args):
 
     # e2e: same call with X in pinned host memory (H2D + D2H inside the timed region)
     e2e = None
+    if c["kind"] == "csr" and not args.no_e2e:
+        hx = cg.SparseMatrix(x.rows, x.cols, *(torch.empty(a.shape, dtype=a.dtype, pin_memory=True).copy_(a).numpy()
+                                               for a in (x.row_offsets, x.col_indices, x.values)))
+        cg.countgauss_apply(t, hx)
+        if world > 1:
+            dist.barrier()
+        ts = []
+        k_e2e = max(1, min(args.steps, 5))
+        for _ in range(k_e2e):
+            a = time.perf_counter()
+            zh = cg.countgauss_apply(t, hx)  # synchronous: returns with Z on the host
+            if world > 1:
+                zt = torch.from_numpy(zh.copy()).to(dev)
+                dist.all_reduce(zt)
+                zh = zt.cpu().numpy()
+            ts.append(time.perf_counter() - a)
+        e_s = statistics.median(ts)
+        if world > 1:
+            tt = torch.tensor([e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_s = float(tt[0])
+        e2e = {"value": tot_units / e_s, "unit": "nnz/s", "h2d_bytes_per_step": int(x_bytes),
+               "d2h_bytes_per_step": int(m * d * 8), "ms_per_step": e_s * 1e3, "steps": k_e2e,
+               "how": "cgx_countgauss_apply_csr with host (pinned) int64 row offsets, int32 columns, fp32 values; "
+                      "wall clock, median"}
+        del hx
     if c["kind"] == "dense" and not args.no_e2e:
         xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
         xh.copy_(x)
