@@ -526,7 +526,7 @@ def run_ours(args):
     try:
         tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
         ent = tr.get(args.config)
-        if ent and world == 1 and ent["kernel"] in kernel_name:
+        if ent and world == 1 and ent["kernel"] in kernel_name and ent.get("bytes"):
             traffic = ent["bytes"]
     except (OSError, ValueError, KeyError):
         traffic = None
