@@ -299,12 +299,14 @@ int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int6
  *                  it; 0: G is generated inside the apply kernels.  Set before construction.
  *   "fuse"         1 (default): the one-pass dense kernel (sketch + G + contraction) when G
  *                  is not resident; 2: also when it is; 0: always the two stages.
- *   "fuse_mode"    one-pass variant: 2 (default) warp-specialized, 1 all-warps, 3 G on a
- *                  side stream, 4 6+2 warps with Z in shared memory.
+ *   "fuse_mode"    one-pass variant: 2 (default) warp-specialized, 1 all-warps.
  *   "async_stages" dense row-gather ring depth: 2 (default), 3, 4; 0 = register batches.
- *   "csr_mode"     0/1 (default): bucket-ordered row gather; 2: stable two-level partition.
- *   "gemm_ws"      0 (default): cp.async-pipelined DMMA stage 2; 1: warp-specialized
- *                  bulk-copy producer (large Z whose tiles divide it).
+ *   "csr_mode"     0 (default): the record path for short-row CSR (fp32 values, < 8 nnz/row,
+ *                  >= 4M nnz, B*d >= 2^22; S.X to fp64 rounding), else the gather; 1: always
+ *                  the bucket-ordered row gather (S.X bit-identical to the reference); 3: the
+ *                  record path whenever it applies (csr_atomic.cu).
+ *   "csr_slice_mb", "csr_sc": the record path's S.X slice per partition (8 MB default) and
+ *                  scatter variant.
  *   "oz_slices"    stage 2 (gemm, matrix.cpp:111-129) on the tcgen05 int8 tensor cores with
  *                  FP64 emulated by S planes of 8-bit digits (ozgemm.cu): 7 (default; Z within
  *                  ~1e-14 of fp64), 6 (~7e-13), 5 (~1.5e-10), 3-4; 0 = always the FP64 DMMA

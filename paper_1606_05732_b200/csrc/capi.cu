@@ -319,8 +319,6 @@ void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
     const int64_t chunk_rows = csr_chunk_rows(n, xf->B, d);
     if (chunk_rows == 0 && csr_atomic_applies(ctx, xf, n, d, nnz, dtype))
         launch_sketch_csr_atomic(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, n, d, nnz, sx_dev, s);
-    else if (chunk_rows == 0 && csr_partition_applies(ctx, n, xf->B, d, nnz))
-        launch_sketch_csr_partition(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, nnz, sx_dev, s);
     else
         launch_sketch_csr(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, sx_dev, chunk_rows, s);
     ctx->prof.end(0, s);
@@ -427,9 +425,6 @@ int cgx_init(int device, cgx_ctx** out) {
         CGX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
         CGX_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         CGX_CUDA(cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming));
-        CGX_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-        CGX_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-        CGX_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         CGX_CUDA(cudaMalloc((void**)&ctx->task_ctr, sizeof(unsigned long long)));
         CGX_CUDA(cudaMemsetAsync(ctx->task_ctr, 0, sizeof(unsigned long long), ctx->stream));
         CGX_CUDA(cudaEventRecord(ctx->done, ctx->stream));
@@ -456,9 +451,6 @@ int cgx_free(cgx_ctx* ctx) {
                 cudaEventDestroy(e.second);
             }
         cudaEventDestroy(ctx->done);
-        cudaEventDestroy(ctx->ev_fork);
-        cudaEventDestroy(ctx->ev_join);
-        cudaStreamDestroy(ctx->aux);
         ctx->gfull.release();
         ctx->gchunk.release();
         for (DevBuf& b : ctx->part) b.release();
@@ -841,34 +833,6 @@ int cgx_countgauss_apply_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x,
         int64_t rld = ld;
         const void* xd = dense_rowmajor(ctx, xf, x, &dtype, layout, ld, n, d, x_mem, &rld, sc.st);
         if (d == 0) return;
-        // Overlapped stages: G (m x B, <= 64 MB, L2-resident) is generated on the side
-        // stream while the streaming sketch kernel reads X on the caller's stream -- the
-        // FP64-bound generator and the HBM-bound gather share the SMs -- then one small
-        // DMMA GEMM contracts the two.  The join is an event: no kernel waits on another.
-        const bool wide = d >= 17 && (dtype == CGX_F32 ? d % 4 == 0 || d <= 64 : d <= 64 || d % 2 == 0);
-        if (!ctx->no_fuse && ctx->fuse_mode == 3 && !xf->g_dev && wide &&
-            xf->m * xf->B * 8 <= (int64_t(64) << 20)) {
-            const size_t zb = sizeof(double) * (size_t)(xf->m * d);
-            double* zd = z_mem == CGX_MEM_HOST ? (double*)ctx->tmp.get(zb) : z;
-            double* gbuf = (double*)ctx->gfull.get(sizeof(double) * (size_t)(xf->m * xf->B));
-            double* sxd = (double*)ctx->sx.get(sizeof(double) * (size_t)(xf->B * d));
-            CGX_CUDA(cudaEventRecord(ctx->ev_fork, sc.st));
-            CGX_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-            launch_gen_gauss(ctx, xf, 0, xf->B, gbuf, ctx->aux);
-            CGX_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux));
-            ctx->prof.begin(0, sc.st);
-            launch_sketch_dense(ctx, xf, xd, dtype, rld, n, d, sxd, sc.st);
-            ctx->prof.end(0, sc.st);
-            CGX_CUDA(cudaStreamWaitEvent(sc.st, ctx->ev_join, 0));
-            ctx->prof.begin(1, sc.st);
-            launch_gemm_g_ready(ctx, xf, gbuf, sxd, d, zd, sc.st);
-            ctx->prof.end(1, sc.st);
-            if (z_mem == CGX_MEM_HOST) {
-                CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
-                sc.sync();
-            }
-            return;
-        }
         // One-pass kernel (sketch + G generation + contraction) when G must be generated and
         // rows are narrow (d <= 64).  With G in memory, or wide rows, the two stages win: the
         // cp.async stream sketch leaves S.X in L2 and the split-K DMMA contraction streams G
@@ -1263,7 +1227,7 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
         if (k == "fuse") {
             ctx->no_fuse = value == 0;
             ctx->force_fuse = value == 2;
-        } else if (k == "fuse_mode")
+        } else if (k == "fuse_mode" && (value == 1 || value == 2))
             ctx->fuse_mode = (int)value;
         else if (k == "rows_per_task" && value >= 1)
             ctx->opt_rows_per_task = value;
@@ -1275,7 +1239,7 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_ws_gw = value;
         else if (k == "async_stages" && (value == 0 || (value >= 2 && value <= 4)))
             ctx->opt_async = value;
-        else if (k == "csr_mode" && value >= 0 && value <= 3)
+        else if (k == "csr_mode" && (value == 0 || value == 1 || value == 3))
             ctx->opt_csr_mode = value;
         else if (k == "csr_slice_mb" && value >= 1 && value <= 1024)
             ctx->opt_csr_slice_mb = value;
@@ -1283,8 +1247,6 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_csr_sc = value;
         else if (k == "g_resident" && (value == 0 || value == 1))
             ctx->opt_g_resident = value;
-        else if (k == "gemm_ws" && (value == 0 || value == 1))
-            ctx->opt_gemm_ws = value;
         else if (k == "gemm_tile" && (value == 0 || value == 1))
             ctx->opt_gemm_tile = value;
         else if (k == "oz_slices" && (value == 0 || (value >= 3 && value <= 7)))

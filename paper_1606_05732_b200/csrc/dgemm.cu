@@ -206,102 +206,6 @@ __global__ void __launch_bounds__(32 * WGM * WGN * KG,
             }
 }
 
-// Warp-specialized form of gemm_dmma for large Z (8 consumer warps of 32 x 32 DMMA tiles +
-// 1 producer warp): the producer moves k-tile t with 1-D bulk copies -- lane k copies row k
-// of the A tile (BM contiguous doubles of a G column) and lane 16 + k row k of the B tile
-// (BN doubles of an S.X row) -- completing on full[stage]; consumers wait on full[stage],
-// run their DMMAs and release the stage on empty[stage].  No CTA barrier and no per-tile
-// index arithmetic in the consumers.  Requires m % BM == 0, d % BN == 0 and 16 B aligned
-// rows.  Option gemm_ws = 1; it measures within 3% of gemm_dmma (c5 9.8 vs 9.5 ms) once the
-// split-K grid is sized to one wave, so gemm_dmma stays the default.
-constexpr int WS_STAGES = 4;
-template <int WGM, int WGN>
-__global__ void __launch_bounds__(32 * (WGM * WGN + 1), 1) gemm_dmma_ws(const double* __restrict__ A, int64_t m,
-                                                                       const double* __restrict__ Bm, int64_t d,
-                                                                       int64_t K, int64_t kps, double* __restrict__ C,
-                                                                       int accumulate) {
-    constexpr int BM = 32 * WGM, BN = 32 * WGN, NC = WGM * WGN;  // NC consumer warps
-    constexpr int LDA = BM + 4, LDB = BN + 4;
-    constexpr int S = WS_STAGES;
-    static_assert(BK <= 16, "one producer lane per tile row of A and of B");
-    extern __shared__ double dsm[];
-    double* As = dsm;                  // [S][BK][LDA]
-    double* Bs = dsm + S * BK * LDA;   // [S][BK][LDB]
-    __shared__ uint64_t full[S], empty[S];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
-    const int64_t split = blockIdx.z;
-    const int64_t kb = split * kps, ke = min(K, kb + kps);
-    const int ntiles = (int)((ke - kb + BK - 1) / BK);
-    if (tid == 0) {
-        for (int st = 0; st < S; ++st) {
-            mbar_init(&full[st], 1);
-            mbar_init(&empty[st], NC);
-        }
-    }
-    __syncthreads();
-    if (warp == NC) {  // ------------------------------------------------------ producer
-        for (int t = 0; t < ntiles; ++t) {
-            const int st = t % S;
-            if (t >= S) mbar_wait(&empty[st], (unsigned)(((t / S) - 1) & 1));
-            const int64_t k0 = kb + (int64_t)t * BK;
-            const int kv = (int)min((int64_t)BK, ke - k0);
-            double* as = As + st * BK * LDA;
-            double* bs = Bs + st * BK * LDB;
-            if (kv < BK) {  // K tail: zero rows kv.. of both tiles (last tile of a split only)
-                for (int e = lane; e < (BK - kv) * LDA; e += 32) as[kv * LDA + e] = 0.0;
-                for (int e = lane; e < (BK - kv) * LDB; e += 32) bs[kv * LDB + e] = 0.0;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_expect_tx(&full[st], (unsigned)(kv * (BM + BN) * sizeof(double)));
-            __syncwarp();
-            if (lane < kv) bulk_g2s(as + lane * LDA, A + (k0 + lane) * m + m0, BM * sizeof(double), &full[st]);
-            if (lane >= 16 && lane - 16 < kv)
-                bulk_g2s(bs + (lane - 16) * LDB, Bm + (k0 + lane - 16) * d + n0, BN * sizeof(double), &full[st]);
-        }
-        return;
-    }
-    // ------------------------------------------------------------------------ consumers
-    const int wm = warp % WGM, wn = warp / WGM;
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int t = 0; t < ntiles; ++t) {
-        const int st = t % S;
-        mbar_wait(&full[st], (unsigned)((t / S) & 1));
-        const double* as = As + st * BK * LDA + wm * 32 + (lane >> 2);
-        const double* bs = Bs + st * BK * LDB + wn * 32 + (lane >> 2);
-#pragma unroll
-        for (int k4 = 0; k4 < BK; k4 += 4) {
-            double a[4], b[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = as[(k4 + (lane & 3)) * LDA + i * 8];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = bs[(k4 + (lane & 3)) * LDB + j * 8];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-    }
-    double* cp = C + split * m * d;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t r = m0 + wm * 32 + i * 8 + (lane >> 2);
-                const int64_t c = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + h;
-                double* p = cp + c * m + r;
-                *p = accumulate ? *p + acc[i][j][h] : acc[i][j][h];
-            }
-}
-
 // G columns [c0, c0 + cols) -> out (m x cols, column-major).
 __global__ void gen_gauss_cols(uint64_t g_seed, int64_t m, int64_t c0, int64_t cols, double* __restrict__ out) {
     const int64_t total = m * cols;
@@ -353,16 +257,8 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
     auto kern = v2 ? gemm_dmma<WGM, WGN, KG, true, FM, FN> : gemm_dmma<WGM, WGN, KG, false, FM, FN>;
     const size_t pipe = sizeof(double) * (size_t)(STAGES * BK * ((BM + 4) + (BN + 4)));
     const size_t fold = sizeof(double) * (size_t)((KG - 1) * BM * BN);  // KG > 1 only with FM = FN = 4
-    size_t smem = pipe > fold ? pipe : fold;
-    // warp-specialized bulk-copy pipeline when the tiles divide Z exactly
-    const bool ws = ctx->opt_gemm_ws && KG == 1 && FM == 4 && FN == 4 && WGM * WGN == 8 && v2 && m % BM == 0 &&
-                    d % BN == 0;
-    int nthreads = NT;
-    if (ws) {
-        kern = gemm_dmma_ws<WGM, WGN>;
-        smem = sizeof(double) * (size_t)(WS_STAGES * BK * ((BM + 4) + (BN + 4)));
-        nthreads = 32 * (WGM * WGN + 1);
-    }
+    const size_t smem = pipe > fold ? pipe : fold;
+    const int nthreads = NT;
     CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     bool first = true;
     for (int64_t c0 = 0; c0 < K; c0 += S) {
@@ -381,12 +277,8 @@ void run_chunks(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0,
             Ach = gbuf;
         }
         const int64_t sp = (cols + kps - 1) / kps;  // splits that have work in this chunk
-        if (ws)
-            kern<<<dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), nthreads, smem, s>>>(Ach, m, sx + c0 * d, d, cols,
-                                                                                         kps, zpart, first ? 0 : 1);
-        else
-            launch_pdl(ctx, kern, dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), dim3(nthreads), smem, s, Ach, m,
-                       sx + c0 * d, d, cols, kps, zpart, first ? 0 : 1);
+        launch_pdl(ctx, kern, dim3((unsigned)tm, (unsigned)tn, (unsigned)sp), dim3(nthreads), smem, s, Ach, m,
+                   sx + c0 * d, d, cols, kps, zpart, first ? 0 : 1);
         count_launch(ctx);
         check_launch("gemm_dmma");
         if (first && sp < splits)  // splits without work in the first chunk start at zero
@@ -487,16 +379,6 @@ void launch_gauss_gemm_rows(cgx_ctx* ctx, const cgx_xform* xf, const double* sx,
     gx.oz_gmax = nullptr;
     gx.oz_gS = 0;
     launch_gauss_gemm(ctx, &gx, sx, 0, B, d, z, s);
-}
-
-void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, const double* sx, int64_t d, double* z,
-                         cudaStream_t s) {
-    if (xf->m >= 8 * d)
-        run_chunks<8, 1>(ctx, xf, sx, 0, xf->B, d, z, s, g);  // 256 x 32 tiles
-    else if (xf->m >= 2 * d)
-        run_chunks<4, 2>(ctx, xf, sx, 0, xf->B, d, z, s, g);
-    else
-        run_chunks<2, 4>(ctx, xf, sx, 0, xf->B, d, z, s, g);
 }
 
 } // namespace cgx

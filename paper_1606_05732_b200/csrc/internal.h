@@ -64,9 +64,7 @@ struct cgx_ctx {
     unsigned long long* task_ctr = nullptr;
     unsigned long long task_base = 0;
     cgx::DevBuf gen_tables;                 // synthetic-input generator tables
-    cudaStream_t aux = nullptr;             // side stream: G generation overlapping the sketch
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    cgx::DevBuf gfull;                      // L2-sized G for the overlapped two-stage path
+    cgx::DevBuf gfull;                      // rows of G for the split-over-m stage 2 (gen_gauss_rows)
     cgx::DevBuf gchunk;                     // G super-chunk of the chunked stage 2 (dgemm.cu)
     void* pinned = nullptr;                 // pinned staging for pageable host inputs
     size_t pinned_bytes = 0;
@@ -85,20 +83,19 @@ struct cgx_ctx {
     std::unordered_map<void*, size_t> pool_class;
     bool no_fuse = false;                  // option "fuse"=0: always run the two stages
     bool force_fuse = false;               // option "fuse"=2: one-pass kernel even when G is in memory
-    int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps fused, 2 warp-specialized
+    int fuse_mode = 2;                      // option "fuse_mode": 1 all-warps one-pass, 2 warp-specialized
     int64_t opt_rows_per_task = 1024;       // option "rows_per_task": dense stream-kernel task size
     int64_t opt_tail_tasks = 2;             // option "tail_tasks": single-bucket tasks per warp at the end
     int64_t opt_grid_waves = 1;             // option "grid_waves": stream-kernel blocks = resident x waves
     int64_t opt_ws_gw = 0;                  // option "ws_gw": buckets per sketch warp per tile (0 = auto)
     int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)
-    int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 2 stable partition, 3 records + L2 atomics
+    int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 3 records + L2 atomics
     int64_t opt_csr_slice_mb = 8;           // option "csr_slice_mb": S.X slice per partition of the record path
     int64_t opt_csr_sc = 0;                 // option "csr_sc": record-scatter variant (rows per lane, CTAs per SM)
-    int64_t opt_gemm_ws = 0;                // option "gemm_ws": warp-specialized bulk-copy stage-2 GEMM
     int64_t opt_gemm_tile = 0;              // option "gemm_tile": 1 = 8-warp 64x128/128x64 large-Z tiles
     int64_t opt_gemm_chunks = 0;            // option "gemm_chunks": 1 = 48 MB K-chunks even when G is in memory
     int64_t opt_g_resident = 1;             // option "g_resident": materialize seeded G at construction (<= 4 GiB)
-    cgx::DevBuf part[6];                    // csr_partition.cu scratch: counters, payload copies, row keys
+    cgx::DevBuf part[6];                    // csr_atomic.cu scratch: counters, records, row hashes
     int64_t opt_pdl = 1;                    // option "pdl": stage-2 kernels launched as programmatic dependents
     int64_t opt_oz_slices = 7;              // option "oz_slices": stage 2 on tcgen05 int8 with S digit planes (0 = DMMA)
     int64_t opt_oz_min_z = 16384;           // option "oz_min_z": smallest m*d that takes the tcgen05 stage 2
@@ -181,15 +178,10 @@ void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr,
                        const void* vals, int dtype, int64_t n, int64_t d, double* sx, int64_t chunk_rows,
                        cudaStream_t s);
 
-// csr_partition.cu: the same S.X by stable two-level partition of the nonzeros (short rows)
-bool csr_partition_applies(const cgx_ctx* ctx, int64_t n, int64_t B, int64_t d, int64_t nnz);
 // csr_atomic.cu: bucket-range partitioned records + L2-resident fp64 RED (short-row CSR)
 bool csr_atomic_applies(const cgx_ctx* ctx, const cgx_xform* xf, int64_t n, int64_t d, int64_t nnz, int dtype);
 void launch_sketch_csr_atomic(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
                               const void* vals, int64_t n, int64_t d, int64_t nnz, double* sx, cudaStream_t s);
-void launch_sketch_csr_partition(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols,
-                                 int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
-                                 double* sx, cudaStream_t s);
 
 // gauss_gemm.cu: z (col-major m x d) = G . sx (row-major B x d)
 // Buckets [b0, b1) only: sx points at row b0 (split-K across ranks).
@@ -207,9 +199,6 @@ void launch_gauss_gemm_rows(cgx_ctx* ctx, const cgx_xform* xf, const double* sx,
 // generated in L2-resident chunks; false when not applicable
 bool launch_gemm_small_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
                                int64_t d, double* z, cudaStream_t s);
-// dgemm.cu: z = g . sx with g = all of G (m x B col-major) already in memory
-void launch_gemm_g_ready(cgx_ctx* ctx, const cgx_xform* xf, const double* g, const double* sx, int64_t d, double* z,
-                         cudaStream_t s);
 // dgemm.cu: G super-chunks + pipelined DMMA GEMM; false when Z is small (not used)
 bool launch_gauss_gemm_chunked(cgx_ctx* ctx, const cgx_xform* xf, const double* sx, int64_t b0, int64_t b1,
                                int64_t d, double* z, cudaStream_t s, bool force = false);

@@ -743,126 +743,6 @@ __global__ void __launch_bounds__(384, 2) countgauss_dense_ws(const T* __restric
     }
 }
 
-// Variant with more HBM parallelism per SM: CTA = 6 sketch warps + 2 math warps at 64
-// registers, so 4 CTAs (24 sketch warps, 96 KB of row loads in flight) fit per SM.  The
-// math warps keep Z in shared memory (each (row, column) owned by one thread, fixed
-// accumulation order) since 2 warps cannot hold an m x 32V tile in registers.
-template <typename T, int V>
-__global__ void __launch_bounds__(256, 4) countgauss_dense_ws2(const T* __restrict__ x, int64_t ld, int64_t d,
-                                                               const uint32_t* __restrict__ perm,
-                                                               const uint32_t* __restrict__ offsets, int64_t B,
-                                                               int64_t m, uint64_t g_seed,
-                                                               const double* __restrict__ g_explicit, int Gw,
-                                                               double* __restrict__ zpart) {
-    constexpr int SKW = 6, MT = 64;  // sketch warps, math threads
-    constexpr int CW = 32 * V;
-    extern __shared__ double fsm[];
-    __shared__ uint64_t full[2], freed[2];
-    const int TB = SKW * Gw;
-    const int slab_sz = TB * CW + (int)m * TB;  // S.X [TB][CW], then G [m][TB]
-    double* sZ = fsm + 2 * slab_sz;              // [m][CW]
-    const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntiles = (B + TB - 1) / TB;
-    if (tid == 0) {
-        mbar_init(&full[0], SKW * 32);
-        mbar_init(&full[1], SKW * 32);
-        mbar_init(&freed[0], MT);
-        mbar_init(&freed[1], MT);
-    }
-    for (int e = tid; e < (int)m * CW; e += blockDim.x) sZ[e] = 0.0;
-    __syncthreads();
-
-    if (warp < SKW) {  // -------------------------------------------------------- sketch
-        const int64_t col0 = (int64_t)lane * V;
-        const bool colok = col0 < d;
-        int64_t k = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-            const int buf = (int)(k & 1);
-            if (k >= 2) mbar_wait(&freed[buf], (unsigned)(((k - 2) >> 1) & 1));
-            double* slab = fsm + buf * slab_sz + (int64_t)warp * Gw * CW + lane * V;
-            const int64_t b0 = tile * TB + (int64_t)warp * Gw;
-            const int nb = b0 < B ? (int)min((int64_t)Gw, B - b0) : 0;
-            if (nb > 0) {
-                stream_buckets<T, V, 4096>(x, ld, col0, colok, perm, offsets, b0, nb,
-                                           [&](int i, const double (&acc)[V]) {
-#pragma unroll
-                                               for (int q = 0; q < V; ++q) slab[i * CW + q] = colok ? acc[q] : 0.0;
-                                           });
-            }
-            for (int i = nb; i < Gw; ++i)
-#pragma unroll
-                for (int q = 0; q < V; ++q) slab[i * CW + q] = 0.0;
-            mbar_arrive(&full[buf]);
-        }
-        return;
-    }
-    // ------------------------------------------------------------------------------ math
-    const int mt = (int)tid - SKW * 32;  // 0..63
-    const int c = mt & 31, rsel = mt >> 5;  // column lane, row parity
-    int64_t k = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-        const int buf = (int)(k & 1);
-        const double* sSX = fsm + buf * slab_sz;
-        double* sG = fsm + buf * slab_sz + TB * CW;
-        const int64_t tb0 = tile * TB;
-        for (int e = mt; e < (int)m * TB; e += MT) {
-            const int s = e / (int)m, r = e - s * (int)m;
-            const int64_t b = tb0 + s;
-            double g = 0.0;
-            if (b < B) g = g_explicit ? g_explicit[b * m + r] : gauss_entry(g_seed, (uint64_t)m, (uint64_t)r, (uint64_t)b);
-            sG[r * TB + s] = g;
-        }
-        named_sync(1, MT);
-        mbar_wait(&full[buf], (unsigned)((k >> 1) & 1));
-        for (int r = rsel; r < m; r += 2) {
-            const double* grow = sG + (int64_t)r * TB;
-            double z[V];
-#pragma unroll
-            for (int q = 0; q < V; ++q) z[q] = sZ[r * CW + c * V + q];
-            for (int s = 0; s < TB; ++s) {
-                const double gv = grow[s];
-#pragma unroll
-                for (int q = 0; q < V; ++q) z[q] = fma(gv, sSX[s * CW + c * V + q], z[q]);
-            }
-#pragma unroll
-            for (int q = 0; q < V; ++q) sZ[r * CW + c * V + q] = z[q];
-        }
-        mbar_arrive(&freed[buf]);
-    }
-    named_sync(1, MT);
-    double* zp = zpart + (int64_t)blockIdx.x * m * d;
-    for (int e = mt; e < (int)m * CW; e += MT) {
-        const int r = e / CW, col = e - r * CW;
-        if (col < d) zp[(int64_t)col * m + r] = sZ[e];
-    }
-}
-
-template <typename T, int V>
-void launch_ws2(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
-    constexpr int CW = 32 * V;
-    const int64_t B = xf->B, m = xf->m;
-    auto kern = countgauss_dense_ws2<T, V>;
-    // Tiles are assigned statically (so Z's summation grouping is fixed); many small tiles
-    // per CTA keep the last round's imbalance small.
-    int64_t Gw = B / (6 * 32 * (int64_t)ctx->num_sms * 4);
-    Gw = Gw < 1 ? 1 : (Gw > 8 ? 8 : Gw);
-    if (ctx->opt_ws_gw > 0) Gw = ctx->opt_ws_gw;
-    const int64_t TB = 6 * Gw;
-    const int64_t ntiles = (B + TB - 1) / TB;
-    const size_t smem = sizeof(double) * (size_t)(2 * (TB * CW + m * TB) + m * CW);
-    CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-    if (per_sm < 1) per_sm = 1;
-    const int64_t grid_cap = (int64_t)ctx->num_sms * per_sm;
-    const int64_t grid = ntiles < grid_cap ? ntiles : grid_cap;
-    double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(grid * m * d));
-    kern<<<(unsigned)grid, 256, smem, s>>>(x, ld, d, xf->perm, xf->offsets, B, m, xf->g_seed,
-                                           xf->g_dev, (int)Gw, zpart);
-    count_launch(ctx);
-    check_launch("countgauss_dense_ws2");
-    launch_reduce_splits(ctx, zpart, grid, m * d, z, s);
-}
 
 template <typename T, int V, int MR>
 void launch_ws(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
@@ -923,11 +803,7 @@ void launch_fused(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int
 template <typename T, int V>
 bool fused_rw(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* z, cudaStream_t s) {
     const int64_t m = xf->m;
-    if (ctx->fuse_mode == 4) {  // warp-specialized, 6+2 warps, Z in shared memory
-        const size_t smem = sizeof(double) * (size_t)(2 * (6 * 32 * V + m * 6) + m * 32 * V);
-        if (smem <= 200 * 1024) return launch_ws2<T, V>(ctx, xf, x, ld, d, z, s), true;
-    }
-    if (ctx->fuse_mode == 2 || ctx->fuse_mode == 4) {  // warp-specialized
+    if (ctx->fuse_mode == 2) {  // warp-specialized
         if (m <= 4) return launch_ws<T, V, 1>(ctx, xf, x, ld, d, z, s), true;
         if (m <= 8) return launch_ws<T, V, 2>(ctx, xf, x, ld, d, z, s), true;
         if (m <= 16) return launch_ws<T, V, 4>(ctx, xf, x, ld, d, z, s), true;

@@ -276,7 +276,6 @@ def _csr_with_dups(rng, n, d, mean_len):
     return rp, c, v
 
 
-@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("n,d,B,mean_len,idx,val", [
     (60000, 256, 262144, 2.5, np.int32, np.float32),   # c3-like: B >> n/B, short rows
     (40000, 256, 4099, 2.5, np.int64, np.float64),
@@ -286,21 +285,22 @@ def _csr_with_dups(rng, n, d, mean_len):
     (20000, 40, 5, 6.0, np.int32, np.float32),         # few buckets: long runs per bin
     (25000, 1000, 33333, 3.0, np.int32, np.float64),   # d not a power of two, padded slices
 ])
-def test_csr_partition_bit_exact(cg, restatement, mode, n, d, B, mean_len, idx, val):
-    """Stable two-level partition (csr_mode 2) and row gather (1): S.X bit-exact against the
-    oracle, including duplicate columns inside a row and empty rows."""
+def test_csr_gather_bit_exact(cg, restatement, n, d, B, mean_len, idx, val):
+    """The bucket-ordered row gather (csr_mode 1): S.X bit-exact against the oracle, including
+    duplicate columns inside a row and empty rows (the record path, csr_mode 3, has its own
+    tests in test_csr_atomic.py)."""
     rng = np.random.default_rng(n + d + B)
     rp, c, v = _csr_with_dups(rng, n, d, mean_len)
     c, v = c.astype(idx), v.astype(val)
     seed = 5 + d
     ctx = cg.context()
-    ctx.set_option("csr_mode", mode)
+    ctx.set_option("csr_mode", 1)
     try:
         t = cg.countgauss_new(8, B, n, cg.SeededRng(seed))
         x = cg.SparseMatrix(n, d, rp, c, v)
         sx = cg.countsketch_apply(t, x)
         z = cg.countgauss_apply(t, x)
-        # explicit map with the same hash/sign: the partition's per-row keys come from perm
+        # explicit map with the same hash/sign
         mp = cg.CountSketchMap.from_arrays(B, t.cs.hash, t.cs.sign)
         sx_explicit = cg.countsketch_apply(mp, x)
     finally:
@@ -348,20 +348,18 @@ def test_csr_zipf_config5_shape(cg, restatement):
     assert rel_fro(cg.countgauss_apply(t, x).cpu().numpy(), z_ref) <= Z_TOL
 
 
-@pytest.fixture(params=[0, 1], ids=["gemm-pipelined", "gemm-warp-specialized"])
-def gemm_ws(request, cg):
+@pytest.fixture
+def dmma_stage2(cg):
     """The DMMA stage 2 (large Z otherwise goes to the tensor-core path, ozgemm.cu)."""
     ctx = cg.context()
-    ctx.set_option("gemm_ws", request.param)
     ctx.set_option("oz_slices", 0)
-    yield request.param
-    ctx.set_option("gemm_ws", 0)
+    yield
     ctx.set_option("oz_slices", 7)
 
 
 @pytest.mark.parametrize("m,d,B", [(96, 300, 20011), (256, 512, 40000), (130, 70, 9000), (64, 129, 33333),
                                    (128, 256, 30000)])
-def test_stage2_large_z(cg, restatement, m, d, B, g_mode, gemm_ws):
+def test_stage2_large_z(cg, restatement, m, d, B, g_mode, dmma_stage2):
     """Stage 2 on its own (gemm(t.g, SX), matrix.cpp:111-129) for Z shapes that take the
     G-super-chunk + pipelined DMMA path, with G seeded (generated) and explicit."""
     import ctypes as C
@@ -605,11 +603,10 @@ def test_device_tensors_match_host(cg, restatement):
 @pytest.mark.parametrize("d,m,dtype", [(32, 64, np.float32), (24, 16, np.float32), (64, 32, np.float32),
                                        (128, 32, np.float32), (100, 8, np.float32), (32, 64, np.float64),
                                        (64, 64, np.float64), (40, 100, np.float32), (33, 5, np.float64)])
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2])
 def test_fused_matches_two_stage(cg, restatement, d, m, dtype, mode, g_mode):
     """The one-pass kernels (sketch + G + contraction; mode 1 all-warps, mode 2
-    warp-specialized) and mode 3 (G generated on a side stream under the sketch, then a
-    DMMA GEMM) vs the two-stage path and the oracle."""
+    warp-specialized) vs the two-stage path and the oracle."""
     import torch
 
     rng = np.random.default_rng(d * 1000 + m)
