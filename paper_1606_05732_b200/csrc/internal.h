@@ -265,6 +265,16 @@ const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, 
 uint64_t host_checksum(cgx_ctx* ctx, const void* p, size_t bytes);
 void host_pool_free(cgx_ctx* ctx);
 
+// Rows per task of the persistent gather kernels: the option's ~1K rows, fewer when the
+// input is small (a row shard) so that every one of the ~num_sms * 32 resident warps gets at
+// least two tasks -- with fewer tasks than warps, each warp walked one long task with one
+// chunk in flight and c2's sketch at n/8 rows took 90 us against ~45 us of streaming.
+inline int64_t rows_per_task(const cgx_ctx* ctx, int64_t n) {
+    const int64_t fair = n / ((int64_t)ctx->num_sms * 32 * 2);
+    int64_t r = ctx->opt_rows_per_task < fair ? ctx->opt_rows_per_task : fair;
+    return r < 64 ? 64 : r;
+}
+
 inline void count_launch(cgx_ctx* ctx, int k = 1) { ctx->launches += (uint64_t)k; }
 // Launch as a programmatic dependent of the previous kernel in the stream (option "pdl"): its
 // CTAs start while that kernel's last CTAs drain and wait in pdl_wait for its results.

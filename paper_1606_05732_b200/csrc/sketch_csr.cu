@@ -391,7 +391,7 @@ bool launch_lean(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const
     // tasks of ~rows_per_task rows (whole buckets), single buckets for the last tail_tasks
     // per warp
     const int64_t rows_per_bucket = xf->n / nb_total + 1;
-    int64_t G = ctx->opt_rows_per_task / rows_per_bucket;
+    int64_t G = rows_per_task(ctx, xf->n) / rows_per_bucket;
     G = G < 1 ? 1 : (G > 64 ? 64 : G);
     int64_t B1 = nb_total - ctx->opt_tail_tasks * nb * wl;
     B1 = B1 < 0 ? 0 : B1 / G * G;

@@ -555,7 +555,7 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
     if (R == 1 && !accumulate && ld * (int64_t)sizeof(T) < ((int64_t)1 << 32)) {
         // ~1K rows per warp task, at most 31 buckets (one offsets load)
         const int64_t rows_per_bucket = xf->n / xf->B + 1;
-        int64_t G = ctx->opt_rows_per_task / rows_per_bucket;
+        int64_t G = rows_per_task(ctx, xf->n) / rows_per_bucket;
         G = G < 1 ? 1 : (G > 31 ? 31 : G);
         const int64_t nchunks = (d + CW - 1) / CW;
         const int64_t tasks = (xf->B + G - 1) / G * nchunks;
