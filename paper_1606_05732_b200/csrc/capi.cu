@@ -1243,7 +1243,7 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_csr_mode = value;
         else if (k == "csr_slice_mb" && value >= 1 && value <= 1024)
             ctx->opt_csr_slice_mb = value;
-        else if (k == "csr_sc" && value >= 0 && value <= 3)
+        else if (k == "csr_sc" && value >= 0 && value <= 2)
             ctx->opt_csr_sc = value;
         else if (k == "g_resident" && (value == 0 || value == 1))
             ctx->opt_g_resident = value;

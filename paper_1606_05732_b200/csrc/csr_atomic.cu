@@ -127,6 +127,25 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
     constexpr int kWarps = kScThreads / 32;
     constexpr int kTile = kScThreads * kGroups;  // rows per tile
     const int64_t ntiles = (n + kTile - 1) / kTile;
+    // the next tile's row offsets and row records are loaded while this tile is staged and
+    // stored (the tile's phases are separated by barriers, so unhidden load latency at the
+    // start of every tile held the kernel at ~2.5 TB/s)
+    int64_t nrb[kGroups], nre[kGroups];
+    uint32_t nbk[kGroups];
+    auto prefetch = [&](int64_t t) {
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g) {
+            const int64_t row = t * kTile + g * kScThreads + threadIdx.x;
+            nrb[g] = nre[g] = 0;
+            nbk[g] = 0;
+            if (t < ntiles && row < n) {
+                nrb[g] = rowptr[row];
+                nre[g] = rowptr[row + 1];
+                nbk[g] = __ldcs(rowinfo + row);
+            }
+        }
+    };
+    prefetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int p = threadIdx.x; p < nparts; p += kScThreads) s_cnt[p] = 0;
         __syncthreads();
@@ -135,18 +154,13 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
         uint32_t bk[kGroups], off[kGroups];
 #pragma unroll
         for (int g = 0; g < kGroups; ++g) {
-            const int64_t row = tile * kTile + g * kScThreads + threadIdx.x;
-            rb[g] = 0;
-            len[g] = 0;
-            bk[g] = 0;
+            rb[g] = nrb[g];
+            len[g] = (int)(nre[g] - nrb[g]);
+            bk[g] = nbk[g];
             off[g] = 0;
-            if (row < n) {
-                rb[g] = rowptr[row];
-                len[g] = (int)(rowptr[row + 1] - rb[g]);
-                bk[g] = __ldcs(rowinfo + row);
-                if (len[g]) off[g] = atomicAdd(&s_cnt[(bk[g] >> 1) >> pshift], (uint32_t)len[g]);
-            }
+            if (len[g]) off[g] = atomicAdd(&s_cnt[(bk[g] >> 1) >> pshift], (uint32_t)len[g]);
         }
+        prefetch(tile + gridDim.x);
         __syncthreads();
         const int sub = (int)(tile & (nsub - 1));
         for (int p = threadIdx.x; p < nparts; p += kScThreads)
@@ -177,10 +191,24 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
             const bool neg = bk[g] & 1u;
             if (staged) {
                 const uint32_t slot = s_off[p] + off[g];
-                for (int k = 0; k < len[g]; ++k) {
-                    const float x = (float)__ldg(vals + rb[g] + k);
-                    s_key[slot + k] = kb | (uint32_t)__ldg(cols + rb[g] + k);
-                    s_val[slot + k] = neg ? -x : x;
+                // four nonzeros' loads in flight per lane before their stores (c3 rows hold
+                // 2.56 on average, so most rows take one step)
+                for (int k0 = 0; k0 < len[g]; k0 += 4) {
+                    float x[4];
+                    uint32_t c[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const bool ok = k0 + u < len[g];
+                        x[u] = ok ? (float)__ldg(vals + rb[g] + k0 + u) : 0.0f;
+                        c[u] = ok ? (uint32_t)__ldg(cols + rb[g] + k0 + u) : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (k0 + u < len[g]) {
+                            s_key[slot + k0 + u] = kb | c[u];
+                            s_val[slot + k0 + u] = neg ? -x[u] : x[u];
+                        }
+                    }
                 }
             } else {
                 const unsigned long long dst = s_gbase[p] + off[g];
@@ -397,9 +425,9 @@ void run_atomic(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const 
                uint32_t*, float*);
     int groups;
     switch (ctx->opt_csr_sc) {
-        case 1: sk = scatter_kernel<float, TI, 4, 3>; groups = 4; break;
-        case 3: sk = scatter_kernel<float, TI, 1, 8>; groups = 1; break;
-        default: sk = scatter_kernel<float, TI, 2, 6>; groups = 2; break;  // c3: 1.42 ms (1: 1.63, 3: 2.11)
+        case 1: sk = scatter_kernel<float, TI, 2, 6>; groups = 2; break;
+        case 2: sk = scatter_kernel<float, TI, 4, 3>; groups = 4; break;
+        default: sk = scatter_kernel<float, TI, 4, 4>; groups = 4; break;  // c3: 1.20 ms (1: 1.49, 2: 1.27)
     }
     const int tile_rows = kScThreads * groups;
     int tile_shift = 0;
