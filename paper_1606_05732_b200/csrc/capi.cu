@@ -1245,6 +1245,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_csr_slice_mb = value;
         else if (k == "csr_sc" && value >= 0 && value <= 2)
             ctx->opt_csr_sc = value;
+        else if (k == "csr_zero" && (value == 0 || value == 1))
+            ctx->opt_csr_zero = value;
         else if (k == "g_resident" && (value == 0 || value == 1))
             ctx->opt_g_resident = value;
         else if (k == "gemm_tile" && (value == 0 || value == 1))

@@ -112,7 +112,7 @@ __global__ void bucket_count(KeySrc src, int64_t n, uint32_t* counts) {
          idx += (int64_t)gridDim.x * blockDim.x) {
         uint32_t key, val;
         load_item<MODE>(src, idx, key, val);
-        atomicAdd(&counts[key], 1u);
+        red_add(&counts[key], 1u);
     }
 }
 

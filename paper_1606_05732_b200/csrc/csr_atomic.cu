@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) count_kernel(const int64_t* __restrict__ 
     for (int p = threadIdx.x; p < nbins; p += blockDim.x) {
         unsigned long long t = 0;
         for (int w = 0; w < 8; ++w) t += hist[w * nbins + p];
-        if (t) atomicAdd(&counts[p], t);
+        if (t) red_add(&counts[p], t);
     }
 }
 
@@ -251,13 +251,14 @@ __global__ void __launch_bounds__(kAccThreads) accumulate_kernel(const uint32_t*
                                                                   int nparts, int pshift, int64_t B, int cbits, int64_t d,
                                                                   double* __restrict__ sx,
                                                                   unsigned int* __restrict__ next_item,
-                                                                  unsigned int* __restrict__ zdone) {
+                                                                  unsigned int* __restrict__ zdone, int zero_inline) {
     __shared__ unsigned long long s_pstart[kMaxParts + 1];  // record start of each partition
     __shared__ unsigned int s_gstart[2 * kMaxParts + 1];    // first item of each queue group
     __shared__ unsigned int s_item;
     const int ngroups = 2 * nparts;
     const int64_t W = (int64_t)1 << pshift;
     auto zitems = [&](int p) -> unsigned {
+        if (!zero_inline) return 0u;  // S.X zero-filled before the launch
         const int64_t e = (min(B, (p + 1) * W) - p * W) * d;
         return (unsigned)((e + kZeroItem - 1) / kZeroItem);
     };
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(kAccThreads) accumulate_kernel(const uint32_t*
 #pragma unroll
             for (int u = 0; u < kPer; ++u)
                 if (kk[u] != 0xffffffffu)
-                    atomicAdd(sx + (int64_t)(kk[u] >> cbits) * d + (kk[u] & cmask), (double)vv[u]);
+                    red_add(sx + (int64_t)(kk[u] >> cbits) * d + (kk[u] & cmask), (double)vv[u]);
         }
         if (threadIdx.x == 0) s_item = nxt;
         __syncthreads();
@@ -449,8 +450,10 @@ void run_atomic(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const 
     // against 1.45 ms for this queue: its warps drift across partitions and the L2 thrashes)
     int acc_per_sm = 0;
     CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&acc_per_sm, accumulate_kernel, kAccThreads, 0));
+    const int zero_inline = ctx->opt_csr_zero == 1;
+    if (!zero_inline) CGX_CUDA(cudaMemsetAsync(sx, 0, sizeof(double) * (size_t)(xf->B * d), s));
     accumulate_kernel<<<ctx->num_sms * std::max(acc_per_sm, 1), kAccThreads, 0, s>>>(
-        rkey, rval, pcount, nparts, pshift, xf->B, cbits, d, sx, next_item, zdone);
+        rkey, rval, pcount, nparts, pshift, xf->B, cbits, d, sx, next_item, zdone, zero_inline);
     count_launch(ctx, 4);
     check_launch("sketch_csr_atomic");
 }

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) gproject_csr_kernel(uint64_t g_seed, int6
     __syncthreads();
     for (int64_t e = threadIdx.x; e < 32 * ncol; e += blockDim.x) {
         const int64_t j = e >> 5, rr = 32 * rb + (e & 31);
-        if (rr < m && zb[e] != 0.0) atomicAdd(&z[(c0 + j) * m + rr], zb[e]);
+        if (rr < m && zb[e] != 0.0) red_add(&z[(c0 + j) * m + rr], zb[e]);
     }
 }
 
