@@ -163,8 +163,6 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
         prefetch(tile + gridDim.x);
         __syncthreads();
         const int sub = (int)(tile & (nsub - 1));
-        for (int p = threadIdx.x; p < nparts; p += kScThreads)
-            if (s_cnt[p]) s_gbase[p] = atomicAdd(&cursor[p * nsub + sub], (unsigned long long)s_cnt[p]);
         if (wid == 0) {  // staging offsets: exclusive scan of the partition counts
             uint32_t run = 0;
             for (int p0 = 0; p0 < nparts; p0 += 32) {
@@ -183,6 +181,14 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
         }
         __syncthreads();
         const bool staged = s_total <= (uint32_t)kStage;
+        // the tile's global reservations (needed only by the write-out) are claimed by the
+        // last warps while the others already copy their rows: the atomics' round trip to the
+        // cursors overlaps the nonzeros' DRAM loads instead of preceding them (for an unstaged
+        // tile the places are needed now, so every thread waits for them)
+        for (int p = (int)threadIdx.x - (kScThreads - nparts % kScThreads) % kScThreads; p < nparts;
+             p += kScThreads)
+            if (p >= 0 && s_cnt[p]) s_gbase[p] = atomicAdd(&cursor[p * nsub + sub], (unsigned long long)s_cnt[p]);
+        if (!staged) __syncthreads();
 #pragma unroll
         for (int g = 0; g < kGroups; ++g) {
             const uint32_t b = bk[g] >> 1;
