@@ -464,10 +464,16 @@ def _dense_args(x):
     if x.dtype not in (np.float32, np.float64):
         x = x.astype(np.float64)
     n, d = x.shape
+    es = x.itemsize
+    s0, s1 = x.strides
     if x.flags.c_contiguous:
         layout, ld = CGX_ROW_MAJOR, max(d, 1)
     elif x.flags.f_contiguous:
         layout, ld = CGX_COL_MAJOR, max(n, 1)
+    elif s0 == es and s1 > 0 and s1 % es == 0 and s1 // es >= n:
+        layout, ld = CGX_COL_MAJOR, s1 // es  # a row block of a column-major matrix: no copy
+    elif s1 == es and s0 > 0 and s0 % es == 0 and s0 // es >= d:
+        layout, ld = CGX_ROW_MAJOR, s0 // es  # a column block of a row-major matrix
     else:
         x = np.ascontiguousarray(x)
         layout, ld = CGX_ROW_MAJOR, max(d, 1)
