@@ -198,7 +198,7 @@ template <typename TV, typename TI>
 __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64_t* __restrict__ rowptr, const TI* __restrict__ cols,
                                                        const TV* __restrict__ vals, const uint32_t* __restrict__ perm,
                                                        const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
-                                                       double* __restrict__ sx, int cbits, int G, int64_t B1,
+                                                       double* __restrict__ sx, int G, int64_t B1,
                                                        unsigned long long* __restrict__ next_task,
                                                        unsigned long long task_base,
                                                        unsigned long long* __restrict__ colmax) {
@@ -293,17 +293,27 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
                     if (neg[u]) x = -x;
                     if (ok) tag[col] = (uint8_t)lane;
                     __syncwarp();
-                    const bool mine = !ok || tag[col] == (uint8_t)lane;
-                    if (__all_sync(0xffffffffu, mine)) {
+                    // rep: the lane whose stamp survived in this column's tag (one per column)
+                    const unsigned rep = ok ? tag[col] : lane;
+                    if (__all_sync(0xffffffffu, rep == lane)) {
                         if (ok) acc[col] += x;
                     } else {  // a column twice in the wave: lane (= row) order per column
-                        const unsigned peers = cbits <= 12 ? match_any_bits(ok ? col : 1u << (cbits - 1), cbits)
-                                                           : __match_any_sync(0xffffffffu, ok ? col : 0xffffffffu);
-                        const unsigned rank = __popc(peers & lt);
-                        for (unsigned rr = 0; __any_sync(0xffffffffu, ok && rank >= rr); ++rr) {
-                            if (ok && rank == rr) acc[col] += x;
-                            __syncwarp();
+                        // Lanes sharing a column share its rep, a 5-bit lane id, so the groups
+                        // come from 5 ballots whatever d is; each group then sums as a chain
+                        // in lane order through shuffles, ((acc + x0) + x1) + ..., and its last
+                        // lane stores -- the serial order, one shared-memory round trip.
+                        const unsigned peers = match_any_bits(rep, 5);
+                        const unsigned before = peers & lt;
+                        const unsigned rank = __popc(before);
+                        const int pred = 31 - __clz(before);  // previous lane of the group
+                        const unsigned maxr = __reduce_max_sync(0xffffffffu, rank);
+                        double s = x;
+                        if (ok && rank == 0) s = acc[col] + x;
+                        for (unsigned rr = 1; rr <= maxr; ++rr) {
+                            const double t = __shfl_sync(0xffffffffu, s, pred & 31);
+                            if (rank == rr) s = t + x;
                         }
+                        if (ok && (peers & ~le) == 0) acc[col] = s;
                     }
                     __syncwarp();
                 }
@@ -386,8 +396,6 @@ bool launch_lean(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const
     int64_t nb = (nb_total + wl - 1) / wl;
     const int64_t cap = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);  // persistent: one wave
     if (nb > cap) nb = cap;
-    int cb = 1;
-    while (((int64_t)1 << (cb - 1)) < d) ++cb;
     // tasks of ~rows_per_task rows (whole buckets), single buckets for the last tail_tasks
     // per warp
     const int64_t rows_per_bucket = xf->n / nb_total + 1;
@@ -396,7 +404,7 @@ bool launch_lean(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const
     int64_t B1 = nb_total - ctx->opt_tail_tasks * nb * wl;
     B1 = B1 < 0 ? 0 : B1 / G * G;
     const unsigned long long base = take_tasks(ctx, B1 / G + nb_total - B1, nb * wl);
-    lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, offs, nb_total, d, sx, cb, (int)G, B1,
+    lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, offs, nb_total, d, sx, (int)G, B1,
                                          ctx->task_ctr, base, colmax);
     count_launch(ctx);
     tasks_launched(ctx, s);
