@@ -54,6 +54,12 @@ __device__ __forceinline__ T ld_na(const T* p) {
     }
 }
 
+// v with its sign bit flipped when neg is 1 (exact: -v), before the widening to fp64
+__device__ __forceinline__ float flip_sign(float v, unsigned neg) { return __int_as_float(__float_as_int(v) ^ (int)(neg << 31)); }
+__device__ __forceinline__ double flip_sign(double v, unsigned neg) {
+    return __longlong_as_double(__double_as_longlong(v) ^ ((long long)neg << 63));
+}
+
 template <typename TV, typename TI, bool CHUNKED>
 __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restrict__ rowptr,
                                                          const TI* __restrict__ cols, const TV* __restrict__ vals,
@@ -255,6 +261,9 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
             const int incl = warp_incl_scan(len, lane);
             const int total = __shfl_sync(0xffffffffu, incl, 31);
             const int excl = incl - len;
+            // item q of the group is nonzero (q - excl_k) of row k: position off_k + q
+            const int64_t off = rb - excl;
+            const unsigned negm = __ballot_sync(0xffffffffu, pe & kNegBit);
             const unsigned nz = __ballot_sync(0xffffffffu, len > 0);
             if (len > 0) tbl[__popc(nz & lt)] = (uint8_t)lane;
             __syncwarp();
@@ -262,25 +271,23 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
             for (int q0 = 0; q0 < total; q0 += 32 * kW) {
                 TI c[kW];
                 TV v[kW];
-                uint32_t neg[kW];
+                unsigned neg[kW];
 #pragma unroll
                 for (int u = 0; u < kW; ++u) {
                     const int w0 = q0 + u * 32;
-                    const bool starts_here = len > 0 && excl >= w0 && excl < w0 + 32;
+                    const bool starts_here = len > 0 && (unsigned)(excl - w0) < 32u;
                     const unsigned st = __reduce_or_sync(0xffffffffu, starts_here ? 1u << (excl - w0) : 0u);
                     const int r = kbase + __popc(st & le) - 1;
                     kbase += __popc(st);
                     const int j = tbl[r & 31];
-                    const int64_t rbj = __shfl_sync(0xffffffffu, rb, j);
-                    const int exj = __shfl_sync(0xffffffffu, excl, j);
-                    neg[u] = __shfl_sync(0xffffffffu, pe, j) & kNegBit;
+                    const int64_t offj = __shfl_sync(0xffffffffu, off, j);
+                    neg[u] = (negm >> j) & 1u;
                     const int q = w0 + (int)lane;
                     c[u] = 0;
                     v[u] = TV(0);
                     if (q < total) {
-                        const int64_t pos = rbj + (q - exj);
-                        c[u] = ld_na(cols + pos);
-                        v[u] = ld_na(vals + pos);
+                        c[u] = ld_na(cols + (offj + q));
+                        v[u] = ld_na(vals + (offj + q));
                     }
                 }
 #pragma unroll
@@ -289,8 +296,7 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
                     if (w0 >= total) break;
                     const bool ok = w0 + (int)lane < total;
                     const uint32_t col = ok ? (uint32_t)c[u] : 0u;
-                    double x = (double)v[u];
-                    if (neg[u]) x = -x;
+                    const double x = (double)flip_sign(v[u], neg[u]);
                     if (ok) tag[col] = (uint8_t)lane;
                     __syncwarp();
                     // rep: the lane whose stamp survived in this column's tag (one per column)
