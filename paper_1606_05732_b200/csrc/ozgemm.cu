@@ -160,20 +160,32 @@ __device__ __forceinline__ int oz_exp(unsigned long long amax_bits) {
     return e;
 }
 
-// Digits of 16 consecutive k of one w, packed 4 per 32-bit word per plane (byte kk % 4 of
+// Digits of NV consecutive k of one w, packed 4 per 32-bit word per plane (byte kk % 4 of
 // word kk / 4).  Balanced base-256 digits: Y = trunc(x * 2^(8S-2-E)) (|Y| < 2^(8S-2)), and
 // U = Y + O with O = 0x80 in each of the S low bytes; byte b of U minus 128 (= byte ^ 0x80)
-// is digit S-1-b of Y, d in [-128, 127], Y = sum_s d_s 256^(S-1-s).  So one F2I per value
-// and one byte permute per digit: no per-digit arithmetic.  sc = 2^(8S-2-E).
+// is digit S-1-b of Y, d in [-128, 127], Y = sum_s d_s 256^(S-1-s).  One byte permute per
+// digit: no per-digit arithmetic.  Y itself comes from the bits of x with integer shifts:
+// x = m * 2^(max(e,1) - 1075) (m the significand with its implicit bit, e the exponent
+// field), so Y = m shifted by max(e,1) - 1077 + 8S - E (<= 1, since |x| < 2^E), negated for
+// negative x -- the same integer as trunc(x * 2^(8S-2-E)) (that product is exact whenever
+// it is >= 1), without the fp64 multiply and the F2I.S64.F64 conversion, whose throughput
+// bounded the converter warps.
 template <int S, int NV>
-__device__ __forceinline__ void oz_digits(const double (&v)[NV], double sc, uint32_t (&dig)[S][NV / 4]) {
+__device__ __forceinline__ void oz_digits(const double (&v)[NV], int E, uint32_t (&dig)[S][NV / 4]) {
     constexpr unsigned long long O = 0x0080808080808080ull >> (8 * (7 - S));
+    const int tb = 1077 - 8 * S + E;
 #pragma unroll
     for (int q = 0; q < NV / 4; ++q) {
         uint32_t lo[4], hi[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const unsigned long long U = (unsigned long long)__double2ll_rz(v[4 * q + b] * sc) + O;
+            const long long bits = __double_as_longlong(v[4 * q + b]);
+            const int ef = (int)((unsigned long long)bits >> 52) & 0x7ff;
+            const unsigned long long m = ((unsigned long long)bits & 0xFFFFFFFFFFFFFull) | ((unsigned long long)(ef != 0) << 52);
+            const int t = (ef > 1 ? ef : 1) - tb;
+            unsigned long long y = t >= 0 ? m << (t < 63 ? t : 63) : m >> (-t < 63 ? -t : 63);
+            if (bits < 0) y = 0ull - y;
+            const unsigned long long U = y + O;
             lo[b] = (uint32_t)U;
             hi[b] = (uint32_t)(U >> 32);
         }
@@ -205,7 +217,7 @@ __global__ void oz_slice(const double* __restrict__ X, int64_t K, int64_t W, int
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) v[kk] = (w < W && k0 + kk < K) ? X[(k0 + kk) * W + w] : 0.0;
         uint32_t dig[S][4];
-        oz_digits<S, 16>(v, ldexp(1.0, 8 * S - 2 - E), dig);
+        oz_digits<S, 16>(v, E, dig);
         const int64_t wt = w / R, r = w % R, kb = k0 / OZ_KB, kc = (k0 % OZ_KB) / 16;
         int8_t* base = img + ((wt * nkb + kb) * S) * (int64_t)(R * OZ_KB) + (r / 8) * 256 + kc * 128 + (r % 8) * 16;
 #pragma unroll
@@ -223,6 +235,10 @@ constexpr int OZ_MAX_RING = 8;
 constexpr int OZ_SMEM_MAX = 225 << 10;  // of the 227 KB opt-in, leaving the static barriers room
 #ifndef OZ_CONVERTER_WARPS
 #define OZ_CONVERTER_WARPS 8
+#endif
+#ifndef OZ_EXP
+#define OZ_EXP 0  // measurement only: 1 = converters skip the digits, 2 = no G loads, 3 = no MMAs,
+                 // 4 = no S.X loads and no MMAs, 5 = no S.X loads
 #endif
 constexpr int OZ_CW = OZ_CONVERTER_WARPS;   // converter warps: 32 * OZ_CW threads = 64 columns x k-groups
 constexpr int OZ_VPT = OZ_KB * OZ_NT / (32 * OZ_CW);  // values of k per converter thread (8 or 4)
@@ -319,7 +335,6 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
         const bool colok = col < d;
         const int F = colok ? oz_exp(amax_b[col]) : 0;
         const double* src = sx + (colok ? col : 0);
-        const double sc = ldexp(1.0, 8 * S - 2 - F);
         // canonical K-major image: 8-row group j/8, 16 B core matrix, row j%8, byte within it
         const int kofs = kq * OZ_VPT;
         const uint32_t soff = (uint32_t)((j / 8) * 256 + (kofs / 16) * 128 + (j % 8) * 16 + (kofs % 16));
@@ -342,11 +357,11 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 if (i + 1 < nk) load(i + 1, nxt);
             }
             uint32_t dig[S][OZ_VPT / 4];
-            oz_digits<S, OZ_VPT>(cur, sc, dig);
+            if (OZ_EXP != 1) oz_digits<S, OZ_VPT>(cur, F, dig);
             if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);  // MMAs of k-block i - STAGES done
             uint8_t* bp = stage + A_BYTES + soff;
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
+            for (int s = 0; s < S * (OZ_EXP != 1); ++s) {
                 if constexpr (OZ_VPT == 8)
                     *reinterpret_cast<uint2*>(bp + s * OZ_NT * OZ_KB) = make_uint2(dig[s][0], dig[s][1]);
                 else
@@ -409,6 +424,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             RingPos sp(OZ_STAGES);
             for (int64_t i = 0; i < nk; ++i, sp.next()) {
                 if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);
+                if (OZ_EXP == 2) { mbar_arrive(&full[sp.idx]); continue; }
                 mbar_arrive_expect_tx(&full[sp.idx], A_BYTES);
                 if (csize > 1) {
                     const unsigned part = A_BYTES / csize;
@@ -434,6 +450,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             RingPos rp(RS);
             for (int64_t i = 0; i < nk; ++i, rp.next()) {
                 if (i >= RS) mbar_wait(&rempty[rp.idx], rp.phase ^ 1u);
+                if (OZ_EXP == 4 || OZ_EXP == 5) { mbar_arrive(&rfull[rp.idx]); continue; }
                 mbar_arrive_expect_tx(&rfull[rp.idx], OZ_RAW);
                 tma_load_2d(raw_ring + rp.idx * OZ_RAW, &sx_map, (int)(nt * OZ_NT), (int)((kb0 + i) * OZ_KB),
                             &rfull[rp.idx]);
@@ -459,7 +476,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 // N = 256 per instruction: S(S+1)/2 products in ~S + S/2 instructions (an
                 // N = 64 MMA costs ~3x its share of the tensor pipe, tools/microbench/umma_i8.cu).
 #pragma unroll
-                for (int s = 0; s < S; ++s)
+                for (int s = 0; s < S * (OZ_EXP != 3 && OZ_EXP != 4); ++s)
 #pragma unroll
                     for (int t0 = 0; t0 < S - s; t0 += 4) {
                         const int w = S - s - t0 < 4 ? S - s - t0 : 4;
@@ -607,16 +624,6 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
         run_absmax(ctx, sx, K, d, amax_b, s);
     }
     ctx->oz_colmax_for = nullptr;
-    // ring depths: the MMA ring as configured (default 3 stages at S >= 6, else 4), the raw
-    // S.X ring takes what is left (<= 8)
-    int nst = ctx->opt_oz_st > 0 ? (int)ctx->opt_oz_st : (S >= 6 ? 3 : 4);
-    const int64_t stage_bytes = oz_stage_bytes<S>();
-    if (nst > OZ_MAX_RING) nst = OZ_MAX_RING;
-    while (nst > 2 && nst * stage_bytes + 2 * OZ_RAW + 1024 > OZ_SMEM_MAX) --nst;
-    int nrs = (int)((OZ_SMEM_MAX - 1024 - nst * stage_bytes) / OZ_RAW);
-    if (ctx->opt_oz_rs > 0 && ctx->opt_oz_rs < nrs) nrs = (int)ctx->opt_oz_rs;
-    if (nrs > OZ_MAX_RING) nrs = OZ_MAX_RING;
-    const size_t smem = (size_t)(nst * stage_bytes + nrs * OZ_RAW + 1024);
     // S.X tiles staged by TMA when its rows are 16 B aligned (a tensor map of the K x d
     // row-major block; boxes of 32 rows x 64 columns, zero-filled past the edges)
     CUtensorMap sx_map;
@@ -637,6 +644,17 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
+    // ring depths: the MMA ring as configured (default 3 stages at S >= 6, else 4), the raw
+    // S.X ring takes what is left (<= 8)
+    int nst = ctx->opt_oz_st > 0 ? (int)ctx->opt_oz_st : (S >= 6 ? 3 : 4);
+    const int64_t stage_bytes = oz_stage_bytes<S>();
+    if (nst > OZ_MAX_RING) nst = OZ_MAX_RING;
+    const int64_t raw_min = staged ? 2 * OZ_RAW : 0;  // the direct path needs no raw ring
+    while (nst > 2 && nst * stage_bytes + raw_min + 1024 > OZ_SMEM_MAX) --nst;
+    int nrs = staged ? (int)((OZ_SMEM_MAX - 1024 - nst * stage_bytes) / OZ_RAW) : 0;
+    if (ctx->opt_oz_rs > 0 && ctx->opt_oz_rs < nrs) nrs = (int)ctx->opt_oz_rs;
+    if (nrs > OZ_MAX_RING) nrs = OZ_MAX_RING;
+    const size_t smem = (size_t)(nst * stage_bytes + nrs * OZ_RAW + 1024);
     CGX_CUDA(cudaFuncSetAttribute(oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // clusters along the N tiles share G's planes by multicast: the GEMM is bound by the
     // operand traffic out of L2, and every N tile otherwise re-reads the same G chunks
