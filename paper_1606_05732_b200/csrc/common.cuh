@@ -189,6 +189,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // ---- bulk copies (TMA engine, 1-D): global -> shared, completion counted on an mbarrier --
 // The arriving thread announces the transaction bytes, then issues copies that complete_tx
 // on the same barrier; waiters see the phase flip once every byte has landed.
+// mbar_wait for long waits (a warp idle for a whole accumulation): polls with a sleep in
+// between, so the spinning does not take issue slots from the warps doing the work
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity, unsigned ns) {
+    for (;;) {
+        unsigned ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+    }
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
                      smem_addr(bar)),

@@ -101,7 +101,7 @@ struct cgx_ctx {
     int64_t opt_oz_slices = 7;              // option "oz_slices": stage 2 on tcgen05 int8 with S digit planes (0 = DMMA)
     int64_t opt_oz_min_z = 16384;           // option "oz_min_z": smallest m*d that takes the tcgen05 stage 2
     int64_t opt_oz_cluster = 2;             // option "oz_cluster": CTAs sharing G's planes by multicast (1, 2, 4, 8)
-    int64_t opt_oz_st = 0, opt_oz_rs = 2;   // options "oz_st"/"oz_rs": ring depths of the tcgen05 stage 2 (0 = auto)
+    int64_t opt_oz_st = 0, opt_oz_rs = 4;   // options "oz_st"/"oz_rs": ring depths of the tcgen05 stage 2 (0 = auto)
     int64_t opt_oz_staged = 1;              // option "oz_staged": S.X rows reach the converters by bulk copy (0 = loads)
     cgx::DevBuf oz_max, oz_a, oz_b;         // (oz_b: column maxima of S.X)
     const double* oz_colmax_for = nullptr;  // S.X whose column maxima the sketch left in oz_b

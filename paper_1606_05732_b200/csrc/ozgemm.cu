@@ -240,9 +240,10 @@ constexpr int OZ_SMEM_MAX = 225 << 10;  // of the 227 KB opt-in, leaving the sta
 #define OZ_EXP 0  // measurement only: 1 = converters skip the digits, 2 = no G loads, 3 = no MMAs,
                  // 4 = no S.X loads and no MMAs, 5 = no S.X loads
 #endif
-constexpr int OZ_CW = OZ_CONVERTER_WARPS;   // converter warps: 32 * OZ_CW threads = 64 columns x k-groups
-constexpr int OZ_VPT = OZ_KB * OZ_NT / (32 * OZ_CW);  // values of k per converter thread (8 or 4)
-static_assert(OZ_VPT == 8 || OZ_VPT == 4, "converter warps: 8 or 16");
+constexpr int OZ_CW = OZ_CONVERTER_WARPS;   // converter warps: 32 * OZ_CW threads = 2 groups x 64 columns x k-groups
+constexpr int OZ_GT = 16 * OZ_CW;           // threads per converter group
+constexpr int OZ_VPT = OZ_KB * OZ_NT / OZ_GT;  // values of k per converter thread (16 or 8)
+static_assert(OZ_VPT == 16 || OZ_VPT == 8, "converter warps: 8 or 16");
 constexpr int OZ_THREADS = 32 * (OZ_CW + 7);
 
 // position in a ring of n slots: slot index and the parity of the current pass (no division
@@ -260,7 +261,7 @@ struct RingPos {
 };
 
 // One CTA: a 128 x 64 tile of Z over k-blocks [kb0, kb1) of its split.
-//   warps 0-7:  converters -- take the k-block's 32 x 64 fp64 S.X tile (TMA-staged, or loaded
+//   warps 0-7:  converters, two groups of 4 on alternate k-blocks -- take the 32 x 64 fp64 S.X tile (TMA-staged, or loaded
 //               directly), cut it into S digit planes in the UMMA image in shared memory;
 //   warps 8-11: epilogue  -- drain the TMEM accumulators (lanes 32(w-8).. = tile rows) every
 //               OZ_FK values of k, scale, and add into the split's partial tile in HBM;
@@ -277,7 +278,6 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     constexpr int A_BYTES = S * OZ_MT * OZ_KB;
     constexpr int STAGE = oz_stage_bytes<S>();  // A planes | B planes
     constexpr int FKB = OZ_FK / OZ_KB;           // k-blocks per accumulation
-    constexpr int NCT = 32 * OZ_CW;              // converter threads
     constexpr int W_EPI = OZ_CW, W_PROD = OZ_CW + 4, W_MMA = OZ_CW + 5, W_RAW = OZ_CW + 6;
     const int OZ_STAGES = nst, RS = nrs;         // ring depths (<= OZ_MAX_RING each)
     // the dynamic window is only guaranteed 16 B alignment under separate compilation: the
@@ -301,12 +301,12 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     if (threadIdx.x == 0) {
         for (int i = 0; i < OZ_STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&bfull[i], NCT);
+            mbar_init(&bfull[i], OZ_GT);  // one converter group per k-block
             mbar_init(&empty[i], csize);  // every CTA of the cluster has read the stage
         }
         for (int i = 0; i < RS; ++i) {
             mbar_init(&rfull[i], 1);
-            mbar_init(&rempty[i], NCT);
+            mbar_init(&rempty[i], OZ_GT);
         }
         mbar_init(&acc_full, 1);
         mbar_init(&acc_empty, 128);
@@ -329,8 +329,13 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     const uint16_t cmask = (uint16_t)((1u << csize) - 1u);
 
     if (warp < OZ_CW) {
-        // converter: thread = (column j of the tile, k-group kq of the k-block: OZ_VPT values of k)
-        const int j = threadIdx.x % OZ_NT, kq = threadIdx.x / OZ_NT;
+        // converters, in two groups that take alternate k-blocks: while one group waits for
+        // its raw tile or for the MMAs to free its stage, the other converts (one group of
+        // all converter warps on every k-block spent most of its time in those waits:
+        // stage 2 with the MMAs removed took nearly as long as with them).
+        // thread = (column j of the tile, k-group kq of the k-block: OZ_VPT values of k)
+        const int grp = (int)threadIdx.x / OZ_GT, gt = (int)threadIdx.x % OZ_GT;
+        const int j = gt % OZ_NT, kq = gt / OZ_NT;
         const int64_t col = nt * OZ_NT + j;
         const bool colok = col < d;
         const int F = colok ? oz_exp(amax_b[col]) : 0;
@@ -338,23 +343,23 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
         // canonical K-major image: 8-row group j/8, 16 B core matrix, row j%8, byte within it
         const int kofs = kq * OZ_VPT;
         const uint32_t soff = (uint32_t)((j / 8) * 256 + (kofs / 16) * 128 + (j % 8) * 16 + (kofs % 16));
-        double cur[OZ_VPT], nxt[OZ_VPT];
-        auto load = [&](int64_t i, double (&v)[OZ_VPT]) {  // direct path: straight from global
-            const int64_t k0 = (kb0 + i) * OZ_KB + kofs;
-#pragma unroll
-            for (int kk = 0; kk < OZ_VPT; ++kk) v[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
-        };
-        if (!staged && nk > 0) load(0, cur);
+        double cur[OZ_VPT];
         RingPos sp(OZ_STAGES), rp(RS);
-        for (int64_t i = 0; i < nk; ++i, sp.next(), rp.next()) {
+        if (grp) {
+            sp.next();
+            rp.next();
+        }
+        for (int64_t i = grp; i < nk; i += 2, sp.next(), sp.next(), rp.next(), rp.next()) {
             uint8_t* stage = smem + sp.idx * STAGE;
             if (staged) {  // TMA zero-fills past K and d
                 mbar_wait(&rfull[rp.idx], rp.phase);
                 const double* raw = reinterpret_cast<const double*>(raw_ring + rp.idx * OZ_RAW) + kofs * OZ_NT + j;
 #pragma unroll
                 for (int kk = 0; kk < OZ_VPT; ++kk) cur[kk] = raw[kk * OZ_NT];
-            } else {
-                if (i + 1 < nk) load(i + 1, nxt);
+            } else {  // direct path: straight from global
+                const int64_t k0 = (kb0 + i) * OZ_KB + kofs;
+#pragma unroll
+                for (int kk = 0; kk < OZ_VPT; ++kk) cur[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
             }
             uint32_t dig[S][OZ_VPT / 4];
             if (OZ_EXP != 1) oz_digits<S, OZ_VPT>(cur, F, dig);
@@ -362,10 +367,10 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             uint8_t* bp = stage + A_BYTES + soff;
 #pragma unroll
             for (int s = 0; s < S * (OZ_EXP != 1); ++s) {
-                if constexpr (OZ_VPT == 8)
-                    *reinterpret_cast<uint2*>(bp + s * OZ_NT * OZ_KB) = make_uint2(dig[s][0], dig[s][1]);
+                if constexpr (OZ_VPT == 16)
+                    *reinterpret_cast<uint4*>(bp + s * OZ_NT * OZ_KB) = make_uint4(dig[s][0], dig[s][1], dig[s][2], dig[s][3]);
                 else
-                    *reinterpret_cast<uint32_t*>(bp + s * OZ_NT * OZ_KB) = dig[s][0];
+                    *reinterpret_cast<uint2*>(bp + s * OZ_NT * OZ_KB) = make_uint2(dig[s][0], dig[s][1]);
             }
             // one proxy fence orders both this thread's generic accesses before the async
             // proxy: the plane writes before the MMA reads them, and the raw-tile reads before
@@ -374,10 +379,6 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&bfull[sp.idx]);
             if (staged) mbar_arrive(&rempty[rp.idx]);
-            if (!staged) {
-#pragma unroll
-                for (int kk = 0; kk < OZ_VPT; ++kk) cur[kk] = nxt[kk];
-            }
         }
     } else if (warp < W_PROD) {
         // epilogue: every accumulation's integer groups -> fp64 (smallest weight first), scaled
@@ -389,7 +390,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
         const int Er = rok ? oz_exp(amax_a[r]) : 0;
         double* zp = zpart + split * m * d;
         for (int64_t c = 0; c < nchunks; ++c) {
-            mbar_wait(&acc_full, (unsigned)(c & 1));
+            mbar_wait_sleep(&acc_full, (unsigned)(c & 1), 256);  // a whole accumulation: sleep between polls
             tc_fence_after();
 #pragma unroll 1
             for (int q = 0; q < OZ_NT / 16; ++q) {
@@ -654,6 +655,10 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     int nrs = staged ? (int)((OZ_SMEM_MAX - 1024 - nst * stage_bytes) / OZ_RAW) : 0;
     if (ctx->opt_oz_rs > 0 && ctx->opt_oz_rs < nrs) nrs = (int)ctx->opt_oz_rs;
     if (nrs > OZ_MAX_RING) nrs = OZ_MAX_RING;
+    // the two converter groups take alternate k-blocks: an even raw ring gives each group its
+    // own slots (with an odd one a group's consecutive waits on a slot would be two phases
+    // apart, which a parity wait cannot tell from one)
+    if (staged) nrs = nrs < 2 ? 2 : nrs & ~1;
     const size_t smem = (size_t)(nst * stage_bytes + nrs * OZ_RAW + 1024);
     CGX_CUDA(cudaFuncSetAttribute(oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // clusters along the N tiles share G's planes by multicast: the GEMM is bound by the

@@ -37,17 +37,20 @@ constexpr int kWaves = 4;  // item waves loaded before they are applied
 // never re-read by this SM) and asks L2 for a 64 B fetch.  Without the L2::64B hint every
 // L1 miss is promoted to a 128 B L2/DRAM fetch: a random 4 B load then costs 128 B of DRAM
 // traffic, with it 64 B (tools/microbench/sector_fetch.cu; 64 B is the smallest hint).
+#ifndef CGX_CSR_FETCH
+#define CGX_CSR_FETCH "64B"
+#endif
 template <typename T>
 __device__ __forceinline__ T ld_na(const T* p) {
     if constexpr (sizeof(T) == 8) {
         unsigned long long v;
-        asm volatile("ld.global.L1::no_allocate.L2::64B.b64 %0, [%1];" : "=l"(v) : "l"(p));
+        asm volatile("ld.global.L1::no_allocate.L2::" CGX_CSR_FETCH ".b64 %0, [%1];" : "=l"(v) : "l"(p));
         T out;
         memcpy(&out, &v, 8);
         return out;
     } else {
         unsigned v;
-        asm volatile("ld.global.L1::no_allocate.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+        asm volatile("ld.global.L1::no_allocate.L2::" CGX_CSR_FETCH ".b32 %0, [%1];" : "=r"(v) : "l"(p));
         T out;
         memcpy(&out, &v, 4);
         return out;
