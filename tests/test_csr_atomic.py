@@ -62,8 +62,23 @@ def test_record_path_matches_oracle(cg, restatement, mode3, idx, B, d):
     rng = np.random.default_rng(B + d)
     lens = np.minimum(rng.poisson(2.5, n), d)
     lens[::97] = 0  # empty rows
+    lens[5000:5100] = 0  # a run of empty rows
     rp, cols, vals = _csr(n, d, lens, 1, idx)
     _check(cg, restatement, 16, B, n, d, rp, cols, vals)
+
+
+def test_record_path_mixed_tiles(cg, restatement, mode3):
+    """Tiles of 1024 rows around the staging limit (4096 records): some staged, some stored
+    directly, and rows of a few hundred nonzeros."""
+    n, d, B = 16 * 1024, 300, 3001
+    rng = np.random.default_rng(8)
+    lens = rng.integers(0, 8, n)
+    lens[1024:2048] = 4  # exactly 4096 items: staged
+    lens[2048:3072] = 4
+    lens[2048] = 5  # 4097 items: direct
+    lens[4096:4100] = 290  # rows spanning many bitmap words
+    rp, cols, vals = _csr(n, d, lens, 3)
+    _check(cg, restatement, 8, B, n, d, rp, cols, vals)
 
 
 def test_record_path_long_rows_overflow_staging(cg, restatement, mode3):
@@ -97,3 +112,37 @@ def test_record_path_is_default_for_short_rows_and_gather_stays_exact(cg, restat
         assert np.array_equal(cg.countsketch_apply(t, x).cpu().numpy(), sx_ref)
     finally:
         ctx.set_option("csr_mode", 0)
+
+
+def test_record_path_key_all_ones(cg, restatement, mode3):
+    """bucket bits + column bits = 32: the record of (bucket B-1, column d-1) has key
+    0xffffffff, which must be added like any other (it once doubled as the accumulate's
+    empty-slot sentinel).  S.X is 2^22 x 1024 (32 GB) and stays on the device."""
+    import torch
+
+    from paper_1606_05732_b200 import SparseMatrix
+
+    n, d, B, seed = 200000, 1024, 1 << 22, 5
+    _, cs, _ = restatement.countgauss_seeds(seed)
+    h, s = restatement.hash_sign(cs, B, n)
+    hot = np.flatnonzero(h == B - 1)
+    if len(hot) == 0:
+        pytest.skip("no row hashes to the last bucket for this seed")
+    lens = np.random.default_rng(1).integers(0, 3, n)
+    lens[hot] = 2
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    rng = np.random.default_rng(2)
+    cols = np.concatenate([np.sort(rng.choice(d - 1, k, replace=False)) for k in lens]).astype(np.int32)
+    cols[rp[hot] + 1] = d - 1  # every hot row's second nonzero in the last column
+    vals = rng.standard_normal(int(rp[-1])).astype(np.float32)
+    dev = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    x = SparseMatrix(n, d, dev(rp), dev(cols), dev(vals))
+    t = cg.countgauss_new(4, B, n, cg.SeededRng(seed))
+    sx = cg.countsketch_apply(t, x)
+    want = 0.0
+    for i in hot:  # ascending rows; one or two terms, so any order gives the same sum
+        want += s[i] * float(vals[rp[i] + 1])
+    assert float(sx[B - 1, d - 1]) == want
+    del sx
+    torch.cuda.empty_cache()
