@@ -56,6 +56,11 @@ const char* cgx_version(void);
 int cgx_init(int device, cgx_ctx** out);
 int cgx_free(cgx_ctx* ctx);
 int cgx_synchronize(cgx_ctx* ctx, void* stream);
+/* Release the device memory the context keeps between calls -- per-call scratch buffers and
+ * the free lists of the transform-array pool (live transforms keep theirs) -- after
+ * waiting for the context's work.  No reference counterpart (the CPU library has no
+ * device memory); for long-lived callers that alternate large and small problems. */
+int cgx_trim(cgx_ctx* ctx);
 /* Device allocations owned by the context's GPU (for callers without an allocator). */
 int cgx_device_alloc(cgx_ctx* ctx, size_t bytes, void** out);
 int cgx_device_free(cgx_ctx* ctx, void* p);

@@ -27,6 +27,7 @@ SIGNATURES = {
     "cgx_init": (_I, [_I, _P]),
     "cgx_free": (_I, [_P]),
     "cgx_synchronize": (_I, [_P, _P]),
+    "cgx_trim": (_I, [_P]),
     "cgx_device_alloc": (_I, [_P, _SZ, _P]),
     "cgx_device_free": (_I, [_P, _P]),
     "cgx_host_alloc": (_I, [_P, _SZ, _P]),

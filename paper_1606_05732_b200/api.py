@@ -113,6 +113,10 @@ class Context:
     def synchronize(self, stream=None):
         check(lib.cgx_synchronize(self.h, stream))
 
+    def trim(self):
+        """Release the scratch and pooled device memory kept between calls (cgx_trim)."""
+        check(lib.cgx_trim(self.h))
+
     # profiling of stage 1 (sketch) / stage 2 (gemm) with CUDA events on the launch stream
     def profile(self, on: bool = True):
         check(lib.cgx_profile_enable(self.h, int(on)))

@@ -45,9 +45,19 @@ void* DevBuf::get(size_t need) {
     return p;
 }
 
-void* pool_alloc(cgx_ctx* ctx, size_t bytes) {
+// Size classes: powers of two up to 1 MiB, then eighths of the enclosing power of two
+// (at most 12.5% over the request: a 2.15 GB G or a 268 MB perm no longer rounds up to 4 GB
+// or 512 MB).
+size_t pool_class_of(size_t bytes) {
     size_t cls = 256;
     while (cls < bytes) cls <<= 1;
+    if (cls <= ((size_t)1 << 20)) return cls;
+    const size_t q = cls >> 3;
+    return (bytes + q - 1) / q * q;
+}
+
+void* pool_alloc(cgx_ctx* ctx, size_t bytes) {
+    const size_t cls = pool_class_of(bytes);
     auto& fl = ctx->pool_free[cls];
     if (!fl.empty()) {
         void* p = fl.back();
@@ -458,6 +468,30 @@ int cgx_free(cgx_ctx* ctx) {
         cudaStreamDestroy(ctx->stream);
         cudaFree(ctx->task_ctr);
         delete ctx;
+    });
+}
+
+int cgx_trim(cgx_ctx* ctx) {
+    return guard([&] {
+        need_ctx(ctx);
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        CGX_CUDA(cudaDeviceSynchronize());
+        for (DevBuf* b : {&ctx->sx, &ctx->zpart, &ctx->xstage, &ctx->tmp, &ctx->sort_k[0], &ctx->sort_k[1],
+                          &ctx->sort_v[0], &ctx->sort_v[1], &ctx->sort_hist, &ctx->counts, &ctx->hstage_dev,
+                          &ctx->gfull, &ctx->gchunk, &ctx->oz_max, &ctx->oz_a})
+            b->release();
+        for (DevBuf& b : ctx->hin) b.release();
+        for (DevBuf& b : ctx->part) b.release();
+        for (auto& kv : ctx->pool_free) {
+            for (void* p : kv.second) {
+                cudaFree(p);
+                ctx->pool_class.erase(p);
+            }
+            kv.second.clear();
+        }
+        ctx->pool_free.clear();
+        ctx->oz_colmax_for = nullptr;
     });
 }
 

@@ -18,6 +18,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <immintrin.h>
 #include <thread>
 #include <vector>
 
@@ -138,6 +139,34 @@ CGX_HOST_SIMD bool narrow_i64(const int64_t* src, int32_t* dst, size_t len) {
     return true;
 }
 
+// memcpy into the pinned ring with non-temporal stores: the ring is written once and read
+// only by the copy engine, so the stores skip the read-for-ownership of every destination
+// line that a plain memcpy of these 2 MiB per-thread pieces pays (glibc switches to
+// streaming stores only for much larger copies).
+__attribute__((target("avx512f"))) static void copy_nt_avx512(char* dst, const char* src, size_t n) {
+    while (n && ((uintptr_t)dst & 63)) {
+        *dst++ = *src++;
+        --n;
+    }
+    for (; n >= 256; n -= 256, dst += 256, src += 256) {
+        const __m512i a = _mm512_loadu_si512(src), b = _mm512_loadu_si512(src + 64);
+        const __m512i c = _mm512_loadu_si512(src + 128), d = _mm512_loadu_si512(src + 192);
+        _mm512_stream_si512((__m512i*)dst, a);
+        _mm512_stream_si512((__m512i*)(dst + 64), b);
+        _mm512_stream_si512((__m512i*)(dst + 128), c);
+        _mm512_stream_si512((__m512i*)(dst + 192), d);
+    }
+    _mm_sfence();
+    std::memcpy(dst, src, n);
+}
+static void copy_nt(char* dst, const char* src, size_t n) {
+    static const bool avx512 = __builtin_cpu_supports("avx512f");
+    if (avx512 && n >= 4096)
+        copy_nt_avx512(dst, src, n);
+    else
+        std::memcpy(dst, src, n);
+}
+
 // Elements [e, e_end) of a source made of segments of `seg` elements spaced `sld`
 // elements apart (a column-major row block: seg = rows, sld = ld), as contiguous pieces:
 // fn(source element offset, destination element offset relative to e, length).
@@ -242,7 +271,7 @@ const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, 
             pool.run([&](int k) {
                 const size_t a = e0 + ne * k / T, b = e0 + ne * (k + 1) / T;
                 for_pieces(a, b, seg, sld, [&](size_t so, size_t dofs, size_t len) {
-                    std::memcpy(buf + (a - e0 + dofs) * esize, sp + so * esize, len * esize);
+                    copy_nt(buf + (a - e0 + dofs) * esize, sp + so * esize, len * esize);
                     return true;
                 });
             });

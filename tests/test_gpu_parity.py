@@ -1007,3 +1007,26 @@ def test_stage2_tensor_core_nan_inf_and_tiny_columns(cg, restatement):
     for j in range(d):
         if fin[:, j].all():
             assert np.linalg.norm(z[:, j] - z_ref[:, j]) <= 1e-12 * np.linalg.norm(z_ref[:, j]), j
+
+
+def test_trim_between_calls(cg, restatement):
+    """cgx_trim frees the context's scratch and pooled blocks between calls; live transforms
+    keep their arrays and every later call (dense, CSR record path, tensor-core stage 2)
+    gives the same bits as before the trim."""
+    from paper_1606_05732_b200 import SparseMatrix, bench_data
+
+    ctx = cg.context()
+    n, d, B, m = 1 << 20, 128, 8192, 128
+    x = bench_data.dense_normal(n, d, seed=3)
+    t = cg.countgauss_new(m, B, n, cg.SeededRng(4))
+    z0 = cg.countgauss_apply(t, x).cpu().numpy()
+    xs = bench_data.csr_bernoulli(n, 256, 0.02, seed=5)
+    t2 = cg.countgauss_new(m, 65536, n, cg.SeededRng(6))
+    s0 = cg.countsketch_apply(t2, xs).cpu().numpy()
+    ctx.trim()
+    t3 = cg.countgauss_new(16, 1000, 5000, cg.SeededRng(7))  # a pool allocation after the trim
+    assert np.array_equal(cg.countgauss_apply(t, x).cpu().numpy(), z0)
+    ctx.trim()
+    s1 = cg.countsketch_apply(t2, xs).cpu().numpy()
+    assert np.allclose(s1, s0, rtol=1e-14, atol=1e-14)  # record path: fp64 rounding order only
+    del t3
