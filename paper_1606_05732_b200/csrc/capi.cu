@@ -1277,6 +1277,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_csr_mode = value;
         else if (k == "csr_slice_mb" && value >= 1 && value <= 1024)
             ctx->opt_csr_slice_mb = value;
+        else if (k == "gather_sms" && value >= 0)
+            ctx->opt_gather_sms = value;
         else if (k == "csr_sc" && value >= 0 && value <= 2)
             ctx->opt_csr_sc = value;
         else if (k == "csr_zero" && (value == 0 || value == 1))

@@ -91,6 +91,7 @@ struct cgx_ctx {
     int64_t opt_async = 2;                  // option "async_stages": cp.async row-gather ring depth (0 = register loads)
     int64_t opt_csr_mode = 0;               // option "csr_mode": 0 auto, 1 row gather, 3 records + L2 atomics
     int64_t opt_csr_slice_mb = 8;           // option "csr_slice_mb": S.X slice per partition of the record path
+    int64_t opt_gather_sms = 0;             // option "gather_sms": SMs the CSR gather's persistent grid spans (0 = all)
     int64_t opt_csr_zero = 1;               // option "csr_zero": 1 S.X slices zeroed in the accumulate queue, 0 memset first
     int64_t opt_csr_sc = 0;                 // option "csr_sc": record-scatter variant (rows per lane, CTAs per SM)
     int64_t opt_gemm_tile = 0;              // option "gemm_tile": 1 = 8-warp 64x128/128x64 large-Z tiles

@@ -30,7 +30,7 @@ constexpr int kWaves = 4;  // item waves loaded before they are applied
 #define CGX_CSR_MINB 4  // 4 CTAs/SM: c5 sketch 17.9 -> 15.3 ms (tools/sweep_csr.sh)
 #endif
 #ifndef CGX_CSR_KW
-#define CGX_CSR_KW 4
+#define CGX_CSR_KW 6  // item waves in flight per warp: c5 12.95 -> 12.82 ms against 4 (8: 14.0, spills)
 #endif
 
 // Random short reads: a global load that does not allocate in L1 (the gathered rows are
@@ -403,7 +403,8 @@ bool launch_lean(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const
     int per_sm = 0;
     CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, wl * 32, sm));
     int64_t nb = (nb_total + wl - 1) / wl;
-    const int64_t cap = (int64_t)ctx->num_sms * (per_sm < 1 ? 1 : per_sm);  // persistent: one wave
+    const int64_t sms = ctx->opt_gather_sms > 0 && ctx->opt_gather_sms < ctx->num_sms ? ctx->opt_gather_sms : ctx->num_sms;
+    const int64_t cap = sms * (per_sm < 1 ? 1 : per_sm);  // persistent: one wave
     if (nb > cap) nb = cap;
     // tasks of ~rows_per_task rows (whole buckets), single buckets for the last tail_tasks
     // per warp
