@@ -122,7 +122,7 @@ def test_record_path_key_all_ones(cg, restatement, mode3):
 
     from paper_1606_05732_b200 import SparseMatrix
 
-    n, d, B, seed = 200000, 1024, 1 << 22, 5
+    n, d, B, seed = 200000, 1024, 1 << 22, 29  # seed 29: row 152986 hashes to bucket B-1
     _, cs, _ = restatement.countgauss_seeds(seed)
     h, s = restatement.hash_sign(cs, B, n)
     hot = np.flatnonzero(h == B - 1)
