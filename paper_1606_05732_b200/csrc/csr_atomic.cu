@@ -122,9 +122,9 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
     unsigned long long* s_gbase = (unsigned long long*)(s_val + kStage);  // nparts
     uint32_t* s_cnt = (uint32_t*)(s_gbase + nparts);                       // nparts
     uint32_t* s_off = s_cnt + nparts;                                      // nparts (exclusive scan)
+    uint16_t* s_part = (uint16_t*)(s_off + nparts);                        // kStage: partition of each staged record
     __shared__ uint32_t s_total;
     const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    constexpr int kWarps = kScThreads / 32;
     constexpr int kTile = kScThreads * kGroups;  // rows per tile
     const int64_t ntiles = (n + kTile - 1) / kTile;
     // the next tile's row offsets and row records are loaded while this tile is staged and
@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
                         if (k0 + u < len[g]) {
                             s_key[slot + k0 + u] = kb | c[u];
                             s_val[slot + k0 + u] = neg ? -x[u] : x[u];
+                            s_part[slot + k0 + u] = (uint16_t)p;
                         }
                     }
                 }
@@ -227,13 +228,16 @@ __global__ void __launch_bounds__(kScThreads, kMinB) scatter_kernel(const int64_
         }
         __syncthreads();
         if (staged) {
-            for (int p = wid; p < nparts; p += kWarps) {
-                const uint32_t c = s_cnt[p], o = s_off[p];
-                const unsigned long long gb = s_gbase[p];
-                for (uint32_t i = lane; i < c; i += 32) {
-                    __stcs(rkey + gb + i, s_key[o + i]);
-                    __stcs(rval + gb + i, s_val[o + i]);
-                }
+            // flat over the staged records (all lanes busy; consecutive records of one
+            // partition go to consecutive places, so the stores coalesce within its run) --
+            // a warp per partition left most lanes idle in its ~40-record runs (31% of the
+            // kernel's instructions on c3)
+            const uint32_t total = s_total;
+            for (uint32_t i = threadIdx.x; i < total; i += kScThreads) {
+                const uint32_t p = s_part[i];
+                const unsigned long long dst = s_gbase[p] + (i - s_off[p]);
+                __stcs(rkey + dst, s_key[i]);
+                __stcs(rval + dst, s_val[i]);
             }
         }
         __syncthreads();
@@ -439,7 +443,7 @@ void run_atomic(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const 
         case 2: sk = scatter_kernel<float, TI, 4, 3>; groups = 4; break;
         default: sk = scatter_kernel<float, TI, 4, 4>; groups = 4; break;  // c3: 1.20 ms (1: 1.49, 2: 1.27)
     }
-    const size_t smem = (sizeof(uint32_t) + sizeof(float)) * kStage +
+    const size_t smem = (sizeof(uint32_t) + sizeof(float) + sizeof(uint16_t)) * kStage +
                         (sizeof(unsigned long long) + 2 * sizeof(uint32_t)) * (size_t)nparts;
     const int tile_rows = kScThreads * groups;
     int tile_shift = 0;
