@@ -1279,8 +1279,6 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_csr_slice_mb = value;
         else if (k == "gather_sms" && value >= 0)
             ctx->opt_gather_sms = value;
-        else if (k == "csr_sc" && value >= 0 && value <= 2)
-            ctx->opt_csr_sc = value;
         else if (k == "csr_zero" && (value == 0 || value == 1))
             ctx->opt_csr_zero = value;
         else if (k == "g_resident" && (value == 0 || value == 1))

@@ -434,15 +434,10 @@ void run_atomic(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const 
     const size_t csm = sizeof(uint32_t) * 8 * (size_t)nbins;
     CGX_CUDA(cudaFuncSetAttribute(count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
     uint32_t* rowinfo = (uint32_t*)ctx->part[4].get(sizeof(uint32_t) * (size_t)n);
-    // scatter variant (option csr_sc): rows per lane per tile and min CTAs per SM
-    void (*sk)(const int64_t*, const TI*, const float*, int64_t, const uint32_t*, int, int, int, int, unsigned long long*,
-               uint32_t*, float*);
-    int groups;
-    switch (ctx->opt_csr_sc) {
-        case 1: sk = scatter_kernel<float, TI, 2, 6>; groups = 2; break;
-        case 2: sk = scatter_kernel<float, TI, 4, 3>; groups = 4; break;
-        default: sk = scatter_kernel<float, TI, 4, 4>; groups = 4; break;  // c3: 1.20 ms (1: 1.49, 2: 1.27)
-    }
+    // scatter: 4 rows per lane per 1024-row tile, 4 CTAs per SM (c3: 1.15 ms; 2 rows x 6 CTAs
+    // measured 1.49 ms, 4 x 3 CTAs 1.27 ms)
+    auto sk = scatter_kernel<float, TI, 4, 4>;
+    const int groups = 4;
     const size_t smem = (sizeof(uint32_t) + sizeof(float) + sizeof(uint16_t)) * kStage +
                         (sizeof(unsigned long long) + 2 * sizeof(uint32_t)) * (size_t)nparts;
     const int tile_rows = kScThreads * groups;

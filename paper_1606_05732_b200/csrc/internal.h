@@ -93,7 +93,6 @@ struct cgx_ctx {
     int64_t opt_csr_slice_mb = 8;           // option "csr_slice_mb": S.X slice per partition of the record path
     int64_t opt_gather_sms = 0;             // option "gather_sms": SMs the CSR gather's persistent grid spans (0 = all)
     int64_t opt_csr_zero = 1;               // option "csr_zero": 1 S.X slices zeroed in the accumulate queue, 0 memset first
-    int64_t opt_csr_sc = 0;                 // option "csr_sc": record-scatter variant (rows per lane, CTAs per SM)
     int64_t opt_gemm_tile = 0;              // option "gemm_tile": 1 = 8-warp 64x128/128x64 large-Z tiles
     int64_t opt_gemm_chunks = 0;            // option "gemm_chunks": 1 = 48 MB K-chunks even when G is in memory
     int64_t opt_g_resident = 1;             // option "g_resident": materialize seeded G at construction (<= 4 GiB)
