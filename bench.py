@@ -531,6 +531,32 @@ def run_ours(args):
     except (OSError, ValueError, KeyError):
         traffic = None
 
+    # The hardware rate that bounds the kernel when it is not HBM bandwidth,
+    # each measured on this GPU by a committed microbenchmark: random 128 B rows for the dense
+    # gather (d*4 <= 128 B rows), random 64 B DRAM accesses for the CSR gather, and for the
+    # record path the sum of its three kernels' floors (count and scatter at the measured copy
+    # rate on their DRAM bytes, the accumulate at the L2 atomic-unit rate on its nnz REDs).
+    ceiling = None
+    if world == 1 and not fused:
+        if c["kind"] == "dense" and d * x.element_size() <= 128:
+            ceiling = {"what": "random 128 B-row gather rate (tools/microbench/gather_bw.cu)", "rate": 5950.0,
+                       "unit": "GB/s", "achieved": achieved, "frac": achieved / 5950.0}
+        elif c["kind"] == "csr" and "record" in kernel_name:
+            # count: row offsets + a 4 B row record; scatter: row offsets + row records +
+            # the nonzeros (8 B) read and their 8 B records written (ncu on c3: 0.78, 3.52 GB)
+            count_b = (rows + 1) * 8 + rows * 4
+            scatter_b = (rows + 1) * 8 + rows * 4 + nnz_local * 16
+            floor_ms = (count_b + scatter_b) / (peak * 1e9) * 1e3 + nnz_local / 187e9 * 1e3
+            ceiling = {"what": "count + scatter DRAM bytes at the measured copy rate, plus one L2 RED per "
+                               "nonzero at 187 G/s (tools/microbench/red_types.cu)",
+                       "floor_ms": floor_ms, "achieved_ms": sk_avg_ms, "frac": floor_ms / sk_avg_ms}
+        elif c["kind"] == "csr" and traffic:
+            acc = traffic / 64.0 / (sk_avg_ms / 1e3)
+            ceiling = {"what": "random 64 B DRAM accesses per second (ncu DRAM bytes / 64) against the best "
+                               "rate of independent random loads on this GPU (tools/microbench/random_access.cu "
+                               "sweep: 36.5-49.7e9/s)",
+                       "rate": 49.7e9, "unit": "accesses/s", "achieved": acc, "frac": acc / 49.7e9}
+
     # e2e: same call with X in pinned host memory (H2D + D2H inside the timed region)
     e2e = None
     if c["kind"] == "csr" and not args.no_e2e:
@@ -662,7 +688,7 @@ def run_ours(args):
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": kernel_name,
-                         "bytes_per_launch": bytes_alg, "peak_source": peak_kind},
+                         "bytes_per_launch": bytes_alg, "peak_source": peak_kind, "ceiling": ceiling},
             "stage2": stage2_line(args, m, B, d, gm_ms / max(gm_n, 1)),
             "e2e": e2e,
             "e2e_dropin": e2e_dropin,
