@@ -1299,6 +1299,8 @@ int cgx_set_option(cgx_ctx* ctx, const char* key, int64_t value) {
             ctx->opt_oz_min_z = value;
         else if (k == "oz_staged" && (value == 0 || value == 1))
             ctx->opt_oz_staged = value;
+        else if (k == "oz_mpair" && (value == 0 || value == 1))
+            ctx->opt_oz_mpair = value;
         else if (k == "gemm_chunks" && (value == 0 || value == 1))
             ctx->opt_gemm_chunks = value;
         else

@@ -103,6 +103,7 @@ struct cgx_ctx {
     int64_t opt_oz_cluster = 2;             // option "oz_cluster": CTAs sharing G's planes by multicast (1, 2, 4, 8)
     int64_t opt_oz_st = 0, opt_oz_rs = 4;   // options "oz_st"/"oz_rs": ring depths of the tcgen05 stage 2 (0 = auto)
     int64_t opt_oz_staged = 1;              // option "oz_staged": S.X rows reach the converters by bulk copy (0 = loads)
+    int64_t opt_oz_mpair = 1;               // option "oz_mpair": M-tile pairs share the S.X conversion over DSMEM
     cgx::DevBuf oz_max, oz_a, oz_b;         // (oz_b: column maxima of S.X)
     const double* oz_colmax_for = nullptr;  // S.X whose column maxima the sketch left in oz_b
     int64_t oz_colmax_d = 0;         // ozgemm.cu scratch: scales, digit images of G and S.X

@@ -44,9 +44,9 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 // K-major, no swizzle: core matrices of 8 rows x 16 B (128 B contiguous); the two core
 // matrices of one 32 B k-step sit LBO = 128 B apart, consecutive 8-row groups SBO = 256 B.
-__device__ __forceinline__ uint64_t umma_desc(unsigned saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
-           (1ull << 46);  // version 1 (sm_100), base offset 0, layout SWIZZLE_NONE
+__device__ __forceinline__ uint64_t umma_desc(unsigned saddr, unsigned lbo = 128, unsigned sbo = 256) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // version 1 (sm_100), base offset 0, SWIZZLE_NONE
 }
 // kind::i8 instruction descriptor: D s32, A/B signed 8-bit, both K-major, M x N
 constexpr uint32_t oz_idesc(int M, int N) {
@@ -97,6 +97,36 @@ __device__ __forceinline__ unsigned cluster_rank() {
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the address of this CTA's shared-memory word `a` in cluster CTA `rank`
+__device__ __forceinline__ unsigned cluster_map(unsigned a, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v2(unsigned addr, uint32_t x, uint32_t y) {
+    asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(x), "r"(y) : "memory");
+}
+// bulk copy of `bytes` from this CTA's shared memory into a peer's (cluster addresses from
+// cluster_map), completing on the peer's mbarrier
+__device__ __forceinline__ void bulk_s2peer(unsigned dst_cluster, const void* src, unsigned bytes, unsigned bar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst_cluster),
+                 "r"(smem_addr(src)), "r"(bytes), "r"(bar_cluster)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(unsigned cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// mbar_wait with cluster-scope acquire: the phase may complete by arrivals (and shared-memory
+// writes) of another CTA of the cluster
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
     asm volatile(
@@ -269,7 +299,15 @@ struct RingPos {
 //               cluster of N tiles when csize > 1);
 //   warp 13:    MMA       -- one thread issues the tcgen05.mma, S + S/2 per k-block;
 //   warp 14:    producer  -- the S.X tile, one TMA load per k-block.
-template <int S>
+// MP (M-tile pairs, c5's m = 256): the two CTAs of a cluster hold the two M tiles of the same
+// (N tile, split) and need the same S.X planes.  Each loads half of every S.X tile (16 of its
+// 32 k), converts it, and sends its half of the planes to the peer with one DSMEM bulk copy,
+// so every S.X value is converted once instead of once per M tile; G's planes are each CTA's
+// own (no N-tile multicast in this mode).  The B planes are laid out k-half-major (each
+// half of all S planes contiguous: LBO = S KB, SBO = 128 B) so that a half is one copy.  A
+// stage is free once both CTAs' MMAs read it (their commits multicast to both `empty`
+// barriers); `bfull` completes on one local arrive plus the peer's copy bytes.
+template <int S, int MP>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const double* __restrict__ sx, int64_t K,
         int64_t d, int64_t nkb, int64_t kb_per_split, const unsigned long long* __restrict__ amax_a,
@@ -277,6 +315,9 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
         int nrs, int csize, const __grid_constant__ CUtensorMap sx_map) {
     constexpr int A_BYTES = S * OZ_MT * OZ_KB;
     constexpr int STAGE = oz_stage_bytes<S>();  // A planes | B planes
+    constexpr int KH = MP ? OZ_KB / 2 : OZ_KB;   // k rows of the raw S.X tile this CTA loads and converts
+    constexpr int VPT = KH * OZ_NT / OZ_GT;      // values per converter thread per k-block
+    constexpr int RAWB = KH * OZ_NT * 8;         // bytes per raw S.X slot
     constexpr int FKB = OZ_FK / OZ_KB;           // k-blocks per accumulation
     constexpr int W_EPI = OZ_CW, W_PROD = OZ_CW + 4, W_MMA = OZ_CW + 5, W_RAW = OZ_CW + 6;
     const int OZ_STAGES = nst, RS = nrs;         // ring depths (<= OZ_MAX_RING each)
@@ -301,7 +342,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
     if (threadIdx.x == 0) {
         for (int i = 0; i < OZ_STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&bfull[i], OZ_GT);  // one converter group per k-block
+            mbar_init(&bfull[i], MP ? 1 : OZ_GT);  // MP: the group's elected arrive (+ the peer's copy bytes)
             mbar_init(&empty[i], csize);  // every CTA of the cluster has read the stage
         }
         for (int i = 0; i < RS; ++i) {
@@ -341,9 +382,14 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
         const int F = colok ? oz_exp(amax_b[col]) : 0;
         const double* src = sx + (colok ? col : 0);
         // canonical K-major image: 8-row group j/8, 16 B core matrix, row j%8, byte within it
-        const int kofs = kq * OZ_VPT;
-        const uint32_t soff = (uint32_t)((j / 8) * 256 + (kofs / 16) * 128 + (j % 8) * 16 + (kofs % 16));
-        double cur[OZ_VPT];
+        const int kloc = kq * VPT;                          // k within this CTA's part of the tile
+        const int kofs = (MP ? (int)crank * KH : 0) + kloc;  // k within the k-block
+        // plane s of this thread's values: non-MP -- [s][j/8: 256 B][k/16: 128 B][j%8: 16 B][k%16];
+        // MP -- [k/16: S KB][s: 1 KB][j/8: 128 B][j%8: 16 B][k%16] (a k-half is contiguous)
+        const uint32_t soff = MP ? (uint32_t)((kofs / 16) * S * 1024 + (j / 8) * 128 + (j % 8) * 16 + (kofs % 16))
+                                 : (uint32_t)((j / 8) * 256 + (kofs / 16) * 128 + (j % 8) * 16 + (kofs % 16));
+        constexpr int PSTRIDE = MP ? 1024 : OZ_NT * OZ_KB;  // bytes between planes
+        double cur[VPT];
         RingPos sp(OZ_STAGES), rp(RS);
         if (grp) {
             sp.next();
@@ -353,31 +399,42 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             uint8_t* stage = smem + sp.idx * STAGE;
             if (staged) {  // TMA zero-fills past K and d
                 mbar_wait(&rfull[rp.idx], rp.phase);
-                const double* raw = reinterpret_cast<const double*>(raw_ring + rp.idx * OZ_RAW) + kofs * OZ_NT + j;
+                const double* raw = reinterpret_cast<const double*>(raw_ring + rp.idx * RAWB) + kloc * OZ_NT + j;
 #pragma unroll
-                for (int kk = 0; kk < OZ_VPT; ++kk) cur[kk] = raw[kk * OZ_NT];
+                for (int kk = 0; kk < VPT; ++kk) cur[kk] = raw[kk * OZ_NT];
             } else {  // direct path: straight from global
                 const int64_t k0 = (kb0 + i) * OZ_KB + kofs;
 #pragma unroll
-                for (int kk = 0; kk < OZ_VPT; ++kk) cur[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
+                for (int kk = 0; kk < VPT; ++kk) cur[kk] = (colok && k0 + kk < K) ? __ldg(src + (k0 + kk) * d) : 0.0;
             }
-            uint32_t dig[S][OZ_VPT / 4];
-            if (OZ_EXP != 1) oz_digits<S, OZ_VPT>(cur, F, dig);
+            uint32_t dig[S][VPT / 4];
+            if (OZ_EXP != 1) oz_digits<S, VPT>(cur, F, dig);
             if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);  // MMAs of k-block i - STAGES done
             uint8_t* bp = stage + A_BYTES + soff;
 #pragma unroll
             for (int s = 0; s < S * (OZ_EXP != 1); ++s) {
-                if constexpr (OZ_VPT == 16)
-                    *reinterpret_cast<uint4*>(bp + s * OZ_NT * OZ_KB) = make_uint4(dig[s][0], dig[s][1], dig[s][2], dig[s][3]);
+                if constexpr (VPT == 16)
+                    *reinterpret_cast<uint4*>(bp + s * PSTRIDE) = make_uint4(dig[s][0], dig[s][1], dig[s][2], dig[s][3]);
                 else
-                    *reinterpret_cast<uint2*>(bp + s * OZ_NT * OZ_KB) = make_uint2(dig[s][0], dig[s][1]);
+                    *reinterpret_cast<uint2*>(bp + s * PSTRIDE) = make_uint2(dig[s][0], dig[s][1]);
             }
             // one proxy fence orders both this thread's generic accesses before the async
             // proxy: the plane writes before the MMA reads them, and the raw-tile reads before
             // the next TMA overwrite of that slot (releasing the slot before a fence raced at
             // S = 6; a second fence per k-block cost c5 0.7 ms)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&bfull[sp.idx]);
+            if constexpr (MP) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(OZ_GT) : "memory");  // the group's half is written
+                if (gt == 0) {
+                    const uint32_t half = (uint32_t)crank * S * 1024;
+                    mbar_arrive_expect_tx(&bfull[sp.idx], S * 1024);  // local arrive; the peer's half follows
+                    bulk_s2peer(cluster_map(smem_addr(stage + A_BYTES + half), crank ^ 1u), stage + A_BYTES + half,
+                                S * 1024, cluster_map(smem_addr(&bfull[sp.idx]), crank ^ 1u));
+                }
+            } else {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&bfull[sp.idx]);
+            }
             if (staged) mbar_arrive(&rempty[rp.idx]);
         }
     } else if (warp < W_PROD) {
@@ -427,7 +484,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);
                 if (OZ_EXP == 2) { mbar_arrive(&full[sp.idx]); continue; }
                 mbar_arrive_expect_tx(&full[sp.idx], A_BYTES);
-                if (csize > 1) {
+                if (csize > 1 && !MP) {
                     const unsigned part = A_BYTES / csize;
                     bulk_g2s_mc(smem + sp.idx * STAGE + crank * part, ga + i * A_BYTES + crank * part, part,
                                 &full[sp.idx], cmask);
@@ -452,9 +509,9 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             for (int64_t i = 0; i < nk; ++i, rp.next()) {
                 if (i >= RS) mbar_wait(&rempty[rp.idx], rp.phase ^ 1u);
                 if (OZ_EXP == 4 || OZ_EXP == 5) { mbar_arrive(&rfull[rp.idx]); continue; }
-                mbar_arrive_expect_tx(&rfull[rp.idx], OZ_RAW);
-                tma_load_2d(raw_ring + rp.idx * OZ_RAW, &sx_map, (int)(nt * OZ_NT), (int)((kb0 + i) * OZ_KB),
-                            &rfull[rp.idx]);
+                mbar_arrive_expect_tx(&rfull[rp.idx], KH * OZ_NT * 8);
+                tma_load_2d(raw_ring + rp.idx * RAWB, &sx_map, (int)(nt * OZ_NT),
+                            (int)((kb0 + i) * OZ_KB + (MP ? crank * KH : 0)), &rfull[rp.idx]);
             }
         }
         __syncwarp();
@@ -468,7 +525,10 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                 const bool first = (i % FKB) == 0;
                 if (first && c > 0) mbar_wait(&acc_empty, (unsigned)((c - 1) & 1));  // drained
                 mbar_wait(&full[st], sp.phase);
-                mbar_wait(&bfull[st], sp.phase);
+                if (MP)
+                    mbar_wait_cluster(&bfull[st], sp.phase);
+                else
+                    mbar_wait(&bfull[st], sp.phase);
                 tc_fence_after();
                 const unsigned sa = sbase + st * STAGE, sb = sa + A_BYTES;
                 // A plane s against B planes t0 .. t0+w-1 in one MMA: the planes sit
@@ -482,7 +542,8 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
                     for (int t0 = 0; t0 < S - s; t0 += 4) {
                         const int w = S - s - t0 < 4 ? S - s - t0 : 4;
                         mma_i8(tmem + (uint32_t)((s + t0) * OZ_NT), umma_desc(sa + s * OZ_MT * OZ_KB),
-                               umma_desc(sb + t0 * OZ_NT * OZ_KB), oz_idesc(OZ_MT, OZ_NT * w),
+                               MP ? umma_desc(sb + t0 * 1024, S * 1024, 128) : umma_desc(sb + t0 * OZ_NT * OZ_KB),
+                               oz_idesc(OZ_MT, OZ_NT * w),
                                (first && s == 0) ? 0 : 1);
                     }
                 if (csize > 1)
@@ -625,8 +686,12 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
         run_absmax(ctx, sx, K, d, amax_b, s);
     }
     ctx->oz_colmax_for = nullptr;
+    // M-tile pairs (MP kernel): the two M tiles of each (N tile, split) share one conversion of
+    // S.X (option oz_mpair; needs an even number of M tiles)
+    const bool mpair = ctx->opt_oz_mpair && tm % 2 == 0;
     // S.X tiles staged by TMA when its rows are 16 B aligned (a tensor map of the K x d
-    // row-major block; boxes of 32 rows x 64 columns, zero-filled past the edges)
+    // row-major block; boxes of 32 rows x 64 columns -- 16 rows for MP -- zero-filled past the
+    // edges)
     CUtensorMap sx_map;
     memset(&sx_map, 0, sizeof(sx_map));
     int staged = ctx->opt_oz_staged && d % 2 == 0 && ((uintptr_t)sx % 16) == 0 && K < (1ll << 31);
@@ -640,7 +705,7 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
         }
         const cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)K};
         const cuuint64_t gstride[1] = {(cuuint64_t)d * 8};
-        const cuuint32_t box[2] = {OZ_NT, OZ_KB}, estride[2] = {1, 1};
+        const cuuint32_t box[2] = {OZ_NT, (cuuint32_t)(mpair ? OZ_KB / 2 : OZ_KB)}, estride[2] = {1, 1};
         staged = encode && encode(&sx_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)sx, gdim, gstride, box, estride,
                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -650,21 +715,25 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     int nst = ctx->opt_oz_st > 0 ? (int)ctx->opt_oz_st : (S >= 6 ? 3 : 4);
     const int64_t stage_bytes = oz_stage_bytes<S>();
     if (nst > OZ_MAX_RING) nst = OZ_MAX_RING;
-    const int64_t raw_min = staged ? 2 * OZ_RAW : 0;  // the direct path needs no raw ring
+    const int64_t raw_bytes = mpair ? OZ_RAW / 2 : OZ_RAW;  // MP: a CTA stages half of each tile
+    const int64_t raw_min = staged ? 2 * raw_bytes : 0;     // the direct path needs no raw ring
     while (nst > 2 && nst * stage_bytes + raw_min + 1024 > OZ_SMEM_MAX) --nst;
-    int nrs = staged ? (int)((OZ_SMEM_MAX - 1024 - nst * stage_bytes) / OZ_RAW) : 0;
-    if (ctx->opt_oz_rs > 0 && ctx->opt_oz_rs < nrs) nrs = (int)ctx->opt_oz_rs;
+    int nrs = staged ? (int)((OZ_SMEM_MAX - 1024 - nst * stage_bytes) / raw_bytes) : 0;
+    // (option oz_rs counts tiles of 16 KB: MP's half tiles get twice as many slots in the same bytes)
+    const int64_t rs_req = ctx->opt_oz_rs * (mpair ? 2 : 1);
+    if (rs_req > 0 && rs_req < nrs) nrs = (int)rs_req;
     if (nrs > OZ_MAX_RING) nrs = OZ_MAX_RING;
     // the two converter groups take alternate k-blocks: an even raw ring gives each group its
     // own slots (with an odd one a group's consecutive waits on a slot would be two phases
     // apart, which a parity wait cannot tell from one)
     if (staged) nrs = nrs < 2 ? 2 : nrs & ~1;
-    const size_t smem = (size_t)(nst * stage_bytes + nrs * OZ_RAW + 1024);
-    CGX_CUDA(cudaFuncSetAttribute(oz_gemm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem = (size_t)(nst * stage_bytes + nrs * raw_bytes + 1024);
+    auto kern = mpair ? oz_gemm<S, 1> : oz_gemm<S, 0>;
+    CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // clusters along the N tiles share G's planes by multicast: the GEMM is bound by the
     // operand traffic out of L2, and every N tile otherwise re-reads the same G chunks
-    int csize = (int)ctx->opt_oz_cluster;
-    while (csize > 1 && tn % csize) csize >>= 1;
+    int csize = mpair ? 2 : (int)ctx->opt_oz_cluster;
+    while (csize > 1 && !mpair && tn % csize) csize >>= 1;
     if (csize < 1) csize = 1;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
@@ -672,8 +741,8 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = (unsigned)csize;
+    attr[0].val.clusterDim.x = mpair ? 2u : 1u;  // MP: the M-tile pair; else N tiles sharing G's planes
+    attr[0].val.clusterDim.y = mpair ? 1u : (unsigned)csize;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
@@ -684,7 +753,7 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     if (csize > 1) {
         cfg.gridDim = dim3((unsigned)tm, (unsigned)tn, 1);
         int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, oz_gemm<S>, &cfg) == cudaSuccess && nclusters > 0)
+        if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters > 0)
             resident = (int64_t)nclusters * csize;
         cudaGetLastError();
     }
@@ -695,7 +764,7 @@ bool run_ozaki(cgx_ctx* ctx, const cgx_xform* xf, int64_t b0, int64_t b1, const 
     splits = (nkb + kps - 1) / kps;
     double* zpart = (double*)ctx->zpart.get(sizeof(double) * (size_t)(splits * m * d));
     cfg.gridDim = dim3((unsigned)tm, (unsigned)tn, (unsigned)splits);
-    CGX_CUDA(cudaLaunchKernelEx(&cfg, oz_gemm<S>, aimg, a_nkb, a_kb0, sx, K, d, nkb, kps, amax_a, amax_b, m, zpart,
+    CGX_CUDA(cudaLaunchKernelEx(&cfg, kern, aimg, a_nkb, a_kb0, sx, K, d, nkb, kps, amax_a, amax_b, m, zpart,
                                 staged, nst, nrs, csize, sx_map));
     count_launch(ctx);
     check_launch("oz_gemm");

@@ -458,8 +458,38 @@ def test_stage2_ozaki_cluster_and_rings(cg, restatement, cluster, rs, st, ozaki)
         assert rel_fro(z, restatement.gemm(G, sx)) <= Z_TOL
     finally:
         ctx.set_option("oz_cluster", 2)
-        ctx.set_option("oz_rs", 2)
+        ctx.set_option("oz_rs", 4)
         ctx.set_option("oz_st", 0)
+
+
+@pytest.mark.parametrize("m,d,B", [(256, 512, 30011), (512, 64, 5000), (256, 70, 999)])
+@pytest.mark.parametrize("S,staged", [(7, 1), (7, 0), (5, 1)])
+def test_stage2_ozaki_mpair(cg, restatement, m, d, B, S, staged, ozaki):
+    """M-tile pairs (option oz_mpair, the default for an even number of 128-row M tiles): each
+    CTA of a pair converts half of every S.X tile and sends its half of the digit planes to the
+    peer over DSMEM.  The digits and the integer products are the same, so Z is bit-identical
+    to the unpaired kernel's, and within the bar of the oracle."""
+    from paper_1606_05732_b200._lib import CGX_MEM_HOST, check, lib
+
+    ozaki(S, staged)
+    ctx = cg.context()
+    sx = np.random.default_rng(m + d).standard_normal((B, d))
+    sx[:, 1] *= 1e-200  # a column at the bottom of the scale range
+    t = cg.countgauss_new(m, B, 10, cg.SeededRng(17))
+    _, _, gs = restatement.countgauss_seeds(17)
+    G = restatement.gaussian(gs, m, B)
+    zs = []
+    try:
+        for mp in (0, 1):
+            ctx.set_option("oz_mpair", mp)
+            z = np.empty((m, d), order="F")
+            check(lib.cgx_gauss_gemm_range(ctx.h, t._xf.h, np.ascontiguousarray(sx).ctypes.data, 0, B, d,
+                                           CGX_MEM_HOST, z.ctypes.data, CGX_MEM_HOST, None))
+            zs.append(z)
+    finally:
+        ctx.set_option("oz_mpair", 1)
+    assert np.array_equal(zs[0], zs[1])
+    assert rel_fro(zs[1], restatement.gemm(G, sx)) <= OZ_TOL[S]
 
 
 @pytest.mark.parametrize("b0,b1", [(0, 4096), (64, 3000), (33, 4000), (4001, 4096)])
