@@ -10,7 +10,8 @@ equal to the oracle where the oracle is exact:
   * sketch_dense_async (cp.async ring, 2/3/4 slots) and the register-batch variant;
   * countgauss_dense_ws (one-pass: sketch warps -> G warps -> math warps over mbarriers);
   * sketch_csr_lean (persistent task queue) and the chunked-branch partial reduction;
-  * oz_gemm (TMA + bulk-copy rings, tcgen05 commits, 1/2/4-CTA cluster multicast);
+  * oz_gemm (TMA + bulk-copy rings, tcgen05 commits, 1/2/4-CTA cluster multicast, and the
+    M-tile pairs' DSMEM bulk copies of digit planes with cluster-scope barriers);
   * the CSR record path's S.X (order-free atomics: equal to the oracle within its bar on
     every run, and Z within 1e-12).
 """
@@ -31,8 +32,8 @@ def _opts(cg, **kv):
 
 
 def _reset(cg, keys):
-    defaults = {"async_stages": 2, "fuse": 1, "g_resident": 1, "csr_mode": 0, "oz_cluster": 2, "oz_rs": 2, "oz_st": 0,
-                "grid_waves": 1}
+    defaults = {"async_stages": 2, "fuse": 1, "g_resident": 1, "csr_mode": 0, "oz_cluster": 2, "oz_rs": 4, "oz_st": 0,
+                "grid_waves": 1, "oz_mpair": 1}
     ctx = cg.context()
     for k in keys:
         ctx.set_option(k, defaults[k])
@@ -125,3 +126,24 @@ def test_csr_record_path_repeatable_within_bar(cg, restatement):
             assert np.linalg.norm(z - z_ref) <= 1e-12 * np.linalg.norm(z_ref)
     finally:
         _reset(cg, ["csr_mode"])
+
+
+@pytest.mark.parametrize("rs,st", [(4, 0), (2, 0), (2, 2), (6, 0)])
+def test_tensor_core_stage2_mpair_repeatable(cg, restatement, rs, st):
+    """M-tile pairs (m = 256: two 128-row tiles per cluster): each CTA converts half of every
+    S.X tile and bulk-copies its digit planes into the peer over DSMEM; Z must be the same
+    bits on every run and equal to the unpaired kernel's."""
+    n, d, B, m = 40000, 192, 12000, 256
+    x = restatement.gen_dense_f32(29, n, d)
+    _opts(cg, oz_rs=rs, oz_st=st, oz_mpair=1)
+    try:
+        t = cg.countgauss_new(m, B, n, cg.SeededRng(13))
+        z0 = cg.countgauss_apply(t, x)
+        z_ref, _ = restatement.countgauss(13, m, B, x=x.astype(np.float64))
+        assert np.linalg.norm(z0 - z_ref) <= 1e-12 * np.linalg.norm(z_ref)
+        for _ in range(REPS):
+            assert np.array_equal(cg.countgauss_apply(t, x), z0)
+        _opts(cg, oz_mpair=0)
+        assert np.array_equal(cg.countgauss_apply(t, x), z0)
+    finally:
+        _reset(cg, ["oz_rs", "oz_st", "oz_mpair"])
