@@ -409,7 +409,12 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             }
             uint32_t dig[S][VPT / 4];
             if (OZ_EXP != 1) oz_digits<S, VPT>(cur, F, dig);
-            if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);  // MMAs of k-block i - STAGES done
+            if (i >= OZ_STAGES) {  // MMAs of k-block i - STAGES done (a peer's, too, with clusters: cluster scope)
+                if (csize > 1)
+                    mbar_wait_cluster(&empty[sp.idx], sp.phase ^ 1u);
+                else
+                    mbar_wait(&empty[sp.idx], sp.phase ^ 1u);
+            }
             uint8_t* bp = stage + A_BYTES + soff;
 #pragma unroll
             for (int s = 0; s < S * (OZ_EXP != 1); ++s) {
@@ -481,7 +486,12 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             const int8_t* ga = aimg + (mt * a_nkb + a_kb0 + kb0) * (int64_t)A_BYTES;
             RingPos sp(OZ_STAGES);
             for (int64_t i = 0; i < nk; ++i, sp.next()) {
-                if (i >= OZ_STAGES) mbar_wait(&empty[sp.idx], sp.phase ^ 1u);
+                if (i >= OZ_STAGES) {
+                    if (csize > 1)
+                        mbar_wait_cluster(&empty[sp.idx], sp.phase ^ 1u);
+                    else
+                        mbar_wait(&empty[sp.idx], sp.phase ^ 1u);
+                }
                 if (OZ_EXP == 2) { mbar_arrive(&full[sp.idx]); continue; }
                 mbar_arrive_expect_tx(&full[sp.idx], A_BYTES);
                 if (csize > 1 && !MP) {
@@ -498,7 +508,7 @@ oz_gemm(const int8_t* __restrict__ aimg, int64_t a_nkb, int64_t a_kb0, const dou
             // exit
             if (csize > 1) {
                 const int64_t i0 = nk > OZ_STAGES ? nk - OZ_STAGES : 0;
-                for (int64_t i = i0; i < nk; ++i) mbar_wait(&empty[i % OZ_STAGES], (unsigned)((i / OZ_STAGES) & 1));
+                for (int64_t i = i0; i < nk; ++i) mbar_wait_cluster(&empty[i % OZ_STAGES], (unsigned)((i / OZ_STAGES) & 1));
             }
         }
         __syncwarp();
