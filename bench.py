@@ -17,10 +17,17 @@ weak are the labelled alternatives.  Time is the max over ranks.
 Reported beside `value` (device-resident X):
   roofline      -- the sketch kernel (stage 1), CUDA events on its launch stream,
                    algorithmic bytes n*d*4 + B*d*8 per launch vs MEASURED_PEAKS hbm_gbs;
+                   roofline.ceiling: the measured hardware rate that bounds it where that
+                   is not HBM bandwidth (random-row gather, random DRAM accesses, the CSR
+                   record path's RED + copy floor; DESIGN.md section 5);
+  stage2        -- the G.(S.X) kernel against its own peak (int8 tensor or FP64 DMMA);
   e2e           -- the same metric through the C-ABI with X in pinned HOST memory
                    (H2D of X and D2H of Z inside the timed region);
+  e2e_dropin    -- cg::countgauss_apply through the reference's own C++ API (pageable fp64
+                   DenseMatrix / SparseMatrix), drop-in vs the reference library, same host;
   cpu_baseline  -- the reference's own countgauss_apply (oracle/_ref, compiled from the
-                   reference sources) on the box's host cores, full c2 in fp64.
+                   reference sources) on the box's host cores, full c2 in fp64;
+  clocks        -- NVML SM clock and clock-event reasons sampled during the timed region.
 --impl reference times that CPU implementation alone (rank 0), as the reference arm.
 """
 from __future__ import annotations
