@@ -273,14 +273,26 @@ int cgx_host_checksum(cgx_ctx* ctx, const void* p, size_t bytes, uint64_t* out);
  *   CGX_COMBINE_SX reduce-scatter of S.X by bucket range (ceil(B/P) buckets per rank);
  *                  split-K stage 2 on the owned slice; all-reduce of Z
  *   CGX_COMBINE_Z  both stages per rank on its shard; all-reduce of Z
+ *   CGX_COMBINE_P2P no NCCL: the reduce-scatter of S.X is fused into the sketch kernels, whose
+ *                  finished bucket rows are stored straight into the owning rank's landing
+ *                  buffer over peer-mapped memory (NVLink / NVSwitch); owners sum their P slots
+ *                  and the partial Z's in rank order, so every rank gets the same bits and the
+ *                  result does not depend on timing.  Needs peer access between all devices
+ *                  (else CGX_EINVAL) and at most 8 ranks.  A device may be listed twice in
+ *                  cgx_group_init (two ranks on one GPU); such a group supports only this mode.
  * Z equals the single-GPU result up to floating-point reassociation across ranks. */
-enum { CGX_COMBINE_Z = 0, CGX_COMBINE_G = 1, CGX_COMBINE_SX = 2 };
+enum { CGX_COMBINE_Z = 0, CGX_COMBINE_G = 1, CGX_COMBINE_SX = 2, CGX_COMBINE_P2P = 3 };
 typedef struct cgx_group cgx_group;
 typedef struct cgx_gxform cgx_gxform;
 int cgx_group_init(int ndev, const int* devs, cgx_group** out);
 int cgx_group_free(cgx_group* g);
 int cgx_group_size(const cgx_group* g);
 int cgx_group_context(cgx_group* g, int rank, cgx_ctx** out); /* rank's context (owned by the group) */
+/* CGX_COMBINE_P2P bookkeeping, summed over ranks: stage-1 calls whose gather kernel stored its
+ * rows straight into the owners' landing slots, and calls that sketched locally and copied the
+ * bucket ranges out (the kernels without segmented stores: narrow dense X, the chunked CSR
+ * branch, the record path). */
+int cgx_group_stats(const cgx_group* g, int64_t* fused_sketches, int64_t* copied_sketches);
 int cgx_group_countgauss_new(cgx_group* g, uint64_t t_seed, int64_t m, int64_t buckets, int64_t input_dim,
                              cgx_gxform** out);
 int cgx_gxform_free(cgx_gxform* t);

@@ -16,7 +16,7 @@ CGX_F64, CGX_F32 = 0, 1
 CGX_I64, CGX_I32 = 0, 1
 CGX_COL_MAJOR, CGX_ROW_MAJOR = 0, 1
 CGX_MEM_HOST, CGX_MEM_DEVICE = 0, 1
-CGX_COMBINE_Z, CGX_COMBINE_G, CGX_COMBINE_SX = 0, 1, 2
+CGX_COMBINE_Z, CGX_COMBINE_G, CGX_COMBINE_SX, CGX_COMBINE_P2P = 0, 1, 2, 3
 
 _P, _I64, _U64, _I, _D, _SZ = C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_double, C.c_size_t
 
@@ -72,6 +72,7 @@ SIGNATURES = {
     "cgx_separable_mixing": (_I, [_U64, _I64, _I64, _D, _P]),
     "cgx_host_checksum": (_I, [_P, _P, _SZ, _P]),
     "cgx_group_init": (_I, [_I, _P, _P]),
+    "cgx_group_stats": (_I, [_P, _P, _P]),
     "cgx_group_free": (_I, [_P]),
     "cgx_group_size": (_I, [_P]),
     "cgx_group_context": (_I, [_P, _I, _P]),

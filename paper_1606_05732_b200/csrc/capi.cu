@@ -267,6 +267,35 @@ const void* dense_rowmajor(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int
     return xd;
 }
 
+// A stage-1 call of a device group in CGX_COMBINE_P2P mode (ctx->out_segs set): when the
+// sketch kernel that will run cannot store into the peers' landing slots itself, it writes a
+// local S.X (ctx->seg_local) and the bucket ranges are copied out afterwards.
+struct SegsFallback {
+    cgx_ctx* ctx;
+    const cgx_xform* xf;
+    int64_t d;
+    const OutSegs* held = nullptr;
+    double* local = nullptr;
+    SegsFallback(cgx_ctx* c, const cgx_xform* x, int64_t dd, bool fused, double** sx) : ctx(c), xf(x), d(dd) {
+        if (!ctx->out_segs) return;
+        ++(fused ? ctx->seg_fused : ctx->seg_copied);
+        if (fused) return;
+        held = ctx->out_segs;
+        ctx->out_segs = nullptr;
+        local = (double*)ctx->seg_local.get(sizeof(double) * (size_t)(xf->B * d));
+        *sx = local;
+    }
+    void finish(cudaStream_t s) {
+        if (!held) return;
+        ctx->out_segs = held;
+        push_segs(ctx, local, xf->B, d, *held, s);
+        held = nullptr;
+    }
+    ~SegsFallback() {
+        if (held) ctx->out_segs = held;
+    }
+};
+
 // Stage 1 (dense): SX row-major (B x d) into `sx_dev`.
 void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
                       int64_t n, int64_t d, int x_mem, double* sx_dev, cudaStream_t s) {
@@ -289,7 +318,9 @@ void sketch_dense_dev(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtyp
     }
     if (d == 0) return;
     ctx->prof.begin(0, s);
+    SegsFallback fb(ctx, xf, d, sketch_dense_fuses_segs(ctx, xd, dtype, rld, d), &sx_dev);
     launch_sketch_dense(ctx, xf, xd, dtype, rld, n, d, sx_dev, s);
+    fb.finish(s);
     ctx->prof.end(0, s);
 }
 
@@ -327,12 +358,25 @@ void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
     stage_csr(ctx, &rp, &cp, &idx_type, &vp, &dtype, n, nnz, x_mem, s);
     ctx->prof.begin(0, s);
     const int64_t chunk_rows = csr_chunk_rows(n, xf->B, d);
-    if (chunk_rows == 0 && csr_atomic_applies(ctx, xf, n, d, nnz, dtype))
+    const bool records = chunk_rows == 0 && csr_atomic_applies(ctx, xf, n, d, nnz, dtype);
+    SegsFallback fb(ctx, xf, d, !records && sketch_csr_fuses_segs(ctx, d, chunk_rows), &sx_dev);
+    if (records)
         launch_sketch_csr_atomic(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, n, d, nnz, sx_dev, s);
     else
         launch_sketch_csr(ctx, xf, (const int64_t*)rp, cp, idx_type, vp, dtype, n, d, sx_dev, chunk_rows, s);
+    fb.finish(s);
     ctx->prof.end(0, s);
 }
+
+} // namespace
+void push_segs(cgx_ctx* ctx, const double* sx, int64_t B, int64_t d, const OutSegs& segs, cudaStream_t s) {
+    (void)ctx;
+    for (int64_t q = 0, b0 = 0; b0 < B; ++q, b0 += segs.per) {
+        const int64_t nb = std::min<int64_t>(segs.per, B - b0);
+        CGX_CUDA(cudaMemcpyAsync(segs.base[q], sx + b0 * d, sizeof(double) * (size_t)(nb * d), cudaMemcpyDeviceToDevice, s));
+    }
+}
+namespace {
 
 void need_g(const cgx_xform* xf) {
     if (!xf->has_g) fail(CGX_EINVAL, "countgauss_apply: transform has no Gaussian factor (use countgauss_new)");
@@ -464,7 +508,7 @@ int cgx_free(cgx_ctx* ctx) {
         ctx->gfull.release();
         ctx->gchunk.release();
         for (DevBuf& b : ctx->part) b.release();
-        for (DevBuf* b : {&ctx->oz_max, &ctx->oz_a, &ctx->oz_b}) b->release();
+        for (DevBuf* b : {&ctx->oz_max, &ctx->oz_a, &ctx->oz_b, &ctx->seg_local}) b->release();
         cudaStreamDestroy(ctx->stream);
         cudaFree(ctx->task_ctr);
         delete ctx;
@@ -479,7 +523,7 @@ int cgx_trim(cgx_ctx* ctx) {
         CGX_CUDA(cudaDeviceSynchronize());
         for (DevBuf* b : {&ctx->sx, &ctx->zpart, &ctx->xstage, &ctx->tmp, &ctx->sort_k[0], &ctx->sort_k[1],
                           &ctx->sort_v[0], &ctx->sort_v[1], &ctx->sort_hist, &ctx->counts, &ctx->hstage_dev,
-                          &ctx->gfull, &ctx->gchunk, &ctx->oz_max, &ctx->oz_a})
+                          &ctx->gfull, &ctx->gchunk, &ctx->oz_max, &ctx->oz_a, &ctx->seg_local})
             b->release();
         for (DevBuf& b : ctx->hin) b.release();
         for (DevBuf& b : ctx->part) b.release();

@@ -11,6 +11,18 @@
 //   CGX_COMBINE_SX (CSR):  reduce-scatter of S.X by bucket range, split-K stage 2 on the
 //                  owned slice, all-reduce of Z;
 //   CGX_COMBINE_Z:         every rank runs both stages on its shard, all-reduce of Z.
+// and, without NCCL, over peer memory:
+//   CGX_COMBINE_P2P: the reduce-scatter of S.X is fused into the sketch kernels.  Every rank
+//                  owns a bucket range and a landing buffer of P slots; rank p's gather
+//                  kernel stores each finished bucket row straight into slot p of the
+//                  owner's buffer (peer-mapped pointers, NVLink stores: OutSegs in
+//                  internal.h), so the transfer rides under the whole sketch instead of
+//                  following it.  The owner then sums its P slots in rank order
+//                  (`sum_slots`: a fixed order, so the result does not depend on timing),
+//                  runs the split-K stage 2 on its range, writes its m x d partial Z into
+//                  every rank's Z slots, and each rank sums those in rank order: every
+//                  rank ends with the same bits.  Ranks order their streams with events
+//                  (record, host join, wait): no kernel ever waits on another GPU's kernel.
 // Each device is driven by its own host thread (host-input staging blocks the host), its
 // kernels and collectives ordered on its context's stream.  NCCL is loaded with dlopen on
 // first use, so libcgx has no link-time NCCL dependency.
@@ -112,6 +124,25 @@ void ok_or_throw(int rc) {
     if (rc != CGX_OK) fail(rc, cgx_last_error());
 }
 
+// out[i] = ((slot_0[i] + slot_1[i]) + slot_2[i]) + ... for i < count; slots `stride` apart.
+__global__ void sum_slots(const double* __restrict__ slots, int P, int64_t stride, int64_t count,
+                          double* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        double a = slots[i];
+        for (int q = 1; q < P; ++q) a += slots[(int64_t)q * stride + i];
+        out[i] = a;
+    }
+}
+
+void launch_sum_slots(cgx_ctx* c, const double* slots, int P, int64_t stride, int64_t count, double* out,
+                      cudaStream_t st) {
+    if (count <= 0) return;
+    const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)c->num_sms * 16);
+    sum_slots<<<(unsigned)blocks, 256, 0, st>>>(slots, P, stride, count, out);
+    c->launches++;
+    CGX_CUDA(cudaGetLastError());
+}
+
 } // namespace
 } // namespace cgx
 
@@ -121,6 +152,12 @@ struct cgx_group {
     std::vector<cgx_ctx*> ctx;
     std::vector<ncclComm_t> comm;
     std::vector<cgx::DevBuf> sx, slice, zp, zg, rp;  // per-rank scratch (rp: Z row blocks)
+    // CGX_COMBINE_P2P: per-rank landing buffers (P slots of ceil(B/P) x d, and of m x d) that
+    // the other ranks' kernels and copies write, and the events ordering the ranks' streams
+    std::vector<cgx::DevBuf> land, zslot;
+    std::vector<cudaEvent_t> ev_sx, ev_z;
+    bool have_nccl = false, p2p = false;
+    std::string nccl_why, p2p_why;
 };
 
 struct cgx_gxform {
@@ -228,9 +265,80 @@ void partial_rank(cgx_group* g, const cgx_gxform* t, int p, int64_t d, int mode,
     apply(c, t->xf[(size_t)p], sx, false);
 }
 
-void check_mode(int mode) {
+void check_mode(const cgx_group* g, int mode) {
+    if (mode == CGX_COMBINE_P2P) {
+        if (!g->p2p) fail(CGX_EINVAL, "cgx_group: CGX_COMBINE_P2P unavailable: " + g->p2p_why);
+        return;
+    }
     if (mode != CGX_COMBINE_Z && mode != CGX_COMBINE_G && mode != CGX_COMBINE_SX)
-        fail(CGX_EINVAL, "cgx_group: combine must be CGX_COMBINE_Z, CGX_COMBINE_G or CGX_COMBINE_SX");
+        fail(CGX_EINVAL, "cgx_group: combine must be CGX_COMBINE_Z, _G, _SX or _P2P");
+    if (!g->have_nccl) fail(CGX_ENCCL, "cgx_group: " + g->nccl_why);
+}
+
+// CGX_COMBINE_P2P.  stage1(p, ctx, xform, out) queues rank p's countsketch_apply with `out` as
+// its (device, row-major) destination; ctx->out_segs redirects the rows to the owners' slots.
+void apply_p2p(cgx_group* g, const cgx_gxform* t, int64_t d,
+               const std::function<void(int, cgx_ctx*, cgx_xform*, double*)>& stage1, double* z_host, int z_mem,
+               double* const* z_dev) {
+    const int P = g->P;
+    const int64_t m = t->m, B = t->B, per = (B + P - 1) / P;
+    const int64_t slot = per * d, zn = m * d;
+    // every rank's kernels store into every rank's landing buffer: allocate them all first
+    for (int p = 0; p < P; ++p) {
+        CGX_CUDA(cudaSetDevice(g->dev[(size_t)p]));
+        g->land[(size_t)p].get(sizeof(double) * (size_t)(slot * P));
+        g->zslot[(size_t)p].get(sizeof(double) * (size_t)(zn * P));
+    }
+    // A: the sketches, storing (or copying) bucket range q into slot p of rank q
+    each_rank(P, [&](int p) {
+        cgx_ctx* c = g->ctx[(size_t)p];
+        CGX_CUDA(cudaSetDevice(c->device));
+        OutSegs segs{};
+        for (int q = 0; q < P; ++q) segs.base[q] = (double*)g->land[(size_t)q].p + (int64_t)p * slot;
+        segs.per = (uint32_t)per;
+        c->out_segs = &segs;
+        try {
+            stage1(p, c, t->xf[(size_t)p], segs.base[p]);
+        } catch (...) {
+            c->out_segs = nullptr;
+            throw;
+        }
+        c->out_segs = nullptr;
+        CGX_CUDA(cudaEventRecord(g->ev_sx[(size_t)p], c->stream));
+    });
+    // B: rank p sums its slots, runs stage 2 on its bucket range, hands its partial Z to everyone
+    each_rank(P, [&](int p) {
+        cgx_ctx* c = g->ctx[(size_t)p];
+        cudaStream_t st = c->stream;
+        CGX_CUDA(cudaSetDevice(c->device));
+        for (int q = 0; q < P; ++q) CGX_CUDA(cudaStreamWaitEvent(st, g->ev_sx[(size_t)q], 0));
+        const int64_t b0 = std::min(B, p * per), b1 = std::min(B, b0 + per);
+        double* sl = (double*)g->slice[(size_t)p].get(sizeof(double) * (size_t)slot);
+        double* zp = (double*)g->zp[(size_t)p].get(sizeof(double) * (size_t)zn);
+        launch_sum_slots(c, (const double*)g->land[(size_t)p].p, P, slot, (b1 - b0) * d, sl, st);
+        if (b1 > b0)
+            ok_or_throw(cgx_gauss_gemm_range(c, t->xf[(size_t)p], sl, b0, b1, d, CGX_MEM_DEVICE, zp, CGX_MEM_DEVICE, st));
+        else
+            CGX_CUDA(cudaMemsetAsync(zp, 0, sizeof(double) * (size_t)zn, st));
+        for (int q = 0; q < P; ++q)
+            CGX_CUDA(cudaMemcpyAsync((double*)g->zslot[(size_t)q].p + (int64_t)p * zn, zp, sizeof(double) * (size_t)zn,
+                                     cudaMemcpyDeviceToDevice, st));
+        CGX_CUDA(cudaEventRecord(g->ev_z[(size_t)p], st));
+    });
+    // C: Z = the partials in rank order, on every rank
+    each_rank(P, [&](int p) {
+        cgx_ctx* c = g->ctx[(size_t)p];
+        cudaStream_t st = c->stream;
+        CGX_CUDA(cudaSetDevice(c->device));
+        for (int q = 0; q < P; ++q) CGX_CUDA(cudaStreamWaitEvent(st, g->ev_z[(size_t)q], 0));
+        double* zfull = (double*)g->zg[(size_t)p].get(sizeof(double) * (size_t)zn);
+        launch_sum_slots(c, (const double*)g->zslot[(size_t)p].p, P, zn, zn, zfull, st);
+        if (z_mem == CGX_MEM_DEVICE)
+            CGX_CUDA(cudaMemcpyAsync(z_dev[p], zfull, sizeof(double) * (size_t)zn, cudaMemcpyDeviceToDevice, st));
+        else if (p == 0)
+            CGX_CUDA(cudaMemcpyAsync(z_host, zfull, sizeof(double) * (size_t)zn, cudaMemcpyDeviceToHost, st));
+        CGX_CUDA(cudaStreamSynchronize(st));
+    });
 }
 
 } // namespace
@@ -240,22 +348,62 @@ extern "C" {
 int cgx_group_init(int ndev, const int* devs, cgx_group** out) {
     return gguard([&] {
         if (!out || ndev < 1 || !devs) fail(CGX_EINVAL, "cgx_group_init: need ndev >= 1 devices");
+        // A device listed twice gives two ranks on one GPU: NCCL refuses that, the peer-memory
+        // combine does not (its "peer" pointers are then local) -- which is also how the P2P path
+        // is tested on a one-GPU box.
+        std::vector<int> uniq(devs, devs + ndev);
+        std::sort(uniq.begin(), uniq.end());
+        const bool distinct = std::adjacent_find(uniq.begin(), uniq.end()) == uniq.end();
         const Nccl& N = nccl();
-        if (!N.ok) fail(CGX_ENCCL, "cgx_group_init: " + N.why);
+        if (distinct && !N.ok) fail(CGX_ENCCL, "cgx_group_init: " + N.why);
         auto* g = new cgx_group;
         g->P = ndev;
         g->dev.assign(devs, devs + ndev);
         g->ctx.assign((size_t)ndev, nullptr);
         g->comm.assign((size_t)ndev, nullptr);
-        g->sx.resize((size_t)ndev);
-        g->slice.resize((size_t)ndev);
-        g->zp.resize((size_t)ndev);
-        g->zg.resize((size_t)ndev);
-        g->rp.resize((size_t)ndev);
+        g->ev_sx.assign((size_t)ndev, nullptr);
+        g->ev_z.assign((size_t)ndev, nullptr);
+        for (auto* v : {&g->sx, &g->slice, &g->zp, &g->zg, &g->rp, &g->land, &g->zslot}) v->resize((size_t)ndev);
         try {
             for (int p = 0; p < ndev; ++p) ok_or_throw(cgx_init(devs[p], &g->ctx[(size_t)p]));
-            check_nccl(N.CommInitAll(g->comm.data(), ndev, devs), "ncclCommInitAll");
+            if (distinct) {
+                check_nccl(N.CommInitAll(g->comm.data(), ndev, devs), "ncclCommInitAll");
+                g->have_nccl = true;
+            } else {
+                g->nccl_why = "a device appears twice in the group: only CGX_COMBINE_P2P applies";
+            }
+            // peer access, both ways, between every pair of distinct devices
+            g->p2p = ndev <= kMaxSegs;
+            if (!g->p2p) g->p2p_why = "more than " + std::to_string(kMaxSegs) + " ranks";
+            for (int p = 0; p < ndev && g->p2p; ++p) {
+                CGX_CUDA(cudaSetDevice(devs[p]));
+                for (int q = 0; q < ndev && g->p2p; ++q) {
+                    if (devs[q] == devs[p]) continue;
+                    int can = 0;
+                    CGX_CUDA(cudaDeviceCanAccessPeer(&can, devs[p], devs[q]));
+                    if (!can) {
+                        g->p2p = false;
+                        g->p2p_why = "device " + std::to_string(devs[p]) + " cannot map device " + std::to_string(devs[q]);
+                        break;
+                    }
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(devs[q], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled)
+                        cudaGetLastError();
+                    else
+                        CGX_CUDA(e);
+                }
+            }
+            for (int p = 0; p < ndev; ++p) {
+                CGX_CUDA(cudaSetDevice(devs[p]));
+                CGX_CUDA(cudaEventCreateWithFlags(&g->ev_sx[(size_t)p], cudaEventDisableTiming));
+                CGX_CUDA(cudaEventCreateWithFlags(&g->ev_z[(size_t)p], cudaEventDisableTiming));
+            }
         } catch (...) {
+            for (int p = 0; p < ndev; ++p) {
+                if (g->ev_sx[(size_t)p]) cudaEventDestroy(g->ev_sx[(size_t)p]);
+                if (g->ev_z[(size_t)p]) cudaEventDestroy(g->ev_z[(size_t)p]);
+                if (g->comm[(size_t)p]) N.CommDestroy(g->comm[(size_t)p]);
+            }
             for (auto* c : g->ctx)
                 if (c) cgx_free(c);
             delete g;
@@ -268,12 +416,17 @@ int cgx_group_init(int ndev, const int* devs, cgx_group** out) {
 int cgx_group_free(cgx_group* g) {
     return gguard([&] {
         if (!g) return;
-        for (int p = 0; p < g->P; ++p) {
+        for (int p = 0; p < g->P; ++p) {  // (peers write each other's buffers: quiesce all first)
             cudaSetDevice(g->dev[(size_t)p]);
             cudaDeviceSynchronize();
+        }
+        for (int p = 0; p < g->P; ++p) {
+            cudaSetDevice(g->dev[(size_t)p]);
             for (auto* b : {&g->sx[(size_t)p], &g->slice[(size_t)p], &g->zp[(size_t)p], &g->zg[(size_t)p],
-                            &g->rp[(size_t)p]})
+                            &g->rp[(size_t)p], &g->land[(size_t)p], &g->zslot[(size_t)p]})
                 b->release();
+            cudaEventDestroy(g->ev_sx[(size_t)p]);
+            cudaEventDestroy(g->ev_z[(size_t)p]);
             if (g->comm[(size_t)p]) nccl().CommDestroy(g->comm[(size_t)p]);
             cgx_free(g->ctx[(size_t)p]);
         }
@@ -282,6 +435,19 @@ int cgx_group_free(cgx_group* g) {
 }
 
 int cgx_group_size(const cgx_group* g) { return g ? g->P : 0; }
+
+int cgx_group_stats(const cgx_group* g, int64_t* fused_sketches, int64_t* copied_sketches) {
+    return gguard([&] {
+        if (!g) fail(CGX_EINVAL, "cgx_group_stats: null group");
+        int64_t f = 0, c = 0;
+        for (const cgx_ctx* x : g->ctx) {
+            f += x->seg_fused;
+            c += x->seg_copied;
+        }
+        if (fused_sketches) *fused_sketches = f;
+        if (copied_sketches) *copied_sketches = c;
+    });
+}
 
 int cgx_group_context(cgx_group* g, int rank, cgx_ctx** out) {
     return gguard([&] {
@@ -342,22 +508,32 @@ int cgx_group_countgauss_apply_dense(cgx_group* g, const cgx_gxform* t, const vo
                                      int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem, int combine) {
     return gguard([&] {
         if (!g || !t || t->g != g) fail(CGX_EINVAL, "cgx_group: null group or transform of another group");
-        check_mode(combine);
+        check_mode(g, combine);
         if (n != t->n)
             fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
                                  std::to_string(t->n));
         if (d < 1) fail(CGX_EINVAL, "cgx_group: X must have at least one column");
         if (layout != CGX_COL_MAJOR && layout != CGX_ROW_MAJOR) fail(CGX_EINVAL, "cgx: bad layout");
         const size_t es = dtype == CGX_F32 ? 4 : 8;
+        auto shard_of = [&](int p, int64_t* rows) -> const void* {
+            const int64_t r0 = t->r0[(size_t)p];
+            *rows = t->r1[(size_t)p] - r0;
+            if (x_mem == CGX_MEM_DEVICE) return ((const void* const*)x)[p];  // rank p's shard on its device
+            return (const char*)x + es * (size_t)(layout == CGX_COL_MAJOR ? r0 : r0 * ld);
+        };
+        if (combine == CGX_COMBINE_P2P) {
+            apply_p2p(g, t, d, [&](int p, cgx_ctx* c, cgx_xform* xf, double* out) {
+                int64_t rows = 0;
+                const void* xp = shard_of(p, &rows);
+                ok_or_throw(cgx_countsketch_apply_dense(c, xf, xp, dtype, layout, ld, rows, d, x_mem, out, CGX_ROW_MAJOR,
+                                                        CGX_MEM_DEVICE, nullptr));
+            }, z, z_mem, (double* const*)z);
+            return;
+        }
         each_rank(g->P, [&](int p) {
-            const int64_t r0 = t->r0[(size_t)p], rows = t->r1[(size_t)p] - r0;
-            const void* xp;
-            int64_t lp = ld;
-            if (x_mem == CGX_MEM_DEVICE) {
-                xp = ((const void* const*)x)[p];  // rank p's shard on its device
-            } else {
-                xp = (const char*)x + es * (size_t)(layout == CGX_COL_MAJOR ? r0 : r0 * ld);
-            }
+            int64_t rows = 0;
+            const void* xp = shard_of(p, &rows);
+            const int64_t lp = ld;
             partial_rank(g, t, p, d, combine, [&](cgx_ctx* c, cgx_xform* xf, double* out, bool both) {
                 if (both)
                     ok_or_throw(cgx_countgauss_apply_dense(c, xf, xp, dtype, layout, lp, rows, d, x_mem, out,
@@ -376,20 +552,38 @@ int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int6
                                    double* z, int z_mem, int combine) {
     return gguard([&] {
         if (!g || !t || t->g != g) fail(CGX_EINVAL, "cgx_group: null group or transform of another group");
-        check_mode(combine);
+        check_mode(g, combine);
         if (n != t->n)
             fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
                                  std::to_string(t->n));
         if (d < 1 || nnz < 0) fail(CGX_EINVAL, "cgx_group: bad CSR sizes");
         if (!rowptr || rowptr[0] != 0 || rowptr[n] != nnz) fail(CGX_EINVAL, "cgx_group: row offsets must run 0..nnz");
         const size_t is = idx_type == CGX_I32 ? 4 : 8, vs = dtype == CGX_F32 ? 4 : 8;
+        // the shard's row offsets, rebased to its own nonzeros; its nonzeros stay in the
+        // caller's host arrays and are staged by the apply (pipelined, narrowed)
+        auto rebase = [&](int p, std::vector<int64_t>& rp, int64_t* rows, int64_t* q0, int64_t* q1) {
+            const int64_t r0 = t->r0[(size_t)p];
+            *rows = t->r1[(size_t)p] - r0;
+            *q0 = rowptr[r0];
+            *q1 = rowptr[r0 + *rows];
+            rp.resize((size_t)(*rows + 1));
+            for (int64_t i = 0; i <= *rows; ++i) rp[(size_t)i] = rowptr[r0 + i] - *q0;
+        };
+        if (combine == CGX_COMBINE_P2P) {
+            apply_p2p(g, t, d, [&](int p, cgx_ctx* c, cgx_xform* xf, double* out) {
+                std::vector<int64_t> rp;
+                int64_t rows, q0, q1;
+                rebase(p, rp, &rows, &q0, &q1);
+                ok_or_throw(cgx_countsketch_apply_csr(c, xf, rp.data(), (const char*)cols + is * (size_t)q0, idx_type,
+                                                      (const char*)vals + vs * (size_t)q0, dtype, rows, d, q1 - q0,
+                                                      CGX_MEM_HOST, out, CGX_ROW_MAJOR, CGX_MEM_DEVICE, nullptr));
+            }, z, z_mem, (double* const*)z);
+            return;
+        }
         each_rank(g->P, [&](int p) {
-            const int64_t r0 = t->r0[(size_t)p], rows = t->r1[(size_t)p] - r0;
-            const int64_t q0 = rowptr[r0], q1 = rowptr[r0 + rows];
-            // the shard's row offsets, rebased to its own nonzeros; its nonzeros stay in the
-            // caller's host arrays and are staged by the apply (pipelined, narrowed)
-            std::vector<int64_t> rp((size_t)(rows + 1));
-            for (int64_t i = 0; i <= rows; ++i) rp[(size_t)i] = rowptr[r0 + i] - q0;
+            std::vector<int64_t> rp;
+            int64_t rows, q0, q1;
+            rebase(p, rp, &rows, &q0, &q1);
             const void* cp = (const char*)cols + is * (size_t)q0;
             const void* vp = (const char*)vals + vs * (size_t)q0;
             partial_rank(g, t, p, d, combine, [&](cgx_ctx* c, cgx_xform* xf, double* out, bool both) {

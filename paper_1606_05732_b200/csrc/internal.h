@@ -36,6 +36,16 @@ struct DevBuf {
 
 struct HostPool;
 
+// Where a sketch kernel's finished S.X rows land when a device group combines the partial
+// sketches over peer memory (group.cu, CGX_COMBINE_P2P): bucket b's row is stored at
+// base[b / per] + (b % per) * d -- base[q] is this rank's slot in the landing buffer of the
+// rank that owns buckets [q*per, (q+1)*per), a peer-mapped pointer (NVLink / NVSwitch).
+constexpr int kMaxSegs = 8;
+struct OutSegs {
+    double* base[kMaxSegs];
+    uint32_t per;
+};
+
 struct Profile {
     bool on = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[2];
@@ -105,6 +115,12 @@ struct cgx_ctx {
     int64_t opt_oz_staged = 1;              // option "oz_staged": S.X rows reach the converters by bulk copy (0 = loads)
     int64_t opt_oz_mpair = 1;               // option "oz_mpair": M-tile pairs share the S.X conversion over DSMEM
     cgx::DevBuf oz_max, oz_a, oz_b;         // (oz_b: column maxima of S.X)
+    // Set by group.cu around a stage-1 call: S.X rows go to the owners' landing slots instead of
+    // `sx`.  The gather kernels store there directly (sketch_dense_async, sketch_csr_lean);
+    // every other sketch path writes seg_local and push_segs copies the bucket ranges out.
+    const cgx::OutSegs* out_segs = nullptr;
+    cgx::DevBuf seg_local;
+    int64_t seg_fused = 0, seg_copied = 0;  // stage-1 calls of each kind (cgx_group_stats)
     const double* oz_colmax_for = nullptr;  // S.X whose column maxima the sketch left in oz_b
     int64_t oz_colmax_d = 0;         // ozgemm.cu scratch: scales, digit images of G and S.X
 };
@@ -174,6 +190,12 @@ void launch_transpose_x(cgx_ctx* ctx, const void* x, int dtype, int64_t ld, int6
                         cudaStream_t s);
 // row-major B x d (fp64) -> col-major
 void launch_transpose_sx(cgx_ctx* ctx, const double* src, int64_t B, int64_t d, double* dst, cudaStream_t s);
+
+// sketch_dense.cu / sketch_csr.cu: whether the launch below stores straight into ctx->out_segs
+bool sketch_dense_fuses_segs(const cgx_ctx* ctx, const void* x, int dtype, int64_t ld, int64_t d);
+bool sketch_csr_fuses_segs(const cgx_ctx* ctx, int64_t d, int64_t chunk_rows);
+// capi.cu: rows [q*per, (q+1)*per) of a local row-major S.X -> segs.base[q] (device-to-device copies)
+void push_segs(cgx_ctx* ctx, const double* sx, int64_t B, int64_t d, const OutSegs& segs, cudaStream_t s);
 
 // sketch_csr.cu
 void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,

@@ -203,14 +203,18 @@ __global__ void __launch_bounds__(256) sketch_csr_kernel(const int64_t* __restri
 //  * warps are persistent and pull tasks of G consecutive buckets from a counter, the last
 //    ones single buckets (B1 = buckets in G-groups), so no SM idles while a late CTA wave
 //    finishes.
-template <typename TV, typename TI>
+//  * SEG: a bucket's finished row goes to its owner's landing slot in peer memory (`segs`,
+//    internal.h OutSegs) instead of sx: the device group's reduce-scatter transfer, spread
+//    over the whole kernel (group.cu, CGX_COMBINE_P2P).
+template <typename TV, typename TI, bool SEG = false>
 __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64_t* __restrict__ rowptr, const TI* __restrict__ cols,
                                                        const TV* __restrict__ vals, const uint32_t* __restrict__ perm,
                                                        const uint32_t* __restrict__ offsets, int64_t B, int64_t d,
                                                        double* __restrict__ sx, int G, int64_t B1,
                                                        unsigned long long* __restrict__ next_task,
                                                        unsigned long long task_base,
-                                                       unsigned long long* __restrict__ colmax) {
+                                                       unsigned long long* __restrict__ colmax,
+                                                       const __grid_constant__ OutSegs segs) {
     constexpr int kW = CGX_CSR_KW;
     pdl_trigger();  // stage 2 may be scheduled as these CTAs drain
     extern __shared__ double smem[];
@@ -329,8 +333,13 @@ __global__ void __launch_bounds__(256, CGX_CSR_MINB) sketch_csr_lean(const int64
             }
         }
         __syncwarp();
+        double* orow = sx + b * d;
+        if (SEG) {
+            const uint32_t q = (uint32_t)b / segs.per;
+            orow = segs.base[q] + (int64_t)((uint32_t)b - q * segs.per) * d;
+        }
         for (int64_t j = lane; j < d; j += 32) {
-            sx[b * d + j] = acc[j];
+            orow[j] = acc[j];
             if (colmax) {  // (a plain read first: after the first buckets the max rarely moves)
                 const unsigned long long u = (unsigned long long)__double_as_longlong(fabs(acc[j]));
                 if (u > *(volatile unsigned long long*)&cmax[j]) atomicMax(&cmax[j], u);
@@ -390,15 +399,17 @@ bool launch_lean(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const
     int wl = (int)((96 * 1024) / per_warp_l);
     wl = wl > 8 ? 8 : wl;
     if (wl < 1) return false;
+    const OutSegs* segs = ctx->out_segs;  // (a partial sketch: its column maxima are not S.X's)
+    if (segs && !colmax_ok) fail(CGX_ECUDA, "internal: the chunked CSR sketch cannot write peer landing slots");
     unsigned long long* colmax = nullptr;
-    if (colmax_ok && oz_stage2_applies(ctx, xf, d)) {
+    if (colmax_ok && !segs && oz_stage2_applies(ctx, xf, d)) {
         colmax = (unsigned long long*)ctx->oz_b.get(sizeof(unsigned long long) * (size_t)d);
         CGX_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * (size_t)d, s));
         ctx->oz_colmax_for = sx;
         ctx->oz_colmax_d = d;
     }
     const size_t sm = (per_warp_l * wl + 7) / 8 * 8 + (colmax ? sizeof(unsigned long long) * (size_t)d : 8);
-    auto lk = sketch_csr_lean<TV, TI>;
+    auto lk = segs ? sketch_csr_lean<TV, TI, true> : sketch_csr_lean<TV, TI>;
     CGX_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 0;
     CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, wl * 32, sm));
@@ -415,7 +426,7 @@ bool launch_lean(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const
     B1 = B1 < 0 ? 0 : B1 / G * G;
     const unsigned long long base = take_tasks(ctx, B1 / G + nb_total - B1, nb * wl);
     lk<<<(unsigned)nb, wl * 32, sm, s>>>(rowptr, cols, vals, xf->perm, offs, nb_total, d, sx, (int)G, B1,
-                                         ctx->task_ctr, base, colmax);
+                                         ctx->task_ctr, base, colmax, segs ? *segs : OutSegs{});
     count_launch(ctx);
     tasks_launched(ctx, s);
     check_launch("sketch_csr_lean");
@@ -469,6 +480,7 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const TI* 
             }
         }
     }
+    if (ctx->out_segs) fail(CGX_ECUDA, "internal: this CSR sketch kernel cannot write peer landing slots");
     auto kern = sketch_csr_kernel<TV, TI, CHUNKED>;
     if (smem > 40 * 1024) CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int64_t blocks = (xf->B + warps - 1) / warps;
@@ -492,6 +504,12 @@ void dispatch_chunk(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
 }
 
 } // namespace
+
+// Mirrors launch<>(): the lean gather, unchunked, with a warp's accumulator in shared memory.
+bool sketch_csr_fuses_segs(const cgx_ctx* ctx, int64_t d, int64_t chunk_rows) {
+    (void)ctx;
+    return chunk_rows == 0 && d <= 8192;
+}
 
 void launch_sketch_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols, int idx_type,
                        const void* vals, int dtype, int64_t n, int64_t d, double* sx, int64_t chunk_rows,

@@ -328,13 +328,17 @@ __device__ __forceinline__ void stream_buckets_async(const T* __restrict__ x, in
 // and output as sketch_dense_stream.  Shared memory: per warp S x 32 x CB ring + S masks.
 // Tasks are handed out in bucket order: groups of G buckets for the first B1 buckets, then
 // single buckets, so the last tasks -- which set the kernel's tail -- are short.
-template <typename T, int V, int S>
+// SEG: the finished rows go to `segs` (the bucket-range owners' landing slots in peer memory,
+// internal.h OutSegs) instead of sx -- the stores of the partial sketch are the transfer of
+// the device group's reduce-scatter, spread over the whole kernel (group.cu, CGX_COMBINE_P2P).
+template <typename T, int V, int S, bool SEG = false>
 __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ x, int64_t ld, int64_t d,
                                                           const uint32_t* __restrict__ perm,
                                                           const uint32_t* __restrict__ offsets, int64_t B,
                                                           int64_t nchunks, int G, int64_t B1, double* __restrict__ sx,
                                                           unsigned long long* __restrict__ next_task,
-                                                          unsigned long long task_base) {
+                                                          unsigned long long task_base,
+                                                          const __grid_constant__ OutSegs segs) {
     pdl_trigger();  // stage 2 may be scheduled as these CTAs drain
     constexpr int CW = 32 * V;
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -361,8 +365,13 @@ __global__ void __launch_bounds__(256) sketch_dense_async(const T* __restrict__ 
         stream_buckets_async<T, V, S>(x, ld, cw0, qv, perm, offsets, b0, nb, ring, sneg,
                                       [&](int i, const double (&acc)[V]) {
                                           if (colok) {
+                                              double* o = out + (int64_t)i * d;
+                                              if (SEG) {
+                                                  const uint32_t b = (uint32_t)(b0 + i), q = b / segs.per;
+                                                  o = segs.base[q] + (int64_t)(b - q * segs.per) * d + col0;
+                                              }
 #pragma unroll
-                                              for (int k = 0; k < V; ++k) out[(int64_t)i * d + k] = acc[k];
+                                              for (int k = 0; k < V; ++k) o[k] = acc[k];
                                           }
                                       });
     }
@@ -548,6 +557,16 @@ void transpose(cgx_ctx* ctx, const E* src, int64_t rows, int64_t cols, int64_t l
     }
 }
 
+// The cp.async ring kernel applies: 16 B pieces all the way (and a row pitch below 4 GB).
+inline bool async_ring_ok(int S, const void* x, size_t es, int64_t ld, int64_t d) {
+    return S >= 2 && (uintptr_t)x % 16 == 0 && (ld * es) % 16 == 0 && (d * es) % 16 == 0;
+}
+// Paths that cannot store into a device group's landing slots: capi.cu's SegsFallback has
+// cleared ctx->out_segs for them (sketch_dense_fuses_segs said so).
+inline void no_segs(const cgx_ctx* ctx) {
+    if (ctx->out_segs) fail(CGX_ECUDA, "internal: this sketch kernel cannot write peer landing slots");
+}
+
 template <typename T, int V, int R>
 void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d, double* sx, int accumulate,
             cudaStream_t s) {
@@ -561,14 +580,17 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
         const int64_t tasks = (xf->B + G - 1) / G * nchunks;
         const int S = (int)ctx->opt_async;
         const size_t CB = (size_t)CW * sizeof(T);
-        if (S >= 2 && (uintptr_t)x % 16 == 0 && (ld * sizeof(T)) % 16 == 0 && (d * sizeof(T)) % 16 == 0) {
+        if (async_ring_ok(S, x, sizeof(T), ld, d)) {
             // cp.async ring: W warps per CTA, each with S x 32 rows x CB of shared memory
             const size_t per_warp = (size_t)S * 32 * CB + (size_t)S * 4;
             int W = (int)((200 * 1024) / per_warp);
             W = W > 8 ? 8 : (W < 1 ? 1 : W);
             const size_t smem = per_warp * W;
-            auto kern = S == 2 ? sketch_dense_async<T, V, 2> : S == 3 ? sketch_dense_async<T, V, 3>
-                                                                       : sketch_dense_async<T, V, 4>;
+            const OutSegs* segs = ctx->out_segs;  // (only with S == 2: sketch_dense_fuses_segs)
+            auto kern = segs     ? sketch_dense_async<T, V, 2, true>
+                        : S == 2 ? sketch_dense_async<T, V, 2>
+                        : S == 3 ? sketch_dense_async<T, V, 3>
+                                 : sketch_dense_async<T, V, 4>;
             CGX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int per_sm = 0;
             CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem));
@@ -580,12 +602,13 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
             B1 = B1 < 0 ? 0 : B1 / G * G;
             const unsigned long long base = take_tasks(ctx, (B1 / G + xf->B - B1) * nchunks, blocks * W);
             kern<<<(unsigned)blocks, 32 * W, smem, s>>>(x, ld, d, xf->perm, xf->offsets, xf->B, nchunks, (int)G, B1,
-                                                        sx, ctx->task_ctr, base);
+                                                        sx, ctx->task_ctr, base, segs ? *segs : OutSegs{});
             count_launch(ctx);
             tasks_launched(ctx, s);
             check_launch("sketch_dense_async");
             return;
         }
+        no_segs(ctx);
         auto kern = sketch_dense_stream<T, V>;
         int per_sm = 0;
         CGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
@@ -598,6 +621,7 @@ void launch(cgx_ctx* ctx, const cgx_xform* xf, const T* x, int64_t ld, int64_t d
         check_launch("sketch_dense_stream");
         return;
     }
+    no_segs(ctx);
     const int64_t nchunks = (d + CW - 1) / CW;
     const int64_t warps = xf->B * nchunks;
     int64_t blocks = (warps + 7) / 8;
@@ -839,6 +863,12 @@ bool launch_countgauss_dense_fused(cgx_ctx* ctx, const cgx_xform* xf, const void
                                    int64_t d, double* z, cudaStream_t s) {
     if (dtype == CGX_F32) return fused_dispatch<float>(ctx, xf, (const float*)x, ld, d, z, s);
     return fused_dispatch<double>(ctx, xf, (const double*)x, ld, d, z, s);
+}
+
+// Mirrors dispatch() + launch(): R == 1 (d > 16), the async ring with its default depth.
+bool sketch_dense_fuses_segs(const cgx_ctx* ctx, const void* x, int dtype, int64_t ld, int64_t d) {
+    const size_t es = dtype == CGX_F32 ? 4 : 8;
+    return d > 16 && ld * (int64_t)es < ((int64_t)1 << 32) && ctx->opt_async == 2 && async_ring_ok(2, x, es, ld, d);
 }
 
 void launch_sketch_dense(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int64_t ld, int64_t n,
