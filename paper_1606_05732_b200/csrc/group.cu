@@ -29,8 +29,11 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -123,6 +126,30 @@ void each_rank(int P, F&& f) {
 void ok_or_throw(int rc) {
     if (rc != CGX_OK) fail(rc, cgx_last_error());
 }
+
+// Phase boundary of the rank threads inside one each_rank (the peer-memory combine): a rank
+// that failed keeps arriving, so nobody is left waiting, and everyone skips the later phases.
+struct PhaseBarrier {
+    explicit PhaseBarrier(int n) : n_(n) {}
+    void arrive_and_wait() {
+        std::unique_lock<std::mutex> lk(m_);
+        const uint64_t g = gen_;
+        if (++count_ == n_) {
+            count_ = 0;
+            ++gen_;
+            cv_.notify_all();
+        } else {
+            cv_.wait(lk, [&] { return gen_ != g; });
+        }
+    }
+    std::atomic<bool> failed{false};
+
+private:
+    std::mutex m_;
+    std::condition_variable cv_;
+    int n_, count_ = 0;
+    uint64_t gen_ = 0;
+};
 
 // out[i] = ((slot_0[i] + slot_1[i]) + slot_2[i]) + ... for i < count; slots `stride` apart.
 __global__ void sum_slots(const double* __restrict__ slots, int P, int64_t stride, int64_t count,
@@ -289,55 +316,78 @@ void apply_p2p(cgx_group* g, const cgx_gxform* t, int64_t d,
         g->land[(size_t)p].get(sizeof(double) * (size_t)(slot * P));
         g->zslot[(size_t)p].get(sizeof(double) * (size_t)(zn * P));
     }
-    // A: the sketches, storing (or copying) bucket range q into slot p of rank q
+    // One thread per rank, three phases separated by host barriers (an event must have been
+    // recorded before another rank's stream can be made to wait on it).
+    PhaseBarrier bar(P);
     each_rank(P, [&](int p) {
         cgx_ctx* c = g->ctx[(size_t)p];
-        CGX_CUDA(cudaSetDevice(c->device));
-        OutSegs segs{};
-        for (int q = 0; q < P; ++q) segs.base[q] = (double*)g->land[(size_t)q].p + (int64_t)p * slot;
-        segs.per = (uint32_t)per;
-        c->out_segs = &segs;
-        try {
-            stage1(p, c, t->xf[(size_t)p], segs.base[p]);
-        } catch (...) {
+        cudaStream_t st = c->stream;
+        Error err{CGX_OK, ""};
+        auto phase = [&](auto&& body) {
+            if (bar.failed.load()) return;
+            try {
+                body();
+            } catch (const Error& e) {
+                err = e;
+                bar.failed.store(true);
+            } catch (const std::exception& e) {
+                err = Error{CGX_ECUDA, e.what()};
+                bar.failed.store(true);
+            }
+        };
+        // A: the sketch, storing (or copying) bucket range q into slot p of rank q
+        phase([&] {
+            CGX_CUDA(cudaSetDevice(c->device));
+            OutSegs segs{};
+            for (int q = 0; q < P; ++q) segs.base[q] = (double*)g->land[(size_t)q].p + (int64_t)p * slot;
+            segs.per = (uint32_t)per;
+            c->out_segs = &segs;
+            try {
+                stage1(p, c, t->xf[(size_t)p], segs.base[p]);
+            } catch (...) {
+                c->out_segs = nullptr;
+                throw;
+            }
             c->out_segs = nullptr;
-            throw;
-        }
-        c->out_segs = nullptr;
-        CGX_CUDA(cudaEventRecord(g->ev_sx[(size_t)p], c->stream));
-    });
-    // B: rank p sums its slots, runs stage 2 on its bucket range, hands its partial Z to everyone
-    each_rank(P, [&](int p) {
-        cgx_ctx* c = g->ctx[(size_t)p];
-        cudaStream_t st = c->stream;
-        CGX_CUDA(cudaSetDevice(c->device));
-        for (int q = 0; q < P; ++q) CGX_CUDA(cudaStreamWaitEvent(st, g->ev_sx[(size_t)q], 0));
-        const int64_t b0 = std::min(B, p * per), b1 = std::min(B, b0 + per);
-        double* sl = (double*)g->slice[(size_t)p].get(sizeof(double) * (size_t)slot);
-        double* zp = (double*)g->zp[(size_t)p].get(sizeof(double) * (size_t)zn);
-        launch_sum_slots(c, (const double*)g->land[(size_t)p].p, P, slot, (b1 - b0) * d, sl, st);
-        if (b1 > b0)
-            ok_or_throw(cgx_gauss_gemm_range(c, t->xf[(size_t)p], sl, b0, b1, d, CGX_MEM_DEVICE, zp, CGX_MEM_DEVICE, st));
-        else
-            CGX_CUDA(cudaMemsetAsync(zp, 0, sizeof(double) * (size_t)zn, st));
-        for (int q = 0; q < P; ++q)
-            CGX_CUDA(cudaMemcpyAsync((double*)g->zslot[(size_t)q].p + (int64_t)p * zn, zp, sizeof(double) * (size_t)zn,
-                                     cudaMemcpyDeviceToDevice, st));
-        CGX_CUDA(cudaEventRecord(g->ev_z[(size_t)p], st));
-    });
-    // C: Z = the partials in rank order, on every rank
-    each_rank(P, [&](int p) {
-        cgx_ctx* c = g->ctx[(size_t)p];
-        cudaStream_t st = c->stream;
-        CGX_CUDA(cudaSetDevice(c->device));
-        for (int q = 0; q < P; ++q) CGX_CUDA(cudaStreamWaitEvent(st, g->ev_z[(size_t)q], 0));
-        double* zfull = (double*)g->zg[(size_t)p].get(sizeof(double) * (size_t)zn);
-        launch_sum_slots(c, (const double*)g->zslot[(size_t)p].p, P, zn, zn, zfull, st);
-        if (z_mem == CGX_MEM_DEVICE)
-            CGX_CUDA(cudaMemcpyAsync(z_dev[p], zfull, sizeof(double) * (size_t)zn, cudaMemcpyDeviceToDevice, st));
-        else if (p == 0)
-            CGX_CUDA(cudaMemcpyAsync(z_host, zfull, sizeof(double) * (size_t)zn, cudaMemcpyDeviceToHost, st));
-        CGX_CUDA(cudaStreamSynchronize(st));
+            CGX_CUDA(cudaEventRecord(g->ev_sx[(size_t)p], st));
+        });
+        bar.arrive_and_wait();
+        // B: rank p sums its slots, runs stage 2 on its bucket range, hands its partial Z to everyone
+        phase([&] {
+            for (int q = 0; q < P; ++q)
+                if (q != p) CGX_CUDA(cudaStreamWaitEvent(st, g->ev_sx[(size_t)q], 0));
+            const int64_t b0 = std::min(B, p * per), b1 = std::min(B, b0 + per);
+            double* sl = (double*)g->slice[(size_t)p].get(sizeof(double) * (size_t)slot);
+            double* zp = (double*)g->zp[(size_t)p].get(sizeof(double) * (size_t)zn);
+            const double* mine = (const double*)g->land[(size_t)p].p;
+            if (P > 1) launch_sum_slots(c, mine, P, slot, (b1 - b0) * d, sl, st);
+            if (b1 > b0)
+                ok_or_throw(cgx_gauss_gemm_range(c, t->xf[(size_t)p], P > 1 ? sl : mine, b0, b1, d, CGX_MEM_DEVICE, zp,
+                                                 CGX_MEM_DEVICE, st));
+            else
+                CGX_CUDA(cudaMemsetAsync(zp, 0, sizeof(double) * (size_t)zn, st));
+            for (int q = 0; q < P; ++q)
+                CGX_CUDA(cudaMemcpyAsync((double*)g->zslot[(size_t)q].p + (int64_t)p * zn, zp,
+                                         sizeof(double) * (size_t)zn, cudaMemcpyDeviceToDevice, st));
+            CGX_CUDA(cudaEventRecord(g->ev_z[(size_t)p], st));
+        });
+        bar.arrive_and_wait();
+        // C: Z = the partials in rank order, on every rank
+        phase([&] {
+            for (int q = 0; q < P; ++q)
+                if (q != p) CGX_CUDA(cudaStreamWaitEvent(st, g->ev_z[(size_t)q], 0));
+            const double* zsl = (const double*)g->zslot[(size_t)p].p;
+            double* zfull = (double*)g->zg[(size_t)p].get(sizeof(double) * (size_t)zn);
+            if (P > 1) launch_sum_slots(c, zsl, P, zn, zn, zfull, st);
+            const double* zres = P > 1 ? zfull : zsl;
+            if (z_mem == CGX_MEM_DEVICE)
+                CGX_CUDA(cudaMemcpyAsync(z_dev[p], zres, sizeof(double) * (size_t)zn, cudaMemcpyDeviceToDevice, st));
+            else if (p == 0)
+                CGX_CUDA(cudaMemcpyAsync(z_host, zres, sizeof(double) * (size_t)zn, cudaMemcpyDeviceToHost, st));
+        });
+        // (a failed rank may have left work queued that reads peers' buffers: always drain)
+        cudaStreamSynchronize(st);
+        if (err.code != CGX_OK) throw err;
     });
 }
 
