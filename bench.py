@@ -424,7 +424,7 @@ def run_ours(args):
 
     from paper_1606_05732_b200.distributed import combine
 
-    sxbuf = torch.empty((B, d), dtype=torch.float64, device=dev) if world > 1 and args.combine in ("sx", "g") else None
+    sxbuf = torch.empty((B, d), dtype=torch.float64, device=dev) if world > 1 and args.combine in ("sx", "sxo", "g") else None
     sxT = torch.empty((d, B), dtype=torch.float64, device=dev) if world > 1 and args.combine == "cols" else None
 
     comb_ev = []  # (start, end) CUDA events around the combine phase of each timed step
@@ -453,8 +453,8 @@ def run_ours(args):
         else:
             cg.api.countsketch_apply_into(t, x, sxbuf)  # partial S.X (row-major B x d)
             e0 = mark()
-            if args.combine == "sx":
-                out = combine("sx", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
+            if args.combine in ("sx", "sxo"):
+                out = combine(args.combine, world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
                               stage2=lambda sl, b0, b1: cg.api.gauss_gemm_range(t, sl, b0, b1))
             else:
                 out = combine("g", world=world, rank=rank, B=B, d=d, m=m, partial_sx=sxbuf,
@@ -674,6 +674,7 @@ def run_ours(args):
                 "parallelism": f"rows sharded x{world} ({args.scaling} scaling: "
                 + ("the config's n rows per rank" if args.scaling == "weak" else "the config's n rows split across ranks")
                 + ")" + ({"z": ", NCCL all-reduce of Z", "sx": ", NCCL reduce-scatter of S.X + split-K stage 2 + all-reduce of Z",
+                       "sxo": ", NCCL all-to-all of S.X bucket ranges summed in rank order + split-K stage 2 + all-gather of Z summed in rank order",
                        "g": ", NCCL all-reduce of S.X + G's m rows split over ranks + all-gather of Z",
                        "cols": ", NCCL column reduce-scatter of S.X + split-N stage 2 + all-gather of Z"}[args.combine]
                       if world > 1 else ""),
@@ -728,9 +729,9 @@ def main():
     ap.add_argument("--placement", default="rows", choices=["rows", "hash"],
                     help="rows: contiguous row shards; hash: each rank holds the rows hashing into its bucket "
                          "range, in bucket order (SURVEY 8e ablation C; dense configs; combine = all-reduce of Z)")
-    ap.add_argument("--combine", default="auto", choices=["auto", "z", "sx", "g", "cols"],
+    ap.add_argument("--combine", default="auto", choices=["auto", "z", "sx", "sxo", "g", "cols"],
                     help="N>1 combine (auto: g for dense configs, sx for CSR -- the north star's schemes): z = all-reduce of Z; sx = reduce-scatter of S.X + split-K stage 2 + "
-                         "all-reduce; g = all-reduce of S.X + G's m rows split over ranks + all-gather; "
+                         "all-reduce; sxo = sx with all-to-all / all-gather and sums in rank order (same bits on every rank); g = all-reduce of S.X + G's m rows split over ranks + all-gather; "
                          "cols = column reduce-scatter of S.X + split-N stage 2 + all-gather")
     args = ap.parse_args()
     if args.combine == "auto":

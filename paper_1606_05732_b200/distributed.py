@@ -13,6 +13,12 @@ T.X is linear, so the partials combine after either stage:
   [b_p, b_{p+1}) of the summed S.X and computes
   Z_p = G[:, b_p:b_{p+1}) . S.X[b_p:b_{p+1}) (split-K: stage 2 and G generation divided
   by P), then Z = sum_p Z_p by all-reduce.  Communication is (P-1)/P * B*d*8 per rank.
+* ``"sxo"``: "sx" with every sum taken **in rank order**: the bucket-range chunks are
+  exchanged with one all-to-all (rank p receives everyone's chunk p), summed
+  ((c_0 + c_1) + c_2) + ..., and the partial Z's are all-gathered and summed the same way, so
+  the result is the same bits on every rank and does not depend on the collective's algorithm
+  or on timing.  This is the arithmetic of the C ABI's CGX_COMBINE_P2P (csrc/group.cu), where
+  the exchange is fused into the sketch kernels' stores over peer memory; same volume as "sx".
 * ``"g"``: the partial sketches are all-reduced (every rank holds the summed S.X), rank p
   computes rows [r_p, r_{p+1}) of Z = G[r_p:r_{p+1}, :] . S.X (cgx_gauss_gemm_rows: the
   m rows of G split across ranks, stage 2 divided by P with no further reduction), and the
@@ -64,6 +70,7 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
     mode "sx": partial_sx (B x d, row-major) is reduce-scattered by bucket range; the
                owned slice goes through stage2(sx_slice, b0, b1) -> Z_p (m x d), which is
                then all-reduced.
+    mode "sxo": the same split with all-to-all / all-gather and sums in rank order.
     mode "g":  partial_sx (B x d, row-major) is all-reduced; stage2(sx, r0, r1) returns
                rows [r0, r1) of Z ((r1-r0) x d) for g_row_range(m, world, rank), and the
                row blocks are all-gathered into Z (m x d, row-major tensor).
@@ -107,16 +114,21 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
         gathered = torch.empty((per * world, m), dtype=zt.dtype, device=zt.device)
         dist.all_gather_into_tensor(gathered, zt, group=group)
         return gathered[:d].t()  # m x d, column-major view
-    if mode != "sx":
-        raise ValueError("combine: mode must be 'z', 'sx', 'g' or 'cols'")
+    if mode not in ("sx", "sxo"):
+        raise ValueError("combine: mode must be 'z', 'sx', 'sxo', 'g' or 'cols'")
     # reduce_scatter_tensor needs equal chunks: pad B up to a multiple of world.
     per = (B + world - 1) // world
     flat = partial_sx.reshape(B, d)
     if per * world != B:
         pad = torch.zeros((per * world - B, d), dtype=flat.dtype, device=flat.device)
         flat = torch.cat([flat, pad], 0)
-    out = torch.empty((per, d), dtype=flat.dtype, device=flat.device)
-    dist.reduce_scatter_tensor(out, flat.contiguous(), group=group)
+    if mode == "sxo":
+        recv = torch.empty((world, per, d), dtype=flat.dtype, device=flat.device)
+        dist.all_to_all_single(recv.view(world * per, d), flat.contiguous(), group=group)
+        out = _ordered_sum(recv)
+    else:
+        out = torch.empty((per, d), dtype=flat.dtype, device=flat.device)
+        dist.reduce_scatter_tensor(out, flat.contiguous(), group=group)
     # rank p owns the ceil(B/world)-bucket chunk [b0, b1) clamped to B (trailing ranks may
     # own nothing when B is small: they contribute a zero Z)
     b0 = min(B, rank * per)
@@ -127,5 +139,18 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
         if m is None:
             raise ValueError("combine: mode 'sx' needs m when a rank owns no buckets")
         z = torch.zeros((m, d), dtype=flat.dtype, device=flat.device).t().contiguous().t()
+    if mode == "sxo":
+        zc = z.contiguous()
+        parts = torch.empty((world,) + tuple(zc.shape), dtype=zc.dtype, device=zc.device)
+        dist.all_gather_into_tensor(parts.view(world * zc.shape[0], zc.shape[1]), zc, group=group)
+        return _ordered_sum(parts)
     dist.all_reduce(z, group=group)
     return z
+
+
+def _ordered_sum(parts):
+    """((parts[0] + parts[1]) + parts[2]) + ...: the slot sum of group.cu's sum_slots."""
+    acc = parts[0].clone()
+    for q in range(1, parts.shape[0]):
+        acc += parts[q]
+    return acc

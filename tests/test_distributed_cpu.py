@@ -82,21 +82,56 @@ def _worker(rank, world, port, mode, out_path, B=B):
                 return torch.zeros((M, D), dtype=torch.float64)
             Gs = O.gaussian(g_seed, M, b1 - b0, c0=b0)
             return torch.from_numpy(np.ascontiguousarray(O.gemm(Gs, sx_slice.numpy())))
-        z = combine("sx", world=world, rank=rank, B=B, d=D, m=M,
+        z = combine(mode, world=world, rank=rank, B=B, d=D, m=M,
                     partial_sx=torch.from_numpy(np.ascontiguousarray(sx_p)), stage2=stage2)
+    if mode == "sxo":  # every rank's Z, for the same-bits check
+        np.save(f"{out_path}.{rank}.npy", np.ascontiguousarray(z.numpy()))
     if rank == 0:
         np.save(out_path, z.numpy())
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("mode", ["z", "sx", "g", "cols", "hash"])
+@pytest.mark.parametrize("mode", ["z", "sx", "sxo", "g", "cols", "hash"])
 def test_multi_rank_combine_matches_single_device(tmp_path, mode, world):
     out = str(tmp_path / f"z_{mode}.npy")
     mp.spawn(_worker, args=(world, _free_port(), mode, out), nprocs=world, join=True)
     z = np.load(out)
     z_ref, _ = oracle.Restatement().countgauss(SEED, M, B, x=_problem())
     assert np.linalg.norm(z - z_ref) / np.linalg.norm(z_ref) <= 1e-13
+
+
+@pytest.mark.parametrize("world,buckets", [(2, B), (3, B), (4, 5)])
+def test_rank_ordered_combine_is_the_sequential_sum_on_every_rank(tmp_path, world, buckets):
+    """"sxo" (the arithmetic of CGX_COMBINE_P2P): every rank returns the same bits, and they
+    are the ones a single process gets by summing the partial S.X chunks and the partial Z's
+    in rank order."""
+    out = str(tmp_path / "z_sxo.npy")
+    mp.spawn(_worker, args=(world, _free_port(), "sxo", out, buckets), nprocs=world, join=True)
+    zs = [np.load(f"{out}.{r}.npy") for r in range(world)]
+    for r in range(1, world):
+        assert np.array_equal(zs[r], zs[0])
+    O = oracle.Restatement()
+    x = _problem()
+    _, cs_seed, g_seed = O.countgauss_seeds(SEED)
+    parts = []
+    for r in range(world):
+        r0, r1 = shard_range(N, world, r)
+        h, s = O.hash_sign(cs_seed, buckets, r1 - r0, i0=r0)
+        parts.append(O.sketch_dense(h, s, buckets, x[r0:r1]))
+    per = (buckets + world - 1) // world
+    z = None
+    for r in range(world):
+        b0 = min(buckets, r * per)
+        b1 = min(buckets, b0 + per)
+        zp = np.zeros((M, D))
+        if b1 > b0:
+            sl = parts[0][b0:b1].copy()
+            for q in range(1, world):
+                sl += parts[q][b0:b1]
+            zp = O.gemm(O.gaussian(g_seed, M, b1 - b0, c0=b0), sl)
+        z = zp.copy() if z is None else z + zp
+    assert np.array_equal(zs[0], z)
 
 
 def test_sx_combine_with_fewer_buckets_than_ranks_chunks(tmp_path):
