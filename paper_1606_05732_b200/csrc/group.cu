@@ -23,8 +23,9 @@
 //                  every rank's Z slots, and each rank sums those in rank order: every
 //                  rank ends with the same bits.  Ranks order their streams with events
 //                  (record, host join, wait): no kernel ever waits on another GPU's kernel.
-// Each device is driven by its own host thread (host-input staging blocks the host), its
-// kernels and collectives ordered on its context's stream.  NCCL is loaded with dlopen on
+// Each device is driven by its own host thread (host-input staging blocks the host; the
+// threads are started with the group and parked between calls), its kernels and collectives
+// ordered on its context's stream.  NCCL is loaded with dlopen on
 // first use, so libcgx has no link-time NCCL dependency.
 #include <dlfcn.h>
 
@@ -33,6 +34,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -100,28 +102,80 @@ void shard(int64_t n, int P, int p, int64_t* a, int64_t* b) {  // distributed.sh
     *b = *a + base + (p < extra ? 1 : 0);
 }
 
-// Runs f(p) for every rank on its own host thread; rethrows the first failure.
-template <class F>
-void each_rank(int P, F&& f) {
-    std::vector<Error> errs((size_t)P);
-    std::vector<char> bad((size_t)P, 0);
-    std::vector<std::thread> th;
-    for (int p = 0; p < P; ++p)
-        th.emplace_back([&, p] {
-            try {
-                f(p);
-            } catch (const Error& e) {
-                errs[(size_t)p] = e;
-                bad[(size_t)p] = 1;
-            } catch (const std::exception& e) {
-                errs[(size_t)p] = Error{CGX_ECUDA, e.what()};
-                bad[(size_t)p] = 1;
+// The group's rank threads: one per device, started once (a thread start per rank and call
+// cost ~40 us of every apply) and parked on a condition variable between calls.  run(f) hands
+// f(p) to every rank's thread, waits for all of them and rethrows the first failure.
+class RankThreads {
+public:
+    explicit RankThreads(int P) : P_(P), errs_((size_t)P), bad_((size_t)P, 0) {
+        for (int p = 0; p < P; ++p) th_.emplace_back([this, p] { loop(p); });
+    }
+    ~RankThreads() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void run(const std::function<void(int)>& f) {
+        std::lock_guard<std::mutex> call(call_);  // one job at a time per group
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            job_ = &f;
+            left_ = P_;
+            std::fill(bad_.begin(), bad_.end(), 0);
+            ++gen_;
+        }
+        cv_.notify_all();
+        {
+            std::unique_lock<std::mutex> lk(m_);
+            done_.wait(lk, [&] { return left_ == 0; });
+            job_ = nullptr;
+        }
+        for (int p = 0; p < P_; ++p)
+            if (bad_[(size_t)p]) throw errs_[(size_t)p];
+    }
+
+private:
+    void loop(int p) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int)>* job;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                job = job_;
             }
-        });
-    for (auto& t : th) t.join();
-    for (int p = 0; p < P; ++p)
-        if (bad[(size_t)p]) throw errs[(size_t)p];
-}
+            try {
+                (*job)(p);
+            } catch (const Error& e) {
+                errs_[(size_t)p] = e;
+                bad_[(size_t)p] = 1;
+            } catch (const std::exception& e) {
+                errs_[(size_t)p] = Error{CGX_ECUDA, e.what()};
+                bad_[(size_t)p] = 1;
+            }
+            {
+                std::lock_guard<std::mutex> lk(m_);
+                if (--left_ == 0) done_.notify_all();
+            }
+        }
+    }
+    int P_;
+    std::vector<std::thread> th_;
+    std::vector<Error> errs_;
+    std::vector<char> bad_;
+    std::mutex m_, call_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* job_ = nullptr;
+    int left_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
 
 void ok_or_throw(int rc) {
     if (rc != CGX_OK) fail(rc, cgx_last_error());
@@ -185,7 +239,17 @@ struct cgx_group {
     std::vector<cudaEvent_t> ev_sx, ev_z;
     bool have_nccl = false, p2p = false;
     std::string nccl_why, p2p_why;
+    std::unique_ptr<cgx::RankThreads> threads;
 };
+
+namespace cgx {
+namespace {
+template <class F>
+void each_rank(cgx_group* g, F&& f) {
+    g->threads->run(std::function<void(int)>(std::forward<F>(f)));
+}
+} // namespace
+} // namespace cgx
 
 struct cgx_gxform {
     cgx_group* g = nullptr;
@@ -319,7 +383,7 @@ void apply_p2p(cgx_group* g, const cgx_gxform* t, int64_t d,
     // One thread per rank, three phases separated by host barriers (an event must have been
     // recorded before another rank's stream can be made to wait on it).
     PhaseBarrier bar(P);
-    each_rank(P, [&](int p) {
+    each_rank(g, [&](int p) {
         cgx_ctx* c = g->ctx[(size_t)p];
         cudaStream_t st = c->stream;
         Error err{CGX_OK, ""};
@@ -416,6 +480,7 @@ int cgx_group_init(int ndev, const int* devs, cgx_group** out) {
         for (auto* v : {&g->sx, &g->slice, &g->zp, &g->zg, &g->rp, &g->land, &g->zslot}) v->resize((size_t)ndev);
         try {
             for (int p = 0; p < ndev; ++p) ok_or_throw(cgx_init(devs[p], &g->ctx[(size_t)p]));
+            g->threads.reset(new RankThreads(ndev));
             if (distinct) {
                 check_nccl(N.CommInitAll(g->comm.data(), ndev, devs), "ncclCommInitAll");
                 g->have_nccl = true;
@@ -466,6 +531,7 @@ int cgx_group_init(int ndev, const int* devs, cgx_group** out) {
 int cgx_group_free(cgx_group* g) {
     return gguard([&] {
         if (!g) return;
+        g->threads.reset();
         for (int p = 0; p < g->P; ++p) {  // (peers write each other's buffers: quiesce all first)
             cudaSetDevice(g->dev[(size_t)p]);
             cudaDeviceSynchronize();
@@ -521,7 +587,7 @@ int cgx_group_countgauss_new(cgx_group* g, uint64_t t_seed, int64_t m, int64_t b
         t->r0.assign((size_t)g->P, 0);
         t->r1.assign((size_t)g->P, 0);
         try {
-            each_rank(g->P, [&](int p) {
+            each_rank(g, [&](int p) {
                 shard(input_dim, g->P, p, &t->r0[(size_t)p], &t->r1[(size_t)p]);
                 ok_or_throw(cgx_countgauss_new_shard(g->ctx[(size_t)p], t_seed, m, buckets, input_dim, t->r0[(size_t)p],
                                                      t->r1[(size_t)p] - t->r0[(size_t)p], &t->xf[(size_t)p]));
@@ -580,7 +646,7 @@ int cgx_group_countgauss_apply_dense(cgx_group* g, const cgx_gxform* t, const vo
             }, z, z_mem, (double* const*)z);
             return;
         }
-        each_rank(g->P, [&](int p) {
+        each_rank(g, [&](int p) {
             int64_t rows = 0;
             const void* xp = shard_of(p, &rows);
             const int64_t lp = ld;
@@ -630,7 +696,7 @@ int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int6
             }, z, z_mem, (double* const*)z);
             return;
         }
-        each_rank(g->P, [&](int p) {
+        each_rank(g, [&](int p) {
             std::vector<int64_t> rp;
             int64_t rows, q0, q1;
             rebase(p, rp, &rows, &q0, &q1);
