@@ -240,6 +240,7 @@ struct cgx_group {
     bool have_nccl = false, p2p = false;
     std::string nccl_why, p2p_why;
     std::unique_ptr<cgx::RankThreads> threads;
+    std::mutex mu;  // one group call at a time (the ranks' scratch and landing buffers are per group)
 };
 
 namespace cgx {
@@ -576,6 +577,7 @@ int cgx_group_countgauss_new(cgx_group* g, uint64_t t_seed, int64_t m, int64_t b
                              cgx_gxform** out) {
     return gguard([&] {
         if (!g || !out) fail(CGX_EINVAL, "cgx_group_countgauss_new: null argument");
+        std::lock_guard<std::mutex> group_lock(g->mu);
         if (m < 1 || buckets < 1 || input_dim < 1)
             fail(CGX_EINVAL, "countgauss_new: m, buckets and input_dim must be >= 1");
         auto* t = new cgx_gxform;
@@ -624,6 +626,7 @@ int cgx_group_countgauss_apply_dense(cgx_group* g, const cgx_gxform* t, const vo
                                      int64_t ld, int64_t n, int64_t d, int x_mem, double* z, int z_mem, int combine) {
     return gguard([&] {
         if (!g || !t || t->g != g) fail(CGX_EINVAL, "cgx_group: null group or transform of another group");
+        std::lock_guard<std::mutex> group_lock(g->mu);
         check_mode(g, combine);
         if (n != t->n)
             fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
@@ -668,6 +671,7 @@ int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int6
                                    double* z, int z_mem, int combine) {
     return gguard([&] {
         if (!g || !t || t->g != g) fail(CGX_EINVAL, "cgx_group: null group or transform of another group");
+        std::lock_guard<std::mutex> group_lock(g->mu);
         check_mode(g, combine);
         if (n != t->n)
             fail(CGX_EINVAL, "countsketch_apply: X has " + std::to_string(n) + " rows, sketch expects " +
