@@ -1,9 +1,11 @@
 """Device groups (group.cu): the C-ABI multi-GPU path -- row shards built from the shared
-seed, partials combined over NCCL (CGX_COMBINE_G / _SX / _Z).  One GPU is available to the
-tests, so the group has one rank here: the plumbing (NCCL communicator, collectives,
-shard bookkeeping, host and device-sharded inputs) runs for real and Z must equal the
-single-context apply within the Z bar.  The multi-rank combine arithmetic is covered on CPU
-by tests/test_distributed_cpu.py (gloo, world 2-4)."""
+seed, partials combined over NCCL (CGX_COMBINE_G / _SX / _Z) or over peer memory with the
+reduce-scatter fused into the sketch kernels (CGX_COMBINE_P2P, second half of this file).  One
+GPU is available to the tests.  The NCCL modes run on a one-rank group: the plumbing (NCCL
+communicator, collectives, shard bookkeeping, host and device-sharded inputs) runs for real and
+Z must equal the single-context apply within the Z bar; their multi-rank combine arithmetic is
+covered on CPU by tests/test_distributed_cpu.py (gloo, world 2-4).  The peer-memory mode runs
+with 1, 2 and 3 ranks that share device 0."""
 import ctypes as C
 
 import numpy as np
