@@ -288,6 +288,9 @@ int cgx_group_init(int ndev, const int* devs, cgx_group** out);
 int cgx_group_free(cgx_group* g);
 int cgx_group_size(const cgx_group* g);
 int cgx_group_context(cgx_group* g, int rank, cgx_ctx** out); /* rank's context (owned by the group) */
+/* 1 if the group can run this combine mode (NCCL modes: distinct devices; CGX_COMBINE_P2P: peer
+ * access between all of them and at most 8 ranks), else 0. */
+int cgx_group_supports(const cgx_group* g, int combine);
 /* CGX_COMBINE_P2P bookkeeping, summed over ranks: stage-1 calls whose gather kernel stored its
  * rows straight into the owners' landing slots, and calls that sketched locally and copied the
  * bucket ranges out (the kernels without segmented stores: narrow dense X, the chunked CSR

@@ -24,15 +24,24 @@
 //  * std::invalid_argument with the reference's messages; CGX_ERANGE -> length_error;
 //  * thread safety: one process-wide context, calls serialized inside libcgx (the
 //    reference calls these from OpenMP regions, distcheck.cpp:107-111).
+// Beyond the reference: CGX_DEVICES="0,1,2,3" makes countgauss_apply on a constructor-built
+// (seeded) transform span those GPUs -- rows of X split across them, each GPU staging its own
+// row block over its own PCIe link, the partial sketches combined over NVLink (cgx_group_*,
+// INTEGRATION.md).  CGX_COMBINE = p2p | g | sx | z picks the combine (default: the sketch
+// kernels' peer-memory stores when the devices can map each other, else NCCL).
 #include "countgauss/sketch.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <list>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
+#include <vector>
 
 #include "cgx.h"
 
@@ -56,6 +65,56 @@ cgx_ctx* context() {
         check(cgx_init(dev ? std::atoi(dev) : 0, &ctx));
     });
     return ctx;
+}
+
+// ---- CGX_DEVICES: the device group and its row-sharded transforms --------------------
+cgx_group* group() {
+    static std::once_flag once;
+    static cgx_group* g = nullptr;
+    std::call_once(once, [] {
+        const char* list = std::getenv("CGX_DEVICES");
+        if (!list) return;
+        std::vector<int> devs;
+        for (const char* p = list; *p;) {
+            char* end = nullptr;
+            const long v = std::strtol(p, &end, 10);
+            if (end == p) break;
+            devs.push_back((int)v);
+            p = *end == ',' ? end + 1 : end;
+        }
+        if (devs.size() < 2) return;  // one device: the single-context path (CGX_DEVICE)
+        check(cgx_group_init((int)devs.size(), devs.data(), &g));
+    });
+    return g;
+}
+
+int group_combine(cgx_group* g, bool dense) {
+    const char* c = std::getenv("CGX_COMBINE");
+    const std::string want = c ? c : "";
+    if (want == "z") return CGX_COMBINE_Z;
+    if (want == "g") return CGX_COMBINE_G;
+    if (want == "sx") return CGX_COMBINE_SX;
+    if (want == "p2p" || cgx_group_supports(g, CGX_COMBINE_P2P)) return CGX_COMBINE_P2P;
+    return dense ? CGX_COMBINE_G : CGX_COMBINE_SX;  // the north star's NCCL schemes
+}
+
+// Group transforms are pure functions of (seed, m, B, n): built on first use, a few kept.
+std::shared_ptr<cgx_gxform> group_xform(cgx_group* g, uint64_t t_seed, index_t m, index_t B, index_t n) {
+    using Key = std::tuple<uint64_t, index_t, index_t, index_t>;
+    static std::mutex mu;
+    static std::list<std::pair<Key, std::shared_ptr<cgx_gxform>>> lru;
+    std::lock_guard<std::mutex> lk(mu);
+    const Key k{t_seed, m, B, n};
+    for (auto it = lru.begin(); it != lru.end(); ++it)
+        if (it->first == k) {
+            lru.splice(lru.begin(), lru, it);
+            return lru.front().second;
+        }
+    cgx_gxform* t = nullptr;
+    check(cgx_group_countgauss_new(g, t_seed, m, B, n, &t));
+    lru.emplace_front(k, std::shared_ptr<cgx_gxform>(t, cgx_gxform_free));
+    while (lru.size() > 4) lru.pop_back();
+    return lru.front().second;
 }
 
 struct Xform {
@@ -263,8 +322,9 @@ CountGaussTransform countgauss_new(index_t m, index_t input_dim, SeededRng& rng)
 }
 
 namespace {
-template <class Apply>
-DenseMatrix countgauss_apply_impl(const CountGaussTransform& t, index_t rows, index_t cols, Apply&& apply) {
+template <class Apply, class GroupApply>
+DenseMatrix countgauss_apply_impl(const CountGaussTransform& t, index_t rows, index_t cols, Apply&& apply,
+                                  GroupApply&& group_apply) {
     if (rows != t.cs.input_dim)
         throw std::invalid_argument("countsketch_apply: X has " + std::to_string(rows) + " rows, sketch expects " +
                                     std::to_string(t.cs.input_dim));
@@ -274,6 +334,15 @@ DenseMatrix countgauss_apply_impl(const CountGaussTransform& t, index_t rows, in
     DenseMatrix z(t.g.rows(), cols);
     if (cols == 0 || t.g.rows() == 0) return z;
     if (std::shared_ptr<cgx_xform> hit = cache().find(t.cs, &t)) {  // seeded fast path
+        cgx_group* g = group();  // CGX_DEVICES: the same transform, row-sharded over the group
+        // (small inputs stay on one GPU: the shards' fixed costs would exceed the work)
+        if (g && rows >= (index_t)4096 * cgx_group_size(g)) {
+            std::shared_ptr<cgx_gxform> gt = group_xform(g, t.seed, t.g.rows(), t.cs.buckets, t.cs.input_dim);
+            group_apply(g, gt.get(), z.data());
+            if (std::getenv("CGX_SHIM_TRACE"))
+                std::fprintf(stderr, "cgx shim: countgauss_apply over %d ranks (CGX_DEVICES)\n", cgx_group_size(g));
+            return z;
+        }
         apply(hit.get(), z.data());
         return z;
     }
@@ -289,6 +358,10 @@ DenseMatrix countgauss_apply(const CountGaussTransform& t, const DenseMatrix& x)
     return countgauss_apply_impl(t, x.rows(), x.cols(), [&](cgx_xform* h, double* z) {
         check(cgx_countgauss_apply_dense(context(), h, x.data(), CGX_F64, CGX_COL_MAJOR, std::max<index_t>(x.rows(), 1),
                                          x.rows(), x.cols(), CGX_MEM_HOST, z, CGX_MEM_HOST, nullptr));
+    }, [&](cgx_group* g, cgx_gxform* gt, double* z) {
+        check(cgx_group_countgauss_apply_dense(g, gt, x.data(), CGX_F64, CGX_COL_MAJOR, std::max<index_t>(x.rows(), 1),
+                                               x.rows(), x.cols(), CGX_MEM_HOST, z, CGX_MEM_HOST,
+                                               group_combine(g, true)));
     });
 }
 
@@ -297,6 +370,10 @@ DenseMatrix countgauss_apply(const CountGaussTransform& t, const SparseMatrix& x
         check(cgx_countgauss_apply_csr(context(), h, x.row_offsets.data(), x.col_indices.data(), CGX_I64,
                                        x.values.data(), CGX_F64, x.rows, x.cols, x.nnz(), CGX_MEM_HOST, z,
                                        CGX_MEM_HOST, nullptr));
+    }, [&](cgx_group* g, cgx_gxform* gt, double* z) {
+        check(cgx_group_countgauss_apply_csr(g, gt, x.row_offsets.data(), x.col_indices.data(), CGX_I64,
+                                             x.values.data(), CGX_F64, x.rows, x.cols, x.nnz(), z, CGX_MEM_HOST,
+                                             group_combine(g, false)));
     });
 }
 

@@ -5,7 +5,7 @@
 // against integration/countgauss_gpu.cpp + libcgx.so (the drop-in, "gpu") and against the
 // reference's sketch.cpp (the CPU library, "cpu"), so both numbers come from one program.
 //
-//   dropin_bench <c1|c2|c3|c4> <reps> [fp64]
+//   dropin_bench <c1|c2|c3|c3s|c4> <reps> [fp64]
 //
 // Inputs: c2/c4 dense N(0,1) values rounded to fp32 and widened (BASELINE's configs hold
 // fp32 entries) -- or, with "fp64", full-precision doubles; c3 is CSR 1% with
@@ -44,6 +44,8 @@ int main(int argc, char** argv) {
         n = (index_t)1 << 25, d = 128, B = 131072, m = 32;
     } else if (cfg == "c3") {
         n = (index_t)1 << 26, d = 256, B = 262144, m = 128;
+    } else if (cfg == "c3s") {  // c3's shape at 1/64 of the rows (test-sized CSR)
+        n = (index_t)1 << 20, d = 256, B = 16384, m = 128;
     } else {
         std::fprintf(stderr, "unknown config %s\n", cfg.c_str());
         return 2;
@@ -55,7 +57,7 @@ int main(int argc, char** argv) {
     DenseMatrix z;
     std::vector<double> ms;
     double units = 0, in_bytes = 0;
-    if (cfg == "c3") {
+    if (cfg == "c3" || cfg == "c3s") {
         SparseMatrix x;
         x.rows = n;
         x.cols = d;

@@ -73,6 +73,7 @@ SIGNATURES = {
     "cgx_host_checksum": (_I, [_P, _P, _SZ, _P]),
     "cgx_group_init": (_I, [_I, _P, _P]),
     "cgx_group_stats": (_I, [_P, _P, _P]),
+    "cgx_group_supports": (_I, [_P, _I]),
     "cgx_group_free": (_I, [_P]),
     "cgx_group_size": (_I, [_P]),
     "cgx_group_context": (_I, [_P, _I, _P]),

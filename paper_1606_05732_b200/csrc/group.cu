@@ -553,6 +553,13 @@ int cgx_group_free(cgx_group* g) {
 
 int cgx_group_size(const cgx_group* g) { return g ? g->P : 0; }
 
+int cgx_group_supports(const cgx_group* g, int combine) {
+    if (!g) return 0;
+    if (combine == CGX_COMBINE_P2P) return g->p2p ? 1 : 0;
+    if (combine == CGX_COMBINE_Z || combine == CGX_COMBINE_G || combine == CGX_COMBINE_SX) return g->have_nccl ? 1 : 0;
+    return 0;
+}
+
 int cgx_group_stats(const cgx_group* g, int64_t* fused_sketches, int64_t* copied_sketches) {
     return gguard([&] {
         if (!g) fail(CGX_EINVAL, "cgx_group_stats: null group");

@@ -61,3 +61,23 @@ def test_dropin_countgauss_apply_matches_reference_library(values):
     c = json.loads(subprocess.run([_bin("dropin_bench_cpu")] + args, capture_output=True, text=True, timeout=300,
                                   check=True).stdout.strip().splitlines()[-1])
     assert abs(g["z_abs_sum"] - c["z_abs_sum"]) <= 1e-12 * abs(c["z_abs_sum"])
+
+
+@pytest.mark.parametrize("devices", ["0,0", "0,0,0"])
+@pytest.mark.parametrize("cfg", ["c1", "c3s"])
+def test_dropin_spans_a_device_group(cfg, devices):
+    """CGX_DEVICES: cg::countgauss_apply on a seeded transform runs row-sharded over a device
+    group (here ranks sharing device 0, so the combine is the peer-memory one), and must agree
+    with the reference library like the single-GPU drop-in does."""
+    args = [cfg, "2"]
+    env = dict(os.environ, CGX_DEVICES=devices, CGX_SHIM_TRACE="1")
+    run = subprocess.run([_bin("dropin_bench_gpu")] + args, capture_output=True, text=True, timeout=300, check=True,
+                         env=env)
+    assert f"over {len(devices.split(','))} ranks" in run.stderr
+    g = json.loads(run.stdout.strip().splitlines()[-1])
+    c = json.loads(subprocess.run([_bin("dropin_bench_cpu")] + args, capture_output=True, text=True, timeout=300,
+                                  check=True).stdout.strip().splitlines()[-1])
+    assert abs(g["z_abs_sum"] - c["z_abs_sum"]) <= 1e-12 * abs(c["z_abs_sum"])
+    one = json.loads(subprocess.run([_bin("dropin_bench_gpu")] + args, capture_output=True, text=True, timeout=300,
+                                    check=True).stdout.strip().splitlines()[-1])
+    assert g["z_abs_sum"] != 0 and abs(g["z_abs_sum"] - one["z_abs_sum"]) <= 1e-12 * abs(one["z_abs_sum"])
