@@ -356,6 +356,10 @@ void sketch_csr_dev(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, co
     const void* vp = vals;
     (void)es;
     stage_csr(ctx, &rp, &cp, &idx_type, &vp, &dtype, n, nnz, x_mem, s);
+    if (ctx->csr_base) {  // offsets count from the caller's element 0: rebase the array pointers instead
+        cp = (const char*)cp - (idx_type == CGX_I32 ? 4 : 8) * ctx->csr_base;
+        vp = (const char*)vp - (int64_t)dsize(dtype) * ctx->csr_base;
+    }
     ctx->prof.begin(0, s);
     const int64_t chunk_rows = csr_chunk_rows(n, xf->B, d);
     const bool records = chunk_rows == 0 && csr_atomic_applies(ctx, xf, n, d, nnz, dtype);

@@ -686,39 +686,39 @@ int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int6
         if (d < 1 || nnz < 0) fail(CGX_EINVAL, "cgx_group: bad CSR sizes");
         if (!rowptr || rowptr[0] != 0 || rowptr[n] != nnz) fail(CGX_EINVAL, "cgx_group: row offsets must run 0..nnz");
         const size_t is = idx_type == CGX_I32 ? 4 : 8, vs = dtype == CGX_F32 ? 4 : 8;
-        // the shard's row offsets, rebased to its own nonzeros; its nonzeros stay in the
-        // caller's host arrays and are staged by the apply (pipelined, narrowed)
-        auto rebase = [&](int p, std::vector<int64_t>& rp, int64_t* rows, int64_t* q0, int64_t* q1) {
-            const int64_t r0 = t->r0[(size_t)p];
-            *rows = t->r1[(size_t)p] - r0;
-            *q0 = rowptr[r0];
-            *q1 = rowptr[r0 + *rows];
-            rp.resize((size_t)(*rows + 1));
-            for (int64_t i = 0; i <= *rows; ++i) rp[(size_t)i] = rowptr[r0 + i] - *q0;
+        // Rank p's shard: its row offsets as they stand in the caller's array (ctx->csr_base tells
+        // the kernels they count from the caller's element 0 -- copying and rebasing 8 B per row
+        // on the host cost c3 more than its whole apply), its nonzeros the part of cols / vals
+        // from rowptr[r0] on; all staged by the apply (pipelined, narrowed).
+        struct Base {  // csr_base only around this rank's call
+            cgx_ctx* c;
+            Base(cgx_ctx* cc, int64_t b) : c(cc) { c->csr_base = b; }
+            ~Base() { c->csr_base = 0; }
         };
         if (combine == CGX_COMBINE_P2P) {
             apply_p2p(g, t, d, [&](int p, cgx_ctx* c, cgx_xform* xf, double* out) {
-                std::vector<int64_t> rp;
-                int64_t rows, q0, q1;
-                rebase(p, rp, &rows, &q0, &q1);
-                ok_or_throw(cgx_countsketch_apply_csr(c, xf, rp.data(), (const char*)cols + is * (size_t)q0, idx_type,
+                const int64_t r0 = t->r0[(size_t)p], rows = t->r1[(size_t)p] - r0;
+                const int64_t q0 = rowptr[r0], q1 = rowptr[r0 + rows];
+                Base base(c, q0);
+                ok_or_throw(cgx_countsketch_apply_csr(c, xf, rowptr + r0, (const char*)cols + is * (size_t)q0, idx_type,
                                                       (const char*)vals + vs * (size_t)q0, dtype, rows, d, q1 - q0,
                                                       CGX_MEM_HOST, out, CGX_ROW_MAJOR, CGX_MEM_DEVICE, nullptr));
             }, z, z_mem, (double* const*)z);
             return;
         }
         each_rank(g, [&](int p) {
-            std::vector<int64_t> rp;
-            int64_t rows, q0, q1;
-            rebase(p, rp, &rows, &q0, &q1);
+            const int64_t r0 = t->r0[(size_t)p], rows = t->r1[(size_t)p] - r0;
+            const int64_t q0 = rowptr[r0], q1 = rowptr[r0 + rows];
+            const int64_t* rpp = rowptr + r0;
             const void* cp = (const char*)cols + is * (size_t)q0;
             const void* vp = (const char*)vals + vs * (size_t)q0;
+            Base base(g->ctx[(size_t)p], q0);
             partial_rank(g, t, p, d, combine, [&](cgx_ctx* c, cgx_xform* xf, double* out, bool both) {
                 if (both)
-                    ok_or_throw(cgx_countgauss_apply_csr(c, xf, rp.data(), cp, idx_type, vp, dtype, rows, d, q1 - q0,
+                    ok_or_throw(cgx_countgauss_apply_csr(c, xf, rpp, cp, idx_type, vp, dtype, rows, d, q1 - q0,
                                                          CGX_MEM_HOST, out, CGX_MEM_DEVICE, nullptr));
                 else
-                    ok_or_throw(cgx_countsketch_apply_csr(c, xf, rp.data(), cp, idx_type, vp, dtype, rows, d, q1 - q0,
+                    ok_or_throw(cgx_countsketch_apply_csr(c, xf, rpp, cp, idx_type, vp, dtype, rows, d, q1 - q0,
                                                           CGX_MEM_HOST, out, CGX_ROW_MAJOR, CGX_MEM_DEVICE, nullptr));
             });
             combine_rank(g, t, p, d, combine, z, z_mem, (double* const*)z);

@@ -121,6 +121,10 @@ struct cgx_ctx {
     const cgx::OutSegs* out_segs = nullptr;
     cgx::DevBuf seg_local;
     int64_t seg_fused = 0, seg_copied = 0;  // stage-1 calls of each kind (cgx_group_stats)
+    // Set by group.cu around a CSR call on a row shard: the shard's row offsets are passed as
+    // they stand in the caller's array (rowptr + row0), i.e. they index the caller's whole
+    // cols/vals arrays, of which the call receives the part starting at element csr_base.
+    int64_t csr_base = 0;
     const double* oz_colmax_for = nullptr;  // S.X whose column maxima the sketch left in oz_b
     int64_t oz_colmax_d = 0;         // ozgemm.cu scratch: scales, digit images of G and S.X
 };
