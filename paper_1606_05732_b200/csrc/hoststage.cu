@@ -232,7 +232,12 @@ const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, 
     HostPool& pool = pool_of(ctx);
     char* dfull = nullptr;                 // allocated when some chunk goes at full width
     char* dhalf = kind ? (char*)half.get(bytes / 2) : nullptr;
-    const size_t per_chunk = kChunk / esize;  // elements per chunk
+    // elements per chunk: a ring slot's worth for long arrays; a mid-sized array (up to a few
+    // slots) goes in ~8 smaller chunks, or its one or two big chunks would be filled and then
+    // copied with next to no overlap
+    size_t chunk_bytes = kChunk;
+    if (bytes < 4 * kChunk) chunk_bytes = std::min(kChunk, std::max<size_t>((size_t)2 << 20, (bytes / 4 + 0xfffff) & ~(size_t)0xfffff));
+    const size_t per_chunk = chunk_bytes / esize;
     const size_t nchunks = (count + per_chunk - 1) / per_chunk;
     std::vector<char> chunk_narrow(nchunks, 0);
     bool try_narrow = kind != 0;
