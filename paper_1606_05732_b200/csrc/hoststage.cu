@@ -346,10 +346,10 @@ const void* stage_in(cgx_ctx* ctx, DevBuf& full, DevBuf& half, const void* src, 
 }
 
 // 64-bit content checksum of a host array (the drop-in shim's check that a transform's
-// public fields still hold what construction put there).  Per 1 MiB block a multiply-mix
+// public fields still hold what construction put there).  Per 64 KiB block a multiply-mix
 // hash of its 8-byte words, combined in block order: independent of the thread count.
 uint64_t host_checksum(cgx_ctx* ctx, const void* p, size_t bytes) {
-    const size_t blk = (size_t)1 << 20;
+    const size_t blk = (size_t)64 << 10;
     const size_t nb = (bytes + blk - 1) / blk;
     std::vector<uint64_t> part(nb);
     auto body = [&](size_t b) {
@@ -367,7 +367,7 @@ uint64_t host_checksum(cgx_ctx* ctx, const void* p, size_t bytes) {
         for (; i < len; ++i) h = (h ^ q[i]) * 0x100000001B3ULL;
         part[b] = fin64(h ^ fin64(h2 + len));
     };
-    if (ctx && bytes >= ((size_t)4 << 20)) {
+    if (ctx && bytes >= ((size_t)256 << 10)) {
         HostPool& pool = pool_of(ctx);
         pool.set_spin(bytes < ((size_t)16 << 20));
         const int T = pool.size();
