@@ -312,6 +312,30 @@ int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int6
                                    int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
                                    double* z, int z_mem, int combine);
 
+/* ---- the peer-memory combine for one process per GPU (torchrun-style launches) -----------
+ * The pieces of CGX_COMBINE_P2P as separate calls, for callers whose ranks are processes: each
+ * rank allocates its landing buffer (cgx_device_alloc), exports it (cgx_ipc_export: a 64-byte
+ * CUDA IPC handle to pass to the other ranks by any host channel), opens the others'
+ * (cgx_ipc_open; on NVLink-connected GPUs the mapping is a peer mapping), and runs its sketch
+ * with cgx_countsketch_apply_*_to: bucket b's finished row goes to bases[b / per] +
+ * (b % per) * d -- the kernels that can, store there directly; the others sketch locally and
+ * copy the ranges (as in CGX_COMBINE_P2P).  After the ranks have synchronized on the host, each
+ * sums its slots in rank order with cgx_sum_slots and runs cgx_gauss_gemm_range on the result
+ * (paper_1606_05732_b200/distributed.py, combine "p2p"). */
+#define CGX_IPC_HANDLE_BYTES 64
+int cgx_ipc_export(cgx_ctx* ctx, const void* dev_ptr, unsigned char* handle /* [CGX_IPC_HANDLE_BYTES] */);
+int cgx_ipc_open(cgx_ctx* ctx, const unsigned char* handle, void** dev_ptr);
+int cgx_ipc_close(cgx_ctx* ctx, void* dev_ptr);
+int cgx_countsketch_apply_dense_to(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
+                                   int64_t n, int64_t d, int x_mem, double* const* bases, int nseg, int64_t per,
+                                   void* stream);
+int cgx_countsketch_apply_csr_to(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols,
+                                 int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem,
+                                 double* const* bases, int nseg, int64_t per, void* stream);
+/* out[i] = ((slot_0[i] + slot_1[i]) + ...) for i < count; slot q starts at slots + q * stride. */
+int cgx_sum_slots(cgx_ctx* ctx, const double* slots, int nslots, int64_t stride, int64_t count, double* out,
+                  void* stream);
+
 /* ---- instrumentation ---------------------------------------------------------------- */
 /* Context options (kernel variants for A/B runs; every variant gives the same S.X bits and
  * Z to rounding -- "oz_slices" below 7 trades Z accuracy for speed, as stated):

@@ -74,6 +74,12 @@ SIGNATURES = {
     "cgx_group_init": (_I, [_I, _P, _P]),
     "cgx_group_stats": (_I, [_P, _P, _P]),
     "cgx_group_supports": (_I, [_P, _I]),
+    "cgx_ipc_export": (_I, [_P, _P, _P]),
+    "cgx_ipc_open": (_I, [_P, _P, _P]),
+    "cgx_ipc_close": (_I, [_P, _P]),
+    "cgx_countsketch_apply_dense_to": (_I, [_P, _P, _P, _I, _I, _I64, _I64, _I64, _I, _P, _I, _I64, _P]),
+    "cgx_countsketch_apply_csr_to": (_I, [_P, _P, _P, _P, _I, _P, _I, _I64, _I64, _I64, _I, _P, _I, _I64, _P]),
+    "cgx_sum_slots": (_I, [_P, _P, _I, _I64, _I64, _P, _P]),
     "cgx_group_free": (_I, [_P]),
     "cgx_group_size": (_I, [_P]),
     "cgx_group_context": (_I, [_P, _I, _P]),

@@ -608,6 +608,36 @@ def countsketch_apply_into(cs, x, sx):
     return sx
 
 
+def countsketch_apply_to(cs, x, bases, per: int):
+    """countsketch_apply with the finished rows stored by bucket range into caller-supplied
+    device destinations: bucket b's row goes to ``bases[b // per] + (b % per) * d`` (doubles).
+    `bases` are device addresses (ints), e.g. this rank's slots in the other ranks' landing
+    buffers (distributed.PeerLanding).  Device inputs; stream-ordered."""
+    if isinstance(cs, CountGaussTransform):
+        cs = cs.cs
+    xf = cs._xf
+    arr = (C.c_void_p * len(bases))(*bases)
+    if isinstance(x, SparseMatrix):
+        rp, ci, it, v, dt, mem, keep, dev = _csr_args(x)
+        if not dev:
+            raise ValueError("countsketch_apply_to: device inputs only")
+        check(lib.cgx_countsketch_apply_csr_to(xf.ctx.h, xf.h, rp, ci, it, v, dt, x.rows, x.cols, x.nnz(), mem,
+                                               arr, len(bases), per, _stream_of(x.values)))
+        return
+    ptr, dt, layout, ld, n, d, mem, keep, dev = _dense_args(x)
+    if not dev:
+        raise ValueError("countsketch_apply_to: device inputs only")
+    check(lib.cgx_countsketch_apply_dense_to(xf.ctx.h, xf.h, ptr, dt, layout, ld, n, d, mem, arr, len(bases), per,
+                                             _stream_of(keep)))
+
+
+def sum_slots(ctx: Context, slots_ptr: int, nslots: int, stride: int, count: int, out):
+    """out[i] = ((slot_0[i] + slot_1[i]) + ...) for i < count (rank order); `out` a CUDA tensor."""
+    check(lib.cgx_sum_slots(ctx.h, C.c_void_p(slots_ptr), nslots, stride, count, C.c_void_p(out.data_ptr()),
+                            _stream_of(out)))
+    return out
+
+
 def _sx_rows_args(sx):
     """Row-major float64 S.X (numpy or CUDA torch): (ptr, d, mem, keepalive, is_torch)."""
     if _is_torch(sx):

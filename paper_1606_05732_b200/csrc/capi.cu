@@ -565,6 +565,36 @@ int cgx_device_free(cgx_ctx* ctx, void* p) {
         CGX_CUDA(cudaFree(p));
     });
 }
+// ---- peer memory across processes (one process per GPU): CUDA IPC ------------------------
+int cgx_ipc_export(cgx_ctx* ctx, const void* p, unsigned char* handle) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!p || !handle) fail(CGX_EINVAL, "cgx_ipc_export: null argument");
+        static_assert(sizeof(cudaIpcMemHandle_t) == CGX_IPC_HANDLE_BYTES, "CUDA IPC handle size");
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        cudaIpcMemHandle_t h;
+        CGX_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(p)));
+        std::memcpy(handle, &h, sizeof h);
+    });
+}
+int cgx_ipc_open(cgx_ctx* ctx, const unsigned char* handle, void** out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!out || !handle) fail(CGX_EINVAL, "cgx_ipc_open: null argument");
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        CGX_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+int cgx_ipc_close(cgx_ctx* ctx, void* p) {
+    return guard([&] {
+        need_ctx(ctx);
+        CGX_CUDA(cudaSetDevice(ctx->device));
+        CGX_CUDA(cudaIpcCloseMemHandle(p));
+    });
+}
+
 int cgx_host_alloc(cgx_ctx* ctx, size_t bytes, void** out) {
     return guard([&] {
         need_ctx(ctx);
@@ -900,6 +930,66 @@ int cgx_countsketch_apply_csr(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* 
         sketch_csr_dev(ctx, xf, rowptr, cols, idx_type, vals, dtype, n, d, nnz, x_mem, sxd, sc.st);
         place_sx(ctx, xf, sxd, d, sx, sx_layout, sx_mem, sc);
         if (x_mem == CGX_MEM_HOST) sc.sync();
+    });
+}
+
+// countsketch_apply with the finished S.X rows stored by bucket range into caller-supplied
+// destinations (peer-mapped landing slots): the stage 1 of CGX_COMBINE_P2P for callers that run
+// one process per GPU (distributed.py "p2p").
+namespace {
+struct SegScope {
+    cgx_ctx* ctx;
+    OutSegs segs{};
+    SegScope(cgx_ctx* c, const cgx_xform* xf, double* const* bases, int nseg, int64_t per) : ctx(c) {
+        if (!bases || nseg < 1 || nseg > kMaxSegs || per < 1 || per * nseg < xf->B)
+            fail(CGX_EINVAL, "cgx_countsketch_apply_*_to: need 1..8 destinations covering all buckets");
+        for (int q = 0; q < nseg; ++q) {
+            if (!bases[q]) fail(CGX_EINVAL, "cgx_countsketch_apply_*_to: null destination");
+            segs.base[q] = bases[q];
+        }
+        segs.per = (uint32_t)per;
+        ctx->out_segs = &segs;
+    }
+    ~SegScope() { ctx->out_segs = nullptr; }
+};
+} // namespace
+
+int cgx_countsketch_apply_dense_to(cgx_ctx* ctx, const cgx_xform* xf, const void* x, int dtype, int layout, int64_t ld,
+                                   int64_t n, int64_t d, int x_mem, double* const* bases, int nseg, int64_t per,
+                                   void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(x_mem);
+        CallScope sc(ctx, stream);
+        SegScope seg(ctx, xf, bases, nseg, per);
+        sketch_dense_dev(ctx, xf, x, dtype, layout, ld, n, d, x_mem, seg.segs.base[0], sc.st);
+        if (x_mem == CGX_MEM_HOST) sc.sync();
+    });
+}
+
+int cgx_countsketch_apply_csr_to(cgx_ctx* ctx, const cgx_xform* xf, const int64_t* rowptr, const void* cols,
+                                 int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz, int x_mem,
+                                 double* const* bases, int nseg, int64_t per, void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        need_xf(xf);
+        need_mem(x_mem);
+        CallScope sc(ctx, stream);
+        SegScope seg(ctx, xf, bases, nseg, per);
+        sketch_csr_dev(ctx, xf, rowptr, cols, idx_type, vals, dtype, n, d, nnz, x_mem, seg.segs.base[0], sc.st);
+        if (x_mem == CGX_MEM_HOST) sc.sync();
+    });
+}
+
+int cgx_sum_slots(cgx_ctx* ctx, const double* slots, int nslots, int64_t stride, int64_t count, double* out,
+                  void* stream) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!slots || !out || nslots < 1 || stride < count || count < 0)
+            fail(CGX_EINVAL, "cgx_sum_slots: bad arguments");
+        CallScope sc(ctx, stream);
+        launch_sum_slots(ctx, slots, nslots, stride, count, out, sc.st);
     });
 }
 

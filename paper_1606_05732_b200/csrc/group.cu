@@ -205,8 +205,10 @@ private:
     uint64_t gen_ = 0;
 };
 
+} // namespace
+
 // out[i] = ((slot_0[i] + slot_1[i]) + slot_2[i]) + ... for i < count; slots `stride` apart.
-__global__ void sum_slots(const double* __restrict__ slots, int P, int64_t stride, int64_t count,
+__global__ void sum_slots_kernel(const double* __restrict__ slots, int P, int64_t stride, int64_t count,
                           double* __restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
         double a = slots[i];
@@ -219,12 +221,10 @@ void launch_sum_slots(cgx_ctx* c, const double* slots, int P, int64_t stride, in
                       cudaStream_t st) {
     if (count <= 0) return;
     const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)c->num_sms * 16);
-    sum_slots<<<(unsigned)blocks, 256, 0, st>>>(slots, P, stride, count, out);
+    sum_slots_kernel<<<(unsigned)blocks, 256, 0, st>>>(slots, P, stride, count, out);
     c->launches++;
     CGX_CUDA(cudaGetLastError());
 }
-
-} // namespace
 } // namespace cgx
 
 struct cgx_group {

@@ -198,6 +198,9 @@ void launch_transpose_sx(cgx_ctx* ctx, const double* src, int64_t B, int64_t d, 
 // sketch_dense.cu / sketch_csr.cu: whether the launch below stores straight into ctx->out_segs
 bool sketch_dense_fuses_segs(const cgx_ctx* ctx, const void* x, int dtype, int64_t ld, int64_t d);
 bool sketch_csr_fuses_segs(const cgx_ctx* ctx, int64_t d, int64_t chunk_rows);
+// group.cu: out[i] = ((slot_0[i] + slot_1[i]) + ...) for i < count, slots `stride` doubles apart
+void launch_sum_slots(cgx_ctx* c, const double* slots, int P, int64_t stride, int64_t count, double* out,
+                      cudaStream_t st);
 // capi.cu: rows [q*per, (q+1)*per) of a local row-major S.X -> segs.base[q] (device-to-device copies)
 void push_segs(cgx_ctx* ctx, const double* sx, int64_t B, int64_t d, const OutSegs& segs, cudaStream_t s);
 

@@ -19,6 +19,14 @@ T.X is linear, so the partials combine after either stage:
   the result is the same bits on every rank and does not depend on the collective's algorithm
   or on timing.  This is the arithmetic of the C ABI's CGX_COMBINE_P2P (csrc/group.cu), where
   the exchange is fused into the sketch kernels' stores over peer memory; same volume as "sx".
+* ``"p2p"``: "sxo" with the exchange of S.X fused into the sketch kernels: every rank owns a
+  landing buffer of P slots shared with the others through CUDA IPC (`PeerLanding`), and a
+  rank's sketch stores each finished bucket row straight into its slot in the owner's buffer
+  over the peer mapping (api.countsketch_apply_to; NVLink stores on a multi-GPU node).  After a
+  host barrier the owner sums its slots in rank order (api.sum_slots), runs stage 2 on its
+  range, and the partial Z's are gathered and summed in rank order.  Same bits as "sxo".  The
+  barrier is on the host (stream sync + `dist.barrier`): a device-side arrival flag would save
+  its latency but makes kernels wait on other GPUs' kernels, which a one-GPU test cannot do.
 * ``"g"``: the partial sketches are all-reduced (every rank holds the summed S.X), rank p
   computes rows [r_p, r_{p+1}) of Z = G[r_p:r_{p+1}, :] . S.X (cgx_gauss_gemm_rows: the
   m rows of G split across ranks, stage 2 divided by P with no further reduction), and the
@@ -146,6 +154,96 @@ def combine(mode: str, *, world: int, rank: int, B: int, d: int, partial_sx=None
         return _ordered_sum(parts)
     dist.all_reduce(z, group=group)
     return z
+
+
+class PeerLanding:
+    """Rank-local landing buffer for the "p2p" combine and the peer mappings of everyone
+    else's: `world` slots of ceil(B/world) x d doubles; slot q of rank p's buffer receives rank
+    q's partial rows of p's bucket range.  Collective: every rank constructs it together."""
+
+    def __init__(self, ctx, world: int, rank: int, B: int, d: int, group=None):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from ._lib import lib
+
+        self.ctx, self.world, self.rank, self.B, self.d = ctx, world, rank, B, d
+        self.per = (B + world - 1) // world
+        self.slot = self.per * d  # doubles per slot
+        p = C.c_void_p()
+        _check(lib.cgx_device_alloc(ctx.h, 8 * self.slot * world, C.byref(p)))
+        self.mine = p.value
+        h = (C.c_ubyte * 64)()
+        _check(lib.cgx_ipc_export(ctx.h, p, h))
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self.peer = []
+        for q in range(world):
+            if q == rank:
+                self.peer.append(self.mine)
+                continue
+            o = C.c_void_p()
+            hb = (C.c_ubyte * 64).from_buffer_copy(handles[q])
+            _check(lib.cgx_ipc_open(ctx.h, hb, C.byref(o)))
+            self.peer.append(o.value)
+        # where this rank's rows of bucket range q go: its slot in rank q's buffer
+        self.bases = [self.peer[q] + 8 * self.slot * rank for q in range(world)]
+        self._group = group
+
+    def close(self):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from ._lib import lib
+
+        if self.mine is None:
+            return
+        self.ctx.synchronize()
+        dist.barrier(group=self._group)  # nobody still writes into a buffer about to go
+        for q, ptr in enumerate(self.peer):
+            if q != self.rank:
+                lib.cgx_ipc_close(self.ctx.h, C.c_void_p(ptr))
+        dist.barrier(group=self._group)
+        lib.cgx_device_free(self.ctx.h, C.c_void_p(self.mine))
+        self.mine = None
+
+
+def _check(rc):
+    if rc != 0:
+        from ._lib import lib
+
+        raise RuntimeError(lib.cgx_last_error().decode())
+
+
+def combine_p2p(landing: "PeerLanding", sketch_to, stage2, *, m: int, group=None):
+    """The "p2p" combine.  sketch_to(bases, per) runs this rank's sketch with segmented
+    destinations (api.countsketch_apply_to); stage2(sx_slice, b0, b1) -> Z_p (m x d) as in "sx".
+    Returns Z (m x d), the same bits on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    L = landing
+    sketch_to(L.bases, L.per)
+    L.ctx.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier(group=group)  # every rank's rows have landed
+    b0 = min(L.B, L.rank * L.per)
+    b1 = min(L.B, b0 + L.per)
+    if b1 > b0:
+        sl = torch.empty((b1 - b0, L.d), dtype=torch.float64, device="cuda")
+        api.sum_slots(L.ctx, L.mine, L.world, L.slot, (b1 - b0) * L.d, sl)
+        z = stage2(sl, b0, b1)
+    else:
+        z = torch.zeros((L.d, m), dtype=torch.float64, device="cuda").t()
+    zc = z.contiguous()
+    parts = torch.empty((L.world,) + tuple(zc.shape), dtype=zc.dtype, device=zc.device)
+    # the gather also orders the next step's stores after this step's slot sums on every rank
+    dist.all_gather_into_tensor(parts.view(L.world * zc.shape[0], zc.shape[1]), zc, group=group)
+    return _ordered_sum(parts)
 
 
 def _ordered_sum(parts):
