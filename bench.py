@@ -422,7 +422,9 @@ def run_ours(args):
     zbuf = torch.empty((d, m), dtype=torch.float64, device=dev)  # contiguous storage of Z^T
     z = zbuf.t()  # column-major m x d view (the reference layout)
 
-    from paper_1606_05732_b200.distributed import combine
+    from paper_1606_05732_b200.distributed import PeerLanding, combine, combine_p2p
+
+    landing = PeerLanding(ctx, world, rank, B, d) if world > 1 and args.combine == "p2p" else None
 
     sxbuf = torch.empty((B, d), dtype=torch.float64, device=dev) if world > 1 and args.combine in ("sx", "sxo", "g") else None
     sxT = torch.empty((d, B), dtype=torch.float64, device=dev) if world > 1 and args.combine == "cols" else None
@@ -445,6 +447,13 @@ def run_ours(args):
                 if e0 is not None:
                     comb_ev.append((e0, mark()))
             return z
+        if args.combine == "p2p":  # the sketch stores its rows into the owners' landing slots (peer memory)
+            e0 = mark()
+            out = combine_p2p(landing, lambda bases, per: cg.api.countsketch_apply_to(t, x, bases, per),
+                              lambda sl, b0, b1: cg.api.gauss_gemm_range(t, sl, b0, b1), m=m)
+            if e0 is not None:
+                comb_ev.append((e0, mark()))
+            return out
         if args.combine == "cols":
             cg.api.countsketch_apply_into(t, x, sxT.t())  # partial S.X, column-major
             e0 = mark()
@@ -674,6 +683,7 @@ def run_ours(args):
                 "parallelism": f"rows sharded x{world} ({args.scaling} scaling: "
                 + ("the config's n rows per rank" if args.scaling == "weak" else "the config's n rows split across ranks")
                 + ")" + ({"z": ", NCCL all-reduce of Z", "sx": ", NCCL reduce-scatter of S.X + split-K stage 2 + all-reduce of Z",
+                       "p2p": ", sketch kernels store S.X rows into the owners' landing buffers over peer memory (CUDA IPC), host barrier, slot sums in rank order + split-K stage 2 + all-gather of Z summed in rank order",
                        "sxo": ", NCCL all-to-all of S.X bucket ranges summed in rank order + split-K stage 2 + all-gather of Z summed in rank order",
                        "g": ", NCCL all-reduce of S.X + G's m rows split over ranks + all-gather of Z",
                        "cols": ", NCCL column reduce-scatter of S.X + split-N stage 2 + all-gather of Z"}[args.combine]
@@ -707,6 +717,8 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        if landing is not None:
+            landing.close()
         dist.destroy_process_group()
     return 0
 
@@ -729,9 +741,9 @@ def main():
     ap.add_argument("--placement", default="rows", choices=["rows", "hash"],
                     help="rows: contiguous row shards; hash: each rank holds the rows hashing into its bucket "
                          "range, in bucket order (SURVEY 8e ablation C; dense configs; combine = all-reduce of Z)")
-    ap.add_argument("--combine", default="auto", choices=["auto", "z", "sx", "sxo", "g", "cols"],
+    ap.add_argument("--combine", default="auto", choices=["auto", "z", "sx", "sxo", "p2p", "g", "cols"],
                     help="N>1 combine (auto: g for dense configs, sx for CSR -- the north star's schemes): z = all-reduce of Z; sx = reduce-scatter of S.X + split-K stage 2 + "
-                         "all-reduce; sxo = sx with all-to-all / all-gather and sums in rank order (same bits on every rank); g = all-reduce of S.X + G's m rows split over ranks + all-gather; "
+                         "all-reduce; sxo = sx with all-to-all / all-gather and sums in rank order (same bits on every rank); p2p = sxo with the S.X exchange fused into the sketch kernels' stores over peer memory (CUDA IPC landing buffers; host barrier per step); g = all-reduce of S.X + G's m rows split over ranks + all-gather; "
                          "cols = column reduce-scatter of S.X + split-N stage 2 + all-gather")
     args = ap.parse_args()
     if args.combine == "auto":
