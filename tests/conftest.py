@@ -12,6 +12,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the sm_100a kernels)")
     config.addinivalue_line("markers", "slow: full BASELINE-size case")
+    config.addinivalue_line("markers", "timeout: per-test limit (pytest-timeout; a no-op without the plugin)")
 
 
 @pytest.fixture(scope="session")

@@ -12,7 +12,7 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
 
 SHAPES = {
     "dense": (300001, 32, 4099, 24),      # cp.async gather stores into the peers' slots
