@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <initializer_list>
 #include <new>
 #include <numeric>
 #include <stdexcept>
@@ -137,6 +138,43 @@ struct CallScope {
     ~CallScope() { cudaEventRecord(ctx->done, st); }
     void sync() { CGX_CUDA(cudaStreamSynchronize(st)); }
 };
+
+// Small results the host reads back (Z, a small S.X, the hash/sign fields of a small map): a
+// cudaMemcpyAsync into pageable memory goes through the driver's own staging and costs ~12 us
+// a call -- a third of a tiny apply -- so up to kSmallPin bytes come back through a pinned
+// bounce buffer instead: one async copy, the stream sync the call needs anyway, a memcpy.
+// `pieces`: consecutive device ranges -> their host destinations.
+constexpr size_t kSmallPin = (size_t)256 << 10;
+struct HostPiece {
+    void* dst;
+    size_t bytes;
+};
+void d2h_sync(cgx_ctx* ctx, const void* src_dev, std::initializer_list<HostPiece> pieces, CallScope& sc) {
+    size_t total = 0;
+    for (const HostPiece& p : pieces) total += p.bytes;
+    if (total <= kSmallPin && !ctx->small_pin) {
+        if (cudaMallocHost((void**)&ctx->small_pin, kSmallPin) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->small_pin = nullptr;
+        }
+    }
+    if (total <= kSmallPin && ctx->small_pin) {
+        CGX_CUDA(cudaMemcpyAsync(ctx->small_pin, src_dev, total, cudaMemcpyDeviceToHost, sc.st));
+        sc.sync();
+        size_t off = 0;
+        for (const HostPiece& p : pieces) {
+            if (p.dst) std::memcpy(p.dst, ctx->small_pin + off, p.bytes);
+            off += p.bytes;
+        }
+        return;
+    }
+    size_t off = 0;
+    for (const HostPiece& p : pieces) {
+        if (p.dst) CGX_CUDA(cudaMemcpyAsync(p.dst, (const char*)src_dev + off, p.bytes, cudaMemcpyDeviceToHost, sc.st));
+        off += p.bytes;
+    }
+    sc.sync();
+}
 
 void need_ctx(cgx_ctx* ctx) {
     if (!ctx) fail(CGX_EINVAL, "cgx: null context");
@@ -397,10 +435,7 @@ void finish_gemm(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_dev, int64_
     ctx->prof.begin(1, sc.st);
     launch_gauss_gemm(ctx, xf, sx_dev, b0, b1, d, zd, sc.st);
     ctx->prof.end(1, sc.st);
-    if (z_mem == CGX_MEM_HOST) {
-        CGX_CUDA(cudaMemcpyAsync(z, zd, zb, cudaMemcpyDeviceToHost, sc.st));
-        sc.sync();
-    }
+    if (z_mem == CGX_MEM_HOST) d2h_sync(ctx, zd, {{z, zb}}, sc);
 }
 
 void place_sx(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_dev, int64_t d, double* sx, int sx_layout, int sx_mem,
@@ -419,8 +454,7 @@ void place_sx(cgx_ctx* ctx, const cgx_xform* xf, const double* sx_dev, int64_t d
         if (src != sx) CGX_CUDA(cudaMemcpyAsync(sx, src, bytes, cudaMemcpyDeviceToDevice, sc.st));
         return;
     }
-    CGX_CUDA(cudaMemcpyAsync(sx, src, bytes, cudaMemcpyDeviceToHost, sc.st));
-    sc.sync();
+    d2h_sync(ctx, src, {{sx, bytes}}, sc);
 }
 
 void build_explicit(cgx_ctx* ctx, cgx_xform* xf, const int64_t* hash, const double* sign, int mem, CallScope& sc) {
@@ -501,6 +535,7 @@ int cgx_free(cgx_ctx* ctx) {
             b->release();
         for (auto& kv : ctx->pool_class) cudaFree(kv.first);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        if (ctx->small_pin) cudaFreeHost(ctx->small_pin);
         for (auto& b : ctx->hin) b.release();
         host_pool_free(ctx);
         for (int s = 0; s < 2; ++s)
@@ -850,15 +885,20 @@ int cgx_fill_hash_sign(cgx_ctx* ctx, const cgx_xform* xf, int64_t* hash, double*
         const size_t hb = sizeof(int64_t) * (size_t)xf->n, sb = sizeof(double) * (size_t)xf->n;
         int64_t* hd = hash;
         double* sd = sign;
+        char* both = nullptr;
         if (mem == CGX_MEM_HOST) {
-            hd = hash ? (int64_t*)ctx->xstage.get(hb + sb) : nullptr;
-            sd = sign ? (double*)((char*)ctx->xstage.get(hb + sb) + hb) : nullptr;
+            both = (char*)ctx->xstage.get(hb + sb);  // hash | sign, contiguous
+            hd = hash ? (int64_t*)both : nullptr;
+            sd = sign ? (double*)(both + hb) : nullptr;
         }
         launch_fill_hash_sign(ctx, xf, hd, sd, sc.st);
         if (mem == CGX_MEM_HOST) {
-            if (hash) CGX_CUDA(cudaMemcpyAsync(hash, hd, hb, cudaMemcpyDeviceToHost, sc.st));
-            if (sign) CGX_CUDA(cudaMemcpyAsync(sign, sd, sb, cudaMemcpyDeviceToHost, sc.st));
-            sc.sync();
+            if (hash && sign)
+                d2h_sync(ctx, both, {{hash, hb}, {sign, sb}}, sc);
+            else if (hash)
+                d2h_sync(ctx, hd, {{hash, hb}}, sc);
+            else if (sign)
+                d2h_sync(ctx, sd, {{sign, sb}}, sc);
         }
     });
 }

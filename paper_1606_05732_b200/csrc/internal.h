@@ -76,6 +76,7 @@ struct cgx_ctx {
     cgx::DevBuf gen_tables;                 // synthetic-input generator tables
     cgx::DevBuf gfull;                      // rows of G for the split-over-m stage 2 (gen_gauss_rows)
     cgx::DevBuf gchunk;                     // G super-chunk of the chunked stage 2 (dgemm.cu)
+    char* small_pin = nullptr;              // pinned bounce buffer for small results read back by the host
     void* pinned = nullptr;                 // pinned staging for pageable host inputs
     size_t pinned_bytes = 0;
     cgx::Profile prof;
