@@ -157,6 +157,44 @@ __global__ void fill_hash_sign_kernel(const uint32_t* perm, const uint32_t* offs
     }
 }
 
+// Tiny maps (n, B <= kTinyMax: distcheck's Monte-Carlo trials build hundreds of thousands of
+// them) in ONE launch of one CTA instead of memset + count + scan + histogram + scan + scatter:
+// bucket counts by shared-memory atomics, their scan by thread 0, and a stable placement where
+// row i's rank inside its bucket is the number of earlier rows with the same bucket.  Same
+// perm / offsets as the radix path (rows of a bucket in ascending order).
+constexpr int kTinyMax = 1024;
+template <int MODE>
+__global__ void __launch_bounds__(kTinyMax) tiny_perm(KeySrc src, int n, int B, uint32_t* __restrict__ perm,
+                                                       uint32_t* __restrict__ offsets) {
+    __shared__ uint32_t s_key[kTinyMax];
+    __shared__ uint32_t s_cnt[kTinyMax + 1];
+    const int tid = threadIdx.x;
+    for (int b = tid; b <= B; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    uint32_t key = 0, val = 0;
+    if (tid < n) {
+        load_item<MODE>(src, tid, key, val);
+        s_key[tid] = key;
+        atomicAdd(&s_cnt[key], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b <= B; ++b) {
+            const uint32_t c = s_cnt[b];
+            s_cnt[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int b = tid; b <= B; b += blockDim.x) offsets[b] = s_cnt[b];
+    if (tid < n) {
+        uint32_t rank = 0;
+        for (int j = 0; j < tid; ++j) rank += s_key[j] == key;
+        perm[s_cnt[key] + rank] = val;
+    }
+}
+
 int key_bits(int64_t B) {
     int bits = 0;
     while (bits < 63 && ((int64_t)1 << bits) < B) ++bits;  // bucket values are < B
@@ -166,6 +204,12 @@ int key_bits(int64_t B) {
 template <int MODE>
 void build_perm(cgx_ctx* ctx, cgx_xform* xf, KeySrc src, cudaStream_t s) {
     const int64_t n = xf->n, B = xf->B;
+    if (n <= kTinyMax && B <= kTinyMax) {
+        tiny_perm<MODE><<<1, kTinyMax, 0, s>>>(src, (int)n, (int)B, xf->perm, xf->offsets);
+        count_launch(ctx);
+        check_launch("tiny_perm");
+        return;
+    }
     // bucket offsets
     uint32_t* counts = (uint32_t*)ctx->counts.get(sizeof(uint32_t) * (size_t)(B + 1));
     CGX_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (size_t)(B + 1), s));
