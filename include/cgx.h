@@ -312,7 +312,8 @@ int cgx_group_countgauss_apply_csr(cgx_group* g, const cgx_gxform* t, const int6
                                    int idx_type, const void* vals, int dtype, int64_t n, int64_t d, int64_t nnz,
                                    double* z, int z_mem, int combine);
 
-/* ---- the peer-memory combine for one process per GPU (torchrun-style launches) -----------
+/* ---- the peer-memory combine for one process per GPU (torchrun-style launches; no reference
+ * counterpart -- the reference has no distributed code, PAPER.md:274-275 only names seed sharing)
  * The pieces of CGX_COMBINE_P2P as separate calls, for callers whose ranks are processes: each
  * rank allocates its landing buffer (cgx_device_alloc), exports it (cgx_ipc_export: a 64-byte
  * CUDA IPC handle to pass to the other ranks by any host channel), opens the others'
